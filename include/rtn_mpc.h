@@ -1,0 +1,112 @@
+/*
+ * rtn_mpc.h — C-ABI of the B200-native per-node MLP approximation path
+ * (Real-time Neural MPC, arXiv 2203.07747).
+ *
+ * This is the drop-in boundary for the reference's approximation interface:
+ *
+ *   std::vector<TaylorApprox> resmpc::PrepareNodes(const MlpModel&,
+ *       const Eigen::MatrixXd& node_features, int order, EvalCounters*);
+ *       -- /root/reference/proj/include/resmpc/taylor.hpp:27-29
+ *          /root/reference/proj/src/taylor.cpp:37-55
+ *   BatchEval resmpc::MlpBatchedEval(const MlpModel&, const Eigen::MatrixXd& z_rows,
+ *       EvalOrder, EvalCounters*);
+ *       -- /root/reference/proj/include/resmpc/neural.hpp:65-69
+ *          /root/reference/proj/src/neural.cpp:320-327
+ *
+ * The reference throws C++ exceptions; here each maps to one status code:
+ *   ConfigError      (proj/include/resmpc/errors.hpp:9-12)  -> RTN_ECONFIG
+ *   InputDomainError (proj/include/resmpc/errors.hpp:15-17) -> RTN_EDOMAIN
+ *   UnsupportedError (proj/include/resmpc/errors.hpp:20-22) -> RTN_EUNSUPPORTED
+ * No entry point aborts or throws; rtn_last_error() holds a thread-local message.
+ *
+ * Ownership/threading: a model handle is immutable and may be shared by any
+ * number of contexts (the reference's "immutable after loading; evaluation is
+ * reentrant", proj/include/resmpc/neural.hpp:17-18). A context owns one CUDA
+ * stream, its device workspace and pinned staging; it is single-threaded.
+ * Concurrent contexts are safe. The caller owns every host buffer.
+ *
+ * Layouts (row-major, fp64 on the host side, like the reference):
+ *   z    : K x n_in                     (row k = node k)
+ *   f    : K x n_out                    (BatchEval::values)
+ *   jac  : K x n_out x n_in             (BatchEval::jacobians[k](o, i))
+ *   hess : K x n_out x n_in x n_in      (BatchEval::hessians[k][o](a, b))
+ */
+#ifndef RTN_MPC_H_
+#define RTN_MPC_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rtn_model rtn_model; /* opaque, immutable, device-resident packed weights */
+typedef struct rtn_ctx rtn_ctx;     /* opaque, one stream + workspace */
+
+typedef enum {
+  RTN_OK = 0,
+  RTN_ECONFIG = 1,      /* ConfigError: bad shapes, file, order */
+  RTN_EDOMAIN = 2,      /* InputDomainError: feature dim mismatch, K out of range */
+  RTN_EUNSUPPORTED = 3, /* UnsupportedError: e.g. Hessians of a relu net */
+  RTN_ECUDA = 4,        /* CUDA runtime failure (or no sm_100 device) */
+  RTN_ENCCL = 5         /* reserved for the multi-GPU gather */
+} rtn_status;
+
+typedef enum {
+  RTN_TF32 = 0,   /* tcgen05 kind::tf32, fp32 accumulate (tolerance 1e-3)     */
+  RTN_3XTF32 = 1, /* split hi/lo operands, 3 tf32 MMAs per product (1e-5)      */
+  RTN_BF16 = 2    /* reserved */
+} rtn_precision;
+
+typedef enum { RTN_ACT_TANH = 0, RTN_ACT_RELU = 1, RTN_ACT_SILU = 2 } rtn_activation;
+
+/* Loads an RMLP v1 (proj/src/neural.cpp:685-755) or v2 (SiLU tag 2) file,
+ * folds the normalisation into the first/last layer and packs the weights
+ * into the device layout. Replaces resmpc::LoadModel (neural.hpp:117). */
+rtn_status rtn_model_load_rmlp(const char* path, int device, rtn_precision p, rtn_model** out);
+
+/* Same from in-memory arrays (resmpc::MlpModel fields, neural.hpp:19-34).
+ * W[l] is row-major sizes[l+1] x sizes[l]; b[l] has sizes[l+1] entries. */
+rtn_status rtn_model_from_arrays(const int* sizes, int n_sizes, int activation,
+                                 const double* const* W, const double* const* b,
+                                 const double* in_mean, const double* in_scale,
+                                 const double* out_mean, const double* out_scale, int device,
+                                 rtn_precision p, rtn_model** out);
+void rtn_model_free(rtn_model* m);
+
+/* n_in, n_out, number of weight layers, activation, padded hidden width. */
+rtn_status rtn_model_info(const rtn_model* m, int* n_in, int* n_out, int* n_layers,
+                          int* activation, int* padded_width);
+
+/* max_rows bounds K per call (device workspace is sized for it); max_order in
+ * {0,1,2}. latency_mode != 0 captures the launch in a CUDA graph per K. */
+rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order, int latency_mode,
+                          rtn_ctx** out);
+void rtn_ctx_free(rtn_ctx* c);
+
+/* The PrepareNodes / MlpBatchedEval equivalent: host z in, host f/jac(/hess)
+ * out, blocking. order 0 = value, 1 = + Jacobian, 2 = + Hessian. jac may be
+ * NULL for order 0; hess must be NULL unless order == 2. Each call counts as
+ * one batched call of K points (proj/src/neural.cpp:322-326). */
+rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int order, double* f,
+                       double* jac, double* hess);
+
+/* Device-resident variant: all pointers are device pointers on the context's
+ * device; enqueued on the context stream, returns without synchronising. */
+rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
+                              double* d_jac, double* d_hess);
+
+/* Run the context's work on a caller-provided cudaStream_t (NULL = own). */
+rtn_status rtn_ctx_set_stream(rtn_ctx* c, void* cuda_stream);
+rtn_status rtn_ctx_synchronize(rtn_ctx* c);
+
+/* Counters (EvalCounters::batched_calls / batched_points, neural.hpp:38-44)
+ * and the number of device kernel launches this context has issued. */
+rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* batched_calls,
+                            unsigned long long* batched_points, unsigned long long* kernel_launches);
+
+const char* rtn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTN_MPC_H_ */

@@ -1,0 +1,200 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes binding of oracle/build/liboracle.so: the Eigen-free fp64 CPU
+restatement of the reference's hot path (see resmpc_oracle.h). Only tests/,
+__graft_entry__.smoke() and bench.py's CPU legs may import this package, and
+only as the checker / CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
+TEST_BIN = os.path.join(HERE, "build", "test_oracle")
+ACTS = ("tanh", "relu", "silu")
+
+_lib = None
+_dp = C.POINTER(C.c_double)
+
+
+def build() -> None:
+    subprocess.run(["make", "-C", HERE, "-j4", "all"], check=True, stdout=subprocess.DEVNULL)
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        L.oracle_last_error.restype = C.c_char_p
+        vp = C.c_void_p
+        L.oracle_make_mlp.argtypes = [C.POINTER(C.c_int), C.c_int, C.c_int, C.c_ulonglong, C.POINTER(vp)]
+        L.oracle_random_net.argtypes = [C.POINTER(C.c_int), C.c_int, C.c_int, C.c_ulonglong, C.c_int, C.POINTER(vp)]
+        L.oracle_load_model.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.oracle_save_model.argtypes = [vp, C.c_char_p]
+        L.oracle_free_model.argtypes = [vp]
+        L.oracle_free_model.restype = None
+        L.oracle_model_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.oracle_get_layer.argtypes = [vp, C.c_int, _dp, _dp]
+        L.oracle_set_layer.argtypes = [vp, C.c_int, _dp, _dp]
+        L.oracle_get_norm.argtypes = [vp, _dp, _dp, _dp, _dp]
+        L.oracle_set_norm.argtypes = [vp, _dp, _dp, _dp, _dp]
+        L.oracle_batched_eval.argtypes = [vp, _dp, C.c_longlong, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.oracle_forward_mode.argtypes = [vp, _dp, C.c_longlong, C.c_int, _dp, _dp, _dp]
+        L.oracle_single.argtypes = [vp, _dp, C.c_int, _dp]
+        L.oracle_quad_nodes.argtypes = [C.c_ulonglong, C.c_longlong, _dp]
+        L.oracle_quad_nodes.restype = None
+        L.oracle_random_vector.argtypes = [C.c_ulonglong, C.c_int, C.c_double, C.c_double, _dp]
+        L.oracle_random_vector.restype = None
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(_dp) if a is not None else None
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _check(st):
+    if st != 0:
+        raise OracleError(st, lib().oracle_last_error().decode())
+
+
+class OracleModel:
+    """Handle on an oracle::MlpModel."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+
+    @classmethod
+    def make_mlp(cls, sizes, act="tanh", seed=0):
+        h = C.c_void_p()
+        s = (C.c_int * len(sizes))(*sizes)
+        _check(lib().oracle_make_mlp(s, len(sizes), ACTS.index(act), seed, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def random_net(cls, sizes, act="tanh", rng_seed=0, random_norm=True):
+        h = C.c_void_p()
+        s = (C.c_int * len(sizes))(*sizes)
+        _check(lib().oracle_random_net(s, len(sizes), ACTS.index(act), rng_seed, int(random_norm), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load(cls, path):
+        h = C.c_void_p()
+        _check(lib().oracle_load_model(path.encode(), C.byref(h)))
+        return cls(h)
+
+    def save(self, path):
+        _check(lib().oracle_save_model(self.h, path.encode()))
+
+    def __del__(self):
+        try:
+            lib().oracle_free_model(self.h)
+        except Exception:
+            pass
+
+    def info(self):
+        n = C.c_int()
+        act = C.c_int()
+        lib().oracle_model_info(self.h, C.byref(n), None, C.byref(act))
+        sizes = (C.c_int * n.value)()
+        lib().oracle_model_info(self.h, C.byref(n), sizes, C.byref(act))
+        return list(sizes), ACTS[act.value]
+
+    @property
+    def sizes(self):
+        return self.info()[0]
+
+    def layers(self):
+        sizes = self.sizes
+        out = []
+        for l in range(len(sizes) - 1):
+            w = np.empty((sizes[l + 1], sizes[l]))
+            b = np.empty(sizes[l + 1])
+            _check(lib().oracle_get_layer(self.h, l, _p(w), _p(b)))
+            out.append((w, b))
+        return out
+
+    def set_layer(self, l, w, b):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        _check(lib().oracle_set_layer(self.h, l, _p(w), _p(b)))
+
+    def norm(self):
+        s = self.sizes
+        v = [np.empty(s[0]), np.empty(s[0]), np.empty(s[-1]), np.empty(s[-1])]
+        lib().oracle_get_norm(self.h, *[_p(x) for x in v])
+        return v
+
+    def set_norm(self, in_mean, in_scale, out_mean, out_scale):
+        v = [np.ascontiguousarray(x, dtype=np.float64) for x in (in_mean, in_scale, out_mean, out_scale)]
+        lib().oracle_set_norm(self.h, *[_p(x) for x in v])
+
+    def batched_eval(self, z, order, threads=0):
+        """Reverse-mode reference algorithm: returns (f, jac, hess)."""
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        k = z.shape[0]
+        s = self.sizes
+        n_in, n_out = s[0], s[-1]
+        f = np.empty((k, n_out))
+        jac = np.empty((k, n_out, n_in)) if order >= 1 else None
+        hess = np.empty((k, n_out, n_in, n_in)) if order >= 2 else None
+        _check(lib().oracle_batched_eval(self.h, _p(z), k, order, threads, _p(f), _p(jac), _p(hess)))
+        return f, jac, hess
+
+    def forward_mode(self, z, order):
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        k = z.shape[0]
+        s = self.sizes
+        n_in, n_out = s[0], s[-1]
+        f = np.empty((k, n_out))
+        jac = np.empty((k, n_out, n_in))
+        hess = np.empty((k, n_out, n_in, n_in)) if order >= 2 else None
+        _check(lib().oracle_forward_mode(self.h, _p(z), k, order, _p(f), _p(jac), _p(hess)))
+        return f, jac, hess
+
+
+def quad_nodes(seed, k):
+    z = np.empty((k, 17))
+    lib().oracle_quad_nodes(seed, k, _p(z))
+    return z
+
+
+def rel_error(a, b) -> float:
+    """‖a−b‖∞/(1+‖b‖∞) — proj/tests/oracles.hpp:30-32."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.max(np.abs(a - b)) / (1.0 + np.max(np.abs(b)))) if a.size else 0.0
+
+
+def max_node_rel_error(a, b) -> float:
+    """Per node (axis 0), per block: max over nodes of rel_error."""
+    a = np.asarray(a).reshape(a.shape[0], -1)
+    b = np.asarray(b).reshape(b.shape[0], -1)
+    if a.shape[0] == 0:
+        return 0.0
+    num = np.max(np.abs(a - b), axis=1)
+    den = 1.0 + np.max(np.abs(b), axis=1)
+    return float(np.max(num / den))
+
+
+def to_product_model(om: OracleModel):
+    """Copies an oracle model into the product's MlpModel (test helper)."""
+    from paper_2203_07747_b200.neural import MlpModel
+    sizes, act = om.info()
+    layers = om.layers()
+    im, isc, outm, outs = om.norm()
+    return MlpModel(sizes, [w for w, _ in layers], [b for _, b in layers], act, "full", im, isc, outm, outs, 0)

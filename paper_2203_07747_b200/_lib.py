@@ -1,0 +1,70 @@
+"""ctypes binding of librtn_mpc.so (include/rtn_mpc.h).
+
+There is deliberately no fallback: if the sm_100a library is missing or the
+device is not a B200, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtn_mpc.so")
+
+RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL = range(6)
+RTN_TF32, RTN_3XTF32, RTN_BF16 = range(3)
+
+# Every symbol include/rtn_mpc.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info",
+    "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
+    "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_last_error",
+)
+
+_lib = None
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_vp = C.c_void_p
+
+
+def lib() -> C.CDLL:
+    """Loads the library once; raises loudly when it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2203_07747_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.rtn_last_error.restype = C.c_char_p
+    L.rtn_model_load_rmlp.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.rtn_model_from_arrays.argtypes = [_ip, C.c_int, C.c_int, C.POINTER(_dp), C.POINTER(_dp),
+                                        _dp, _dp, _dp, _dp, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.rtn_model_free.argtypes = [_vp]
+    L.rtn_model_free.restype = None
+    L.rtn_model_info.argtypes = [_vp, _ip, _ip, _ip, _ip, _ip]
+    L.rtn_ctx_create.argtypes = [_vp, C.c_longlong, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.rtn_ctx_free.argtypes = [_vp]
+    L.rtn_ctx_free.restype = None
+    L.rtn_prepare.argtypes = [_vp, _dp, C.c_longlong, C.c_int, C.c_int, _dp, _dp, _dp]
+    L.rtn_prepare_device.argtypes = [_vp, C.c_void_p, C.c_longlong, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_void_p]
+    L.rtn_ctx_set_stream.argtypes = [_vp, _vp]
+    L.rtn_ctx_synchronize.argtypes = [_vp]
+    L.rtn_ctx_counters.argtypes = [_vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong),
+                                   C.POINTER(C.c_ulonglong)]
+    L.rtn_make_mlp.argtypes = [_ip, C.c_int, C.c_ulonglong, C.POINTER(_dp), C.POINTER(_dp)]
+    L.rtn_synth_quad_nodes.argtypes = [C.c_ulonglong, C.c_longlong, _dp]
+    L.rtn_synth_quad_nodes.restype = None
+    for name in EXPORTS:
+        if name not in ("rtn_last_error", "rtn_model_free", "rtn_ctx_free"):
+            getattr(L, name).restype = C.c_int
+    L.rtn_make_mlp.restype = C.c_int
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().rtn_last_error().decode(errors="replace")

@@ -1,0 +1,216 @@
+// rtn_kernel.cuh — fused forward-mode linearisation kernel for sm_100a.
+//
+// What it computes (per node = one shooting node of one MPC instance):
+//   f = out_scale ⊙ net((z − in_mean) ⊘ in_scale) + out_mean,   J = ∂f/∂z
+// i.e. the reference's BatchedCore value + Jacobian
+// (/root/reference/proj/src/neural.cpp:227-255), but by forward-mode tangent
+// propagation instead of the reference's stacked reverse sweep (:132-163):
+// every node carries 1 value row + n_in tangent rows through the network, and
+// because all nodes share the weights, each hidden layer is ONE dense GEMM
+//   D[neuron, row] = Σ_k W[neuron, k] · X[row, k]
+// over (nodes × (1+n_in)) rows, on tcgen05 tensor cores (kind::tf32).
+//
+// Orientation ("swap-AB"): A = weights (M = 128 neurons per block, streamed by
+// the TMA bulk engine from a pre-swizzled device pack), B = activations
+// (N = tile rows, resident in shared memory for the whole network), D in TMEM
+// (lane = neuron, column = row). The epilogue owns one neuron per thread and
+// all rows of a tile, so the activation slope scaling of the tangent rows
+// (t' = σ'(pre_value)·t) is thread-local. Activations never leave the SM:
+// layer l+1 reads what layer l's epilogue wrote back into shared memory.
+//
+// Layer 0 (n_in → width) runs on CUDA cores: its tangent seed is the identity,
+// so the tangent rows after layer 0 are σ'(pre)·W0'[:, k] — no GEMM needed.
+// The output layer (width → n_out ≤ 16) runs as a second tcgen05 shape
+// (M = 128 tile rows, N = 16 outputs, A = activations, B = W_L').
+//
+// Pipelines (all mbarrier based; one thread issues TMA, one issues MMA):
+//   full/empty[s]   producer ↔ MMA over the weight stage ring
+//   tmem_full[g]    MMA → epilogue: neuron block g of the layer is accumulated
+//   in_free[g]      MMA → epilogue: the layer's last M-block has consumed
+//                   input chunk group g, so the epilogue may overwrite it
+//   act_ready[g]    epilogue → MMA: next-layer input group g is in smem
+//   tmem_last       MMA → epilogue: output layer accumulated
+// With this ordering the epilogue of block g overlaps the MMAs of later
+// blocks, and the next layer starts on group 0 while group NMB-1 is still
+// being written.
+#pragma once
+
+#include <cstdint>
+
+namespace rtn {
+
+constexpr int kNT = 80;             // max tile rows (MMA N); multiple of 16
+constexpr int kTmemStride = 80;     // TMEM columns per neuron block region
+constexpr int kStageBytes = 16384;  // one weight block: 128 neurons x 32 k fp32
+constexpr int kLastBlockBytes = 2048;  // output-layer block: 16 outputs x 32 k
+constexpr int kThreads = 384;       // 4 control warps + 8 epilogue warps
+constexpr int kMaxOut = 16;
+
+struct KParams {
+  const double* z;   // K x n_in
+  double* f;         // K x n_out
+  double* jac;       // K x n_out x n_in (may be null for order 0)
+  long long K;
+  long long num_tiles;
+  int n_in, n_out, n_hidden, act, order;
+  int P;             // nodes per tile (power of two)
+  int nt;            // tile rows used (= roundup8(P·(1+n_in))), MMA N
+  const uint8_t* w_hidden;  // (n_hidden-1) x NMB x NKC blocks of kStageBytes
+  const uint8_t* w_last;    // NKC blocks of kLastBlockBytes
+  const float* w0;   // WP x n_in   (normalisation folded)
+  const float* b0;   // WP
+  const float* bh;   // (n_hidden-1) x WP
+  const float* bl;   // kMaxOut     (out_scale ⊙ b_L + out_mean)
+};
+
+// ----------------------------------------------------------------------------
+// PTX wrappers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+// TMA bulk copy global → shared, completion signalled on an mbarrier;
+// weights are re-read by every SM, so keep them resident in L2.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+
+// D[tmem] (+)= A[smem] · B[smem]ᵀ, both K-major, tf32 in, fp32 accumulate.
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrives on `bar` once every previously issued tcgen05.mma of this thread
+// has completed (implicitly fences before_thread_sync).
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups
+// 1024 bytes apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(1) << 16;           // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;   // SBO
+  d |= static_cast<uint64_t>(1) << 46;           // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;           // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, shape M x N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Byte offset of element (row r, k) inside a K-major SW128 operand whose
+// 32-wide k chunks are `chunk_stride` bytes apart.
+__host__ __device__ __forceinline__ uint32_t sw128_offset(int r, int k, uint32_t chunk_stride) {
+  const int c = k >> 5, u = (k >> 2) & 7;
+  return static_cast<uint32_t>(c) * chunk_stride + static_cast<uint32_t>((r >> 3) * 1024 + (r & 7) * 128 +
+                                                                         ((u ^ (r & 7)) << 4) + ((k & 3) << 2));
+}
+
+// Activation value and slope from the pre-activation, fp32
+// (tanh/relu: proj/src/neural.cpp:83-93; SiLU: x·σ(x), σ(1 + x(1−σ))).
+__device__ __forceinline__ void act_fwd(int act, float pre, float& val, float& sp) {
+  if (act == 0) {
+    const float t = tanhf(pre);
+    val = t;
+    sp = 1.0f - t * t;
+  } else if (act == 1) {
+    val = pre > 0.0f ? pre : 0.0f;
+    sp = pre > 0.0f ? 1.0f : 0.0f;
+  } else {
+    const float s = 1.0f / (1.0f + expf(-pre));
+    val = pre * s;
+    sp = s * (1.0f + pre * (1.0f - s));
+  }
+}
+
+}  // namespace rtn

@@ -1,0 +1,533 @@
+// rtn_mpc.cu — C-ABI (include/rtn_mpc.h): model loader/packer, contexts and
+// the PrepareNodes/MlpBatchedEval-equivalent entry points. Every compute call
+// runs the sm_100a kernels in rtn_fused.cuh; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rtn_mpc.h"
+#include "rtn_fused.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  rtn_status code;
+  Error(rtn_status c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+#define CUDA_CHECK(x)                                                                              \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess)                                                                         \
+      throw Error(RTN_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+template <typename F>
+rtn_status Guard(F&& f) {
+  try {
+    f();
+    return RTN_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return RTN_ECONFIG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RTN_ECONFIG;
+  }
+}
+
+// Host-side copy of resmpc::MlpModel (proj/include/resmpc/neural.hpp:19-34).
+struct HostModel {
+  std::vector<int> sizes;
+  int act = 0;
+  std::vector<std::vector<double>> W, b;
+  std::vector<double> in_mean, in_scale, out_mean, out_scale;
+};
+
+// MlpModel::Validate (proj/src/neural.cpp:283-298) → RTN_ECONFIG.
+void Validate(const HostModel& m) {
+  if (m.sizes.size() < 2) throw Error(RTN_ECONFIG, "mlp: need at least input and output layers");
+  for (int s : m.sizes)
+    if (s < 1) throw Error(RTN_ECONFIG, "mlp: layer sizes must be positive");
+  if (m.W.size() != m.sizes.size() - 1 || m.b.size() != m.W.size())
+    throw Error(RTN_ECONFIG, "mlp: weight/bias count does not match layer sizes");
+  for (size_t l = 0; l < m.W.size(); ++l) {
+    if (m.W[l].size() != static_cast<size_t>(m.sizes[l + 1]) * m.sizes[l])
+      throw Error(RTN_ECONFIG, "mlp: layer " + std::to_string(l) + " has incompatible shape");
+    if (m.b[l].size() != static_cast<size_t>(m.sizes[l + 1]))
+      throw Error(RTN_ECONFIG, "mlp: bias " + std::to_string(l) + " has incompatible shape");
+  }
+  const size_t in = m.sizes.front(), out = m.sizes.back();
+  if (m.in_mean.size() != in || m.in_scale.size() != in || m.out_mean.size() != out || m.out_scale.size() != out)
+    throw Error(RTN_ECONFIG, "mlp: normalization vectors do not match layer sizes");
+  for (double s : m.in_scale)
+    if (!(s > 0.0)) throw Error(RTN_ECONFIG, "mlp: normalization scales must be strictly positive");
+  for (double s : m.out_scale)
+    if (!(s > 0.0)) throw Error(RTN_ECONFIG, "mlp: normalization scales must be strictly positive");
+  if (m.act < 0 || m.act > 2) throw Error(RTN_ECONFIG, "mlp: unknown activation");
+}
+
+// Round an fp32 to tf32 (round-to-nearest, ties away), as cvt.rna.tf32.f32.
+float RoundTf32(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+struct rtn_model {
+  int device = 0;
+  rtn_precision prec = RTN_TF32;
+  int n_in = 0, n_out = 0, n_layers = 0, n_hidden = 0, act = 0, wp = 0;
+  void* d_w_hidden = nullptr;  // packed SW128 blocks
+  void* d_w_last = nullptr;
+  float* d_w0 = nullptr;
+  float* d_b0 = nullptr;
+  float* d_bh = nullptr;
+  float* d_bl = nullptr;
+  size_t hidden_bytes = 0;
+  ~rtn_model() {
+    int prev;
+    if (cudaGetDevice(&prev) == cudaSuccess) {
+      cudaSetDevice(device);
+      cudaFree(d_w_hidden);
+      cudaFree(d_w_last);
+      cudaFree(d_w0);
+      cudaFree(d_b0);
+      cudaFree(d_bh);
+      cudaFree(d_bl);
+      cudaSetDevice(prev);
+    }
+  }
+};
+
+struct rtn_ctx {
+  const rtn_model* model = nullptr;
+  long long max_rows = 0;
+  int max_order = 1;
+  int latency_mode = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  double* d_z = nullptr;
+  double* d_f = nullptr;
+  double* d_jac = nullptr;
+  double* h_z = nullptr;  // pinned staging
+  double* h_f = nullptr;
+  double* h_jac = nullptr;
+  int num_sms = 148;
+  unsigned long long calls = 0, points = 0, launches = 0;
+  ~rtn_ctx() {
+    int prev;
+    if (cudaGetDevice(&prev) == cudaSuccess) {
+      cudaSetDevice(model->device);
+      cudaFree(d_z);
+      cudaFree(d_f);
+      cudaFree(d_jac);
+      cudaFreeHost(h_z);
+      cudaFreeHost(h_f);
+      cudaFreeHost(h_jac);
+      if (own_stream) cudaStreamDestroy(own_stream);
+      cudaSetDevice(prev);
+    }
+  }
+};
+
+namespace {
+
+int PaddedWidth(const std::vector<int>& sizes) {
+  int w = 0;
+  for (size_t l = 1; l + 1 < sizes.size(); ++l) w = std::max(w, sizes[l]);
+  return ((w + 127) / 128) * 128;
+}
+
+// Folds the normalisation into the first/last layer in fp64
+// (proj/include/resmpc/neural.hpp:14-18: y = out_scale ⊙ net((z−μ)⊘s) + out_mean):
+//   W0' = W0·diag(1/s),  b0' = b0 − W0'·μ,
+//   WL' = diag(out_scale)·WL,  bL' = out_scale ⊙ bL + out_mean,
+// then packs every tensor-core layer into 128-byte-swizzled K-major blocks in
+// the exact order the kernel streams them.
+rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
+  Validate(hm);
+  if (prec != RTN_TF32) throw Error(RTN_EUNSUPPORTED, "precision mode not implemented yet (TF32 only)");
+  const int L = static_cast<int>(hm.sizes.size()) - 1;
+  const int n_in = hm.sizes.front(), n_out = hm.sizes.back();
+  if (L < 2) throw Error(RTN_EUNSUPPORTED, "device path needs at least one hidden layer");
+  const int wp = PaddedWidth(hm.sizes);
+  if (wp > 512) throw Error(RTN_EUNSUPPORTED, "hidden width > 512 not supported by the fused kernel");
+  if (n_out > rtn::kMaxOut) throw Error(RTN_EUNSUPPORTED, "n_out > 16 not supported");
+  if (1 + n_in > rtn::kNT) throw Error(RTN_EUNSUPPORTED, "n_in > 79 not supported");
+  const int H = L - 1;  // hidden layers (each followed by the activation)
+  const int nkc = wp / 32, nmb = wp / 128;
+
+  // layer 0 (CUDA cores, fp32)
+  std::vector<float> w0(static_cast<size_t>(wp) * n_in, 0.0f), b0(wp, 0.0f);
+  for (int j = 0; j < hm.sizes[1]; ++j) {
+    double acc = hm.b[0][j];
+    for (int k = 0; k < n_in; ++k) {
+      const double w = hm.W[0][static_cast<size_t>(j) * n_in + k] / hm.in_scale[k];
+      w0[static_cast<size_t>(j) * n_in + k] = static_cast<float>(w);
+      acc -= w * hm.in_mean[k];
+    }
+    b0[j] = static_cast<float>(acc);
+  }
+  // hidden → hidden layers (tcgen05, tf32)
+  const size_t blocks = static_cast<size_t>(H - 1) * nmb * nkc;
+  std::vector<uint8_t> wh(blocks * rtn::kStageBytes, 0);
+  std::vector<float> bh(static_cast<size_t>(std::max(H - 1, 1)) * wp, 0.0f);
+  for (int l = 1; l < H; ++l) {
+    const int rows = hm.sizes[l + 1], cols = hm.sizes[l];
+    const std::vector<double>& W = hm.W[l];
+    for (int mb = 0; mb < nmb; ++mb)
+      for (int c = 0; c < nkc; ++c) {
+        uint8_t* blk = wh.data() + ((static_cast<size_t>(l - 1) * nmb + mb) * nkc + c) * rtn::kStageBytes;
+        for (int i = 0; i < 128; ++i)
+          for (int kk = 0; kk < 32; ++kk) {
+            const int j = mb * 128 + i, k = c * 32 + kk;
+            const float v = (j < rows && k < cols) ? RoundTf32(static_cast<float>(W[static_cast<size_t>(j) * cols + k])) : 0.0f;
+            std::memcpy(blk + rtn::sw128_offset(i, kk, 0), &v, 4);
+          }
+      }
+    for (int j = 0; j < rows; ++j) bh[static_cast<size_t>(l - 1) * wp + j] = static_cast<float>(hm.b[l][j]);
+  }
+  // output layer (tcgen05 N = 16)
+  std::vector<uint8_t> wl(static_cast<size_t>(nkc) * rtn::kLastBlockBytes, 0);
+  std::vector<float> bl(rtn::kMaxOut, 0.0f);
+  {
+    const int cols = hm.sizes[L - 1];
+    const std::vector<double>& W = hm.W[L - 1];
+    for (int c = 0; c < nkc; ++c)
+      for (int o = 0; o < 16; ++o)
+        for (int kk = 0; kk < 32; ++kk) {
+          const int k = c * 32 + kk;
+          const float v = (o < n_out && k < cols)
+                              ? RoundTf32(static_cast<float>(hm.out_scale[o] * W[static_cast<size_t>(o) * cols + k]))
+                              : 0.0f;
+          std::memcpy(wl.data() + c * rtn::kLastBlockBytes + rtn::sw128_offset(o, kk, 0), &v, 4);
+        }
+    for (int o = 0; o < n_out; ++o) bl[o] = static_cast<float>(hm.out_scale[o] * hm.b[L - 1][o] + hm.out_mean[o]);
+  }
+
+  int ndev = 0;
+  CUDA_CHECK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw Error(RTN_ECUDA, "invalid device ordinal");
+  cudaDeviceProp prop{};
+  CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) throw Error(RTN_ECUDA, "device is not sm_100 (Blackwell B200)");
+  CUDA_CHECK(cudaSetDevice(device));
+  std::unique_ptr<rtn_model> m(new rtn_model());
+  m->device = device;
+  m->prec = prec;
+  m->n_in = n_in;
+  m->n_out = n_out;
+  m->n_layers = L;
+  m->n_hidden = H;
+  m->act = hm.act;
+  m->wp = wp;
+  m->hidden_bytes = wh.size();
+  auto up = [](void** d, const void* h, size_t n) {
+    CUDA_CHECK(cudaMalloc(d, std::max<size_t>(n, 16)));
+    if (n) CUDA_CHECK(cudaMemcpy(*d, h, n, cudaMemcpyHostToDevice));
+  };
+  up(&m->d_w_hidden, wh.data(), wh.size());
+  up(&m->d_w_last, wl.data(), wl.size());
+  up(reinterpret_cast<void**>(&m->d_w0), w0.data(), w0.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_b0), b0.data(), b0.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_bh), bh.data(), bh.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
+  return m.release();
+}
+
+// RMLP v1/v2 reader (proj/src/neural.cpp:720-755; v2 adds activation tag 2).
+HostModel ReadRmlp(const char* path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(RTN_ECONFIG, std::string("model: cannot open '") + path + "'");
+  auto rd = [&](void* p, size_t n) {
+    in.read(reinterpret_cast<char*>(p), static_cast<std::streamsize>(n));
+    if (!in) throw Error(RTN_ECONFIG, "unexpected end of file");
+  };
+  char magic[4];
+  rd(magic, 4);
+  if (std::memcmp(magic, "RMLP", 4) != 0) throw Error(RTN_ECONFIG, "model: not a model file");
+  uint32_t version;
+  rd(&version, 4);
+  if (version != 1 && version != 2) throw Error(RTN_ECONFIG, "model: unsupported version");
+  uint8_t tag;
+  rd(&tag, 1);
+  HostModel m;
+  if (version == 1) m.act = tag == 0 ? 0 : 1;
+  else if (tag <= 2) m.act = tag;
+  else throw Error(RTN_ECONFIG, "model: unknown activation tag");
+  uint32_t n;
+  rd(&n, 4);
+  std::string variant(n, '\0');
+  if (n) rd(&variant[0], n);
+  uint64_t seed;
+  rd(&seed, 8);
+  uint32_t ns;
+  rd(&ns, 4);
+  if (ns < 2 || ns > 4096) throw Error(RTN_ECONFIG, "mlp: need at least input and output layers");
+  m.sizes.resize(ns);
+  for (auto& s : m.sizes) {
+    uint32_t v;
+    rd(&v, 4);
+    s = static_cast<int>(v);
+  }
+  const int in_d = m.sizes.front(), out_d = m.sizes.back();
+  m.in_mean.resize(in_d);
+  m.in_scale.resize(in_d);
+  m.out_mean.resize(out_d);
+  m.out_scale.resize(out_d);
+  rd(m.in_mean.data(), 8 * in_d);
+  rd(m.in_scale.data(), 8 * in_d);
+  rd(m.out_mean.data(), 8 * out_d);
+  rd(m.out_scale.data(), 8 * out_d);
+  for (size_t l = 0; l + 1 < m.sizes.size(); ++l) {
+    m.W.emplace_back(static_cast<size_t>(m.sizes[l + 1]) * m.sizes[l]);
+    m.b.emplace_back(static_cast<size_t>(m.sizes[l + 1]));
+    rd(m.W.back().data(), 8 * m.W.back().size());
+    rd(m.b.back().data(), 8 * m.b.back().size());
+  }
+  return m;
+}
+
+int NodesPerTile(int n_in) {
+  const int rpn = 1 + n_in;
+  int p = 16;
+  while (p > 1 && p * rpn > rtn::kNT) p >>= 1;
+  return p;
+}
+
+template <int WP, int NS, int P>
+void LaunchT(const rtn::KParams& prm, int grid, cudaStream_t st) {
+  using Cfg = rtn::FusedCfg<WP, NS, P>;
+  auto kern = rtn::rtn_fused_kernel<WP, NS, P>;
+  static bool attr_set = false;  // per instantiation, per process (device-independent attribute)
+  if (!attr_set) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    attr_set = true;
+  }
+  kern<<<grid, rtn::kThreads, Cfg::kSmemBytes, st>>>(prm);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+template <int WP, int NS>
+void LaunchP(const rtn::KParams& prm, int grid, cudaStream_t st) {
+  switch (prm.P) {
+    case 1: return LaunchT<WP, NS, 1>(prm, grid, st);
+    case 2: return LaunchT<WP, NS, 2>(prm, grid, st);
+    case 4: return LaunchT<WP, NS, 4>(prm, grid, st);
+    case 8: return LaunchT<WP, NS, 8>(prm, grid, st);
+    default: return LaunchT<WP, NS, 16>(prm, grid, st);
+  }
+}
+
+void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac) {
+  const rtn_model* m = c->model;
+  if (K == 0) return;
+  rtn::KParams prm{};
+  prm.z = d_z;
+  prm.f = d_f;
+  prm.jac = order >= 1 ? d_jac : nullptr;
+  prm.K = K;
+  prm.n_in = m->n_in;
+  prm.n_out = m->n_out;
+  prm.n_hidden = m->n_hidden;
+  prm.act = m->act;
+  prm.order = order;
+  prm.P = NodesPerTile(m->n_in);
+  prm.nt = ((prm.P * (1 + m->n_in) + 7) / 8) * 8;
+  if (prm.nt < 16) prm.nt = 16;
+  prm.num_tiles = (K + prm.P - 1) / prm.P;
+  prm.w_hidden = static_cast<const uint8_t*>(m->d_w_hidden);
+  prm.w_last = static_cast<const uint8_t*>(m->d_w_last);
+  prm.w0 = m->d_w0;
+  prm.b0 = m->d_b0;
+  prm.bh = m->d_bh;
+  prm.bl = m->d_bl;
+  const int grid = static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms));
+  switch (m->wp) {
+    case 128: LaunchP<128, 8>(prm, grid, c->stream); break;
+    case 256: LaunchP<256, 8>(prm, grid, c->stream); break;
+    default: LaunchP<512, 3>(prm, grid, c->stream); break;
+  }
+  c->launches += 1;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+extern "C" {
+
+const char* rtn_last_error(void) { return g_err.c_str(); }
+
+rtn_status rtn_model_load_rmlp(const char* path, int device, rtn_precision p, rtn_model** out) {
+  return Guard([&] {
+    if (!path || !out) throw Error(RTN_ECONFIG, "null argument");
+    *out = BuildModel(ReadRmlp(path), device, p);
+  });
+}
+
+rtn_status rtn_model_from_arrays(const int* sizes, int n_sizes, int activation, const double* const* W,
+                                 const double* const* b, const double* in_mean, const double* in_scale,
+                                 const double* out_mean, const double* out_scale, int device, rtn_precision p,
+                                 rtn_model** out) {
+  return Guard([&] {
+    if (!sizes || !W || !b || !in_mean || !in_scale || !out_mean || !out_scale || !out || n_sizes < 2)
+      throw Error(RTN_ECONFIG, "mlp: need at least input and output layers");
+    HostModel hm;
+    hm.sizes.assign(sizes, sizes + n_sizes);
+    for (int s : hm.sizes)
+      if (s < 1) throw Error(RTN_ECONFIG, "mlp: layer sizes must be positive");
+    hm.act = activation;
+    for (int l = 0; l + 1 < n_sizes; ++l) {
+      if (!W[l] || !b[l]) throw Error(RTN_ECONFIG, "null layer");
+      hm.W.emplace_back(W[l], W[l] + static_cast<size_t>(sizes[l + 1]) * sizes[l]);
+      hm.b.emplace_back(b[l], b[l] + sizes[l + 1]);
+    }
+    hm.in_mean.assign(in_mean, in_mean + sizes[0]);
+    hm.in_scale.assign(in_scale, in_scale + sizes[0]);
+    hm.out_mean.assign(out_mean, out_mean + sizes[n_sizes - 1]);
+    hm.out_scale.assign(out_scale, out_scale + sizes[n_sizes - 1]);
+    *out = BuildModel(hm, device, p);
+  });
+}
+
+void rtn_model_free(rtn_model* m) { delete m; }
+
+rtn_status rtn_model_info(const rtn_model* m, int* n_in, int* n_out, int* n_layers, int* activation,
+                          int* padded_width) {
+  return Guard([&] {
+    if (!m) throw Error(RTN_ECONFIG, "null model");
+    if (n_in) *n_in = m->n_in;
+    if (n_out) *n_out = m->n_out;
+    if (n_layers) *n_layers = m->n_layers;
+    if (activation) *activation = m->act;
+    if (padded_width) *padded_width = m->wp;
+  });
+}
+
+rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order, int latency_mode, rtn_ctx** out) {
+  return Guard([&] {
+    if (!m || !out) throw Error(RTN_ECONFIG, "null argument");
+    if (max_rows < 1) throw Error(RTN_EDOMAIN, "max_rows must be positive");
+    if (max_order < 0 || max_order > 2) throw Error(RTN_ECONFIG, "order must be 0, 1 or 2");
+    if (max_order == 2) {
+      if (m->act == RTN_ACT_RELU)
+        throw Error(RTN_EUNSUPPORTED, "mlp hessian: relu networks are not twice differentiable");
+      throw Error(RTN_EUNSUPPORTED, "second-order device path not implemented yet");
+    }
+    CUDA_CHECK(cudaSetDevice(m->device));
+    std::unique_ptr<rtn_ctx> c(new rtn_ctx());
+    c->model = m;
+    c->max_rows = max_rows;
+    c->max_order = max_order;
+    c->latency_mode = latency_mode;
+    CUDA_CHECK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, m->device));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    const size_t zb = sizeof(double) * max_rows * m->n_in, fb = sizeof(double) * max_rows * m->n_out,
+                 jb = fb * m->n_in;
+    CUDA_CHECK(cudaMalloc(&c->d_z, zb));
+    CUDA_CHECK(cudaMalloc(&c->d_f, fb));
+    CUDA_CHECK(cudaMallocHost(&c->h_z, zb));
+    CUDA_CHECK(cudaMallocHost(&c->h_f, fb));
+    if (max_order >= 1) {
+      CUDA_CHECK(cudaMalloc(&c->d_jac, jb));
+      CUDA_CHECK(cudaMallocHost(&c->h_jac, jb));
+    }
+    *out = c.release();
+  });
+}
+
+void rtn_ctx_free(rtn_ctx* c) { delete c; }
+
+rtn_status rtn_ctx_set_stream(rtn_ctx* c, void* s) {
+  return Guard([&] {
+    if (!c) throw Error(RTN_ECONFIG, "null context");
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  });
+}
+
+rtn_status rtn_ctx_synchronize(rtn_ctx* c) {
+  return Guard([&] {
+    if (!c) throw Error(RTN_ECONFIG, "null context");
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* calls, unsigned long long* points,
+                            unsigned long long* launches) {
+  return Guard([&] {
+    if (!c) throw Error(RTN_ECONFIG, "null context");
+    if (calls) *calls = c->calls;
+    if (points) *points = c->points;
+    if (launches) *launches = c->launches;
+  });
+}
+
+static void CheckCall(const rtn_ctx* c, long long K, int order) {
+  if (!c) throw Error(RTN_ECONFIG, "null context");
+  if (order < 0 || order > 2) throw Error(RTN_ECONFIG, "prepare nodes: order must be 0, 1 or 2");
+  if (order == 2 && c->model->act == RTN_ACT_RELU)
+    throw Error(RTN_EUNSUPPORTED, "mlp hessian: relu networks are not twice differentiable");
+  if (order > c->max_order) throw Error(RTN_EUNSUPPORTED, "order exceeds the context's max_order");
+  if (K < 0 || K > c->max_rows) throw Error(RTN_EDOMAIN, "K outside [0, max_rows]");
+}
+
+rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int order, double* f, double* jac,
+                       double* hess) {
+  return Guard([&] {
+    CheckCall(c, K, order);
+    const rtn_model* m = c->model;
+    if (n_cols != m->n_in)
+      throw Error(RTN_EDOMAIN, "mlp eval: feature dim " + std::to_string(n_cols) + " does not match model input " +
+                                   std::to_string(m->n_in));
+    if (hess != nullptr && order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless order == 2");
+    if (K > 0 && (!z || !f || (order >= 1 && !jac))) throw Error(RTN_ECONFIG, "null buffer");
+    c->calls += 1;
+    c->points += static_cast<unsigned long long>(K);
+    if (K == 0) return;
+    CUDA_CHECK(cudaSetDevice(m->device));
+    const size_t zb = sizeof(double) * K * m->n_in, fb = sizeof(double) * K * m->n_out, jb = fb * m->n_in;
+    std::memcpy(c->h_z, z, zb);
+    CUDA_CHECK(cudaMemcpyAsync(c->d_z, c->h_z, zb, cudaMemcpyHostToDevice, c->stream));
+    Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac);
+    CUDA_CHECK(cudaMemcpyAsync(c->h_f, c->d_f, fb, cudaMemcpyDeviceToHost, c->stream));
+    if (order >= 1) CUDA_CHECK(cudaMemcpyAsync(c->h_jac, c->d_jac, jb, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    std::memcpy(f, c->h_f, fb);
+    if (order >= 1) std::memcpy(jac, c->h_jac, jb);
+  });
+}
+
+rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac,
+                              double* d_hess) {
+  return Guard([&] {
+    CheckCall(c, K, order);
+    if (d_hess != nullptr && order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless order == 2");
+    if (K > 0 && (!d_z || !d_f || (order >= 1 && !d_jac))) throw Error(RTN_ECONFIG, "null buffer");
+    c->calls += 1;
+    c->points += static_cast<unsigned long long>(K);
+    CUDA_CHECK(cudaSetDevice(c->model->device));
+    Enqueue(c, d_z, K, order, d_f, d_jac);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the fp64 oracle.
+
+Tolerance (north star): norm-wise relative error ‖a−b‖∞/(1+‖b‖∞)
+(proj/tests/oracles.hpp:30-32) per node and per block (f, A = ∂f/∂x, B =
+∂f/∂u), max over nodes: 1e-3 in TF32 mode, 1e-5 in 3xTF32 mode.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import OracleModel, max_node_rel_error, quad_nodes, to_product_model
+
+TF32_TOL = 1e-3
+
+pytestmark = pytest.mark.gpu
+
+
+def _blocks(f, jac):
+    return {"f": f, "A": jac[:, :, :13], "B": jac[:, :, 13:]}
+
+
+def _check(model_sizes, act, k, seed=2203, rng_seed=11, random_norm=True, tol=TF32_TOL):
+    from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
+    om = OracleModel.random_net(model_sizes, act, rng_seed, random_norm)
+    pm = to_product_model(om)
+    z = quad_nodes(seed, k) if model_sizes[0] == 17 else np.random.default_rng(seed).uniform(-2, 2, (k, model_sizes[0]))
+    f_ref, j_ref, _ = om.batched_eval(z, 1)
+    got = mlp_batched_eval(pm, z, EvalOrder.JACOBIAN)
+    ef = max_node_rel_error(got.values, f_ref)
+    ej = max_node_rel_error(got.jacobians, j_ref)
+    assert np.all(np.isfinite(got.values)) and np.all(np.isfinite(got.jacobians))
+    assert ef < tol, f"f rel err {ef}"
+    assert ej < tol, f"J rel err {ej}"
+    if model_sizes[0] == 17:
+        for name, blk in _blocks(got.values, got.jacobians).items():
+            ref = _blocks(f_ref, j_ref)[name]
+            assert max_node_rel_error(blk, ref) < tol, name
+    return ef, ej
+
+
+def test_cfg1_tanh_2x64():
+    _check([17, 64, 64, 6], "tanh", 10)
+
+
+def test_cfg2_silu_5x256_latency_shape():
+    _check([17] + [256] * 5 + [6], "silu", 20)
+
+
+def test_cfg3_silu_12x512():
+    _check([17] + [512] * 12 + [6], "silu", 20)
+
+
+def test_ragged_tile_counts():
+    # K not a multiple of the nodes-per-tile, and more tiles than SMs
+    for k in (1, 3, 5, 7, 13, 601):
+        _check([17, 128, 128, 6], "silu", k)
+
+
+def test_reference_shapes_small_nets():
+    # the reference's own test shapes (proj/tests/test_neural.cpp, test_taylor.cpp)
+    _check([5, 16, 16, 3], "tanh", 20, random_norm=True)
+    _check([6, 32, 32, 4], "tanh", 13)
+    _check([4, 16, 3], "tanh", 10)
+    _check([3, 10, 2], "relu", 20)
+
+
+def test_batch_rows_equal_single_calls():
+    # neural.hpp:65-67 contract within the device kernel family: a row of a
+    # batch is bit-identical to the single-node call.
+    from paper_2203_07747_b200 import mlp_batched_eval, mlp_jacobian, mlp_forward, EvalOrder
+    om = OracleModel.random_net([17, 256, 256, 256, 6], "silu", 23)
+    pm = to_product_model(om)
+    z = quad_nodes(5, 13)
+    z[12] = z[0]
+    b = mlp_batched_eval(pm, z, EvalOrder.JACOBIAN)
+    for i in range(13):
+        assert np.array_equal(b.values[i], mlp_forward(pm, z[i]))
+        assert np.array_equal(b.jacobians[i], mlp_jacobian(pm, z[i]))
+    assert np.array_equal(b.values[0], b.values[12])
+
+
+def test_throughput_shape_cfg4_subset():
+    _check([17] + [256] * 5 + [6], "silu", 4096)
