@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
       mbar_init(&empty[s], 1);
     }
     for (int g = 0; g < 4; ++g) {
-      mbar_init(&act_ready[g], 128);
+      mbar_init(&act_ready[g], 256);
       mbar_init(&in_free[g], 1);
       mbar_init(&tmem_full[g], 1);
     }
@@ -66,29 +66,26 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
 
   if (warp == 0) {
     // ===================== weight producer (TMA bulk engine) ==================
-    if (lane == 0) {
-      const uint64_t pol = l2_evict_last_policy();
-      int s = 0;
-      uint32_t ph = 0;
-      for (long long tile = blockIdx.x; tile < prm.num_tiles; tile += gridDim.x) {
-        const uint8_t* src = prm.w_hidden;
-        for (int b = 0; b < n_mma_layers * NMB * NKC; ++b, src += kStageBytes) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], kStageBytes);
-          bulk_g2s(stage_s + s * kStageBytes, src, kStageBytes, &full[s], pol);
-          if (++s == NSTAGE) { s = 0; ph ^= 1; }
-        }
-        for (int c = 0; c < NKC; ++c) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], kLastBlockBytes);
-          bulk_g2s(stage_s + s * kStageBytes, prm.w_last + c * kLastBlockBytes, kLastBlockBytes, &full[s], pol);
-          if (++s == NSTAGE) { s = 0; ph ^= 1; }
-        }
+    // Whole warp runs the loop (converged); one elected lane issues.
+    const uint64_t pol = l2_evict_last_policy();
+    int s = 0;
+    uint32_t ph = 0;
+    for (long long tile = blockIdx.x; tile < prm.num_tiles; tile += gridDim.x) {
+      const uint8_t* src = prm.w_hidden;
+      for (int b = 0; b < n_mma_layers * NMB * NKC; ++b, src += kStageBytes) {
+        mbar_wait(&empty[s], ph ^ 1);
+        bulk_g2s_warp(stage_s + s * kStageBytes, src, kStageBytes, &full[s], pol);
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+      }
+      for (int c = 0; c < NKC; ++c) {
+        mbar_wait(&empty[s], ph ^ 1);
+        bulk_g2s_warp(stage_s + s * kStageBytes, prm.w_last + c * kLastBlockBytes, kLastBlockBytes, &full[s], pol);
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (single thread) ========================
-    if (lane == 0) {
+    // ===================== MMA issuer (converged warp, elected lane issues) ===
+    {
       const uint32_t idesc_h = idesc_tf32(128, nt);
       const uint32_t idesc_o = idesc_tf32(128, kMaxOut);
       const uint32_t act_addr = smem_u32(act_s);
@@ -111,12 +108,12 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
               const uint64_t b = sw128_desc(act_addr + c * C::kChunkStride);
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
-                mma_tf32(tmem_base + mb * kTmemStride, a + 2 * kk, b + 2 * kk, idesc_h, (c | kk) != 0);
-              mma_commit(&empty[s]);
-              if (mb == NMB - 1 && (c & 3) == 3) mma_commit(&in_free[c >> 2]);
+                mma_tf32_warp(tmem_base + mb * kTmemStride, a + 2 * kk, b + 2 * kk, idesc_h, (c | kk) != 0);
+              mma_commit_warp(&empty[s]);
+              if (mb == NMB - 1 && (c & 3) == 3) mma_commit_warp(&in_free[c >> 2]);
               if (++s == NSTAGE) { s = 0; ph ^= 1; }
             }
-            mma_commit(&tmem_full[mb]);
+            mma_commit_warp(&tmem_full[mb]);
           }
           ++ar;
         }
@@ -132,24 +129,86 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
           const uint64_t a = sw128_desc(act_addr + c * C::kChunkStride);
           const uint64_t b = sw128_desc(stage_addr + s * kStageBytes);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) mma_tf32(tmem_base, a + 2 * kk, b + 2 * kk, idesc_o, (c | kk) != 0);
-          mma_commit(&empty[s]);
+          for (int kk = 0; kk < 4; ++kk) mma_tf32_warp(tmem_base, a + 2 * kk, b + 2 * kk, idesc_o, (c | kk) != 0);
+          mma_commit_warp(&empty[s]);
           if (++s == NSTAGE) { s = 0; ph ^= 1; }
         }
-        mma_commit(tmem_last);
+        mma_commit_warp(tmem_last);
         ++ar;
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (8 warps, one neuron per thread) =========
-    const int half = (warp - 4) >> 2;   // neuron blocks g ≡ half (mod 2)
+    // ===================== epilogue (8 warps) =================================
+    // Thread = one neuron of a 128-neuron block (TMEM lane); the two warp
+    // halves split the tile rows into interleaved CW-column chunks. For each
+    // block g the math is done in place in TMEM as soon as tmem_full[g] fires;
+    // the copy into shared memory waits for in_free[g] (the layer's last block
+    // has consumed input group g), so math never blocks on the in-place hazard.
+    constexpr int CW = P > 8 ? P : 8;   // chunk width; multiple of P → static (c−P) mod P
+    const int half = (warp - 4) >> 2;
     const int q = warp & 3;             // TMEM lane quadrant
-    const int tid_h = q * 32 + lane;    // neuron within a 128-block / row in the output tile
+    const int tid_h = q * 32 + lane;    // neuron within a 128-block / row of the output tile
     const int etid = threadIdx.x - 128;
     const int act = prm.act;
     const int rows_used = P * (1 + n_in);
+    const int nch = (nt + CW - 1) / CW;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     uint32_t hl = 0;  // hidden layers processed (parity source)
     uint32_t tiles_done = 0;
+
+    // In-place TMEM pass for block g: v = act(pre + b) on value rows,
+    // t = σ'(pre)·t on tangent rows, 0 on padding; tf32-rounded.
+    auto compute_block = [&](int g, int l) {
+      const int j = g * 128 + tid_h;
+      const float bj = __ldg(prm.bh + l * WP + j);
+      const uint32_t tb = tmem_base + lane_base + g * kTmemStride;
+      mbar_wait(&tmem_full[g], hl & 1);
+      tc_fence_after();
+      float head[CW];
+      tmem_ld_cw<CW>(tb, head);
+      tmem_ld_wait();
+      float val[P], sp[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) act_fwd(act, head[p] + bj, val[p], sp[p]);
+      for (int ch = half; ch < nch; ch += 2) {
+        float v[CW];
+        if (ch == 0) {
+#pragma unroll
+          for (int i = 0; i < CW; ++i) v[i] = head[i];
+        } else {
+          tmem_ld_cw<CW>(tb + ch * CW, v);
+          tmem_ld_wait();
+        }
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          const int c = ch * CW + i;
+          if (ch == 0 && i < P) v[i] = to_tf32(val[i]);
+          else v[i] = c < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
+        }
+        tmem_st_cw<CW>(tb + ch * CW, v);
+      }
+      tmem_st_wait();
+    };
+    // Copy block g's results (TMEM) into next-layer input group g (smem).
+    auto write_block = [&](int g) {
+      const int j = g * 128 + tid_h;
+      const uint32_t tb = tmem_base + lane_base + g * kTmemStride;
+      mbar_wait(&in_free[g], hl & 1);
+      uint8_t* col = act_s + sw128_offset(0, j, C::kChunkStride);
+      for (int ch = half; ch < nch; ch += 2) {
+        float v[CW];
+        tmem_ld_cw<CW>(tb + ch * CW, v);
+        tmem_ld_wait();
+        uint8_t* base = col + (ch * CW / 8) * 1024;
+#pragma unroll
+        for (int i = 0; i < CW; ++i)
+          *reinterpret_cast<float*>(base + ((i >> 3) * 1024 + (i & 7) * 128 + ((((j >> 2) & 7) ^ (i & 7)) - ((j >> 2) & 7)) * 16)) = v[i];
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      mbar_arrive(&act_ready[g]);
+    };
+
     for (long long tile = blockIdx.x; tile < prm.num_tiles; tile += gridDim.x, ++tiles_done) {
       const long long node0 = tile * P;
       // ---- previous tile's output layer must have consumed the activations
@@ -165,68 +224,46 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       // ---- layer 0 on CUDA cores: value rows + tangent rows σ'(pre)·W0'[:, k]
-      for (int g = half; g < NMB; g += 2) {
+      for (int g = 0; g < NMB; ++g) {
         const int j = g * 128 + tid_h;
         const float* w0r = prm.w0 + j * n_in;
         const float bj = __ldg(prm.b0 + j);
-        float sp[P];
+        float val[P], sp[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           float pre = bj;
           for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[p * n_in + k], pre);
-          float val;
-          act_fwd(act, pre, val, sp[p]);
-          *reinterpret_cast<float*>(act_s + sw128_offset(p, j, C::kChunkStride)) = to_tf32(val);
+          act_fwd(act, pre, val[p], sp[p]);
         }
-        for (int k = 0; k < n_in; ++k) {
-          const float wk = __ldg(w0r + k);
+        uint8_t* col = act_s + sw128_offset(0, j, C::kChunkStride);
+        for (int ch = half; ch < nch; ch += 2) {
+          uint8_t* base = col + (ch * CW / 8) * 1024;
 #pragma unroll
-          for (int p = 0; p < P; ++p)
-            *reinterpret_cast<float*>(act_s + sw128_offset(P + k * P + p, j, C::kChunkStride)) = to_tf32(sp[p] * wk);
+          for (int i = 0; i < CW; ++i) {
+            const int c = ch * CW + i;
+            float v;
+            if (ch == 0 && i < P) v = val[i];
+            else if (c < rows_used) v = sp[i % P] * __ldg(w0r + (c - P) / P);
+            else v = 0.0f;
+            *reinterpret_cast<float*>(base + ((i >> 3) * 1024 + (i & 7) * 128 + ((((j >> 2) & 7) ^ (i & 7)) - ((j >> 2) & 7)) * 16)) = to_tf32(v);
+          }
         }
-        for (int r = rows_used; r < nt; ++r)
-          *reinterpret_cast<float*>(act_s + sw128_offset(r, j, C::kChunkStride)) = 0.0f;
         fence_proxy_async_smem();
         mbar_arrive(&act_ready[g]);
       }
-      // ---- hidden layers on tensor cores: epilogue of block g
+      // ---- hidden layers on tensor cores
       for (int l = 0; l < n_mma_layers; ++l, ++hl) {
-        for (int g = half; g < NMB; g += 2) {
-          const int j = g * 128 + tid_h;
-          const float bj = __ldg(prm.bh + l * WP + j);
-          mbar_wait(&tmem_full[g], hl & 1);
-          tc_fence_after();
-          float v[kNT];
-          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + g * kTmemStride;
-#pragma unroll
-          for (int c0 = 0; c0 < kNT; c0 += 16)
-            if (c0 < nt) tmem_ld16(taddr + c0, v + c0);
-          tmem_ld_wait();
-          tc_fence_before();
-          float sp[P];
-#pragma unroll
-          for (int p = 0; p < P; ++p) {
-            float val;
-            act_fwd(act, v[p] + bj, val, sp[p]);
-            v[p] = to_tf32(val);
-          }
-#pragma unroll
-          for (int r = P; r < kNT; ++r) v[r] = r < rows_used ? to_tf32(v[r] * sp[(r - P) % P]) : 0.0f;
-          // wait until the layer's last neuron block has read input group g
-          mbar_wait(&in_free[g], hl & 1);
-#pragma unroll
-          for (int r = 0; r < kNT; ++r)
-            if (r < nt) *reinterpret_cast<float*>(act_s + sw128_offset(r, j, C::kChunkStride)) = v[r];
-          fence_proxy_async_smem();
-          mbar_arrive(&act_ready[g]);
-        }
+        for (int g = 0; g + 1 < NMB; ++g) compute_block(g, l);
+        for (int g = 0; g + 1 < NMB; ++g) write_block(g);
+        compute_block(NMB - 1, l);
+        write_block(NMB - 1);
       }
       // ---- output layer epilogue: lane = tile row, column = output
       mbar_wait(tmem_last, tiles_done & 1);
       tc_fence_after();
       if (half == 0) {
         float o[16];
-        tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16), o);
+        tmem_ld16(tmem_base + lane_base, o);
         tmem_ld_wait();
         const int r = tid_h;
         const int n_out = prm.n_out;
