@@ -22,7 +22,7 @@ NVCC_FLAGS = [
 ]
 
 SOURCES = ["rtn_mpc.cu", "rtn_synth.cpp"]
-DEPS = SOURCES + ["rtn_kernel.cuh", "rtn_fused.cuh"]
+DEPS = SOURCES + ["rtn_kernel.cuh", "rtn_fused.cuh", "rtn_pair.cuh"]
 
 
 def _nvcc() -> str:

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
       const uint8_t* src = prm.w_hidden;
       for (int b = 0; b < n_mma_layers * NMB * NKC; ++b, src += kStageBytes) {
         mbar_wait(&empty[s], ph ^ 1);
-        bulk_g2s_warp(stage_s + s * kStageBytes, src, kStageBytes, &full[s], pol);
+        bulk_g2s_warp(stage_s + s * kStageBytes, src, (prm.dbg & 2) ? 1024u : kStageBytes, &full[s], pol);
         if (++s == NSTAGE) { s = 0; ph ^= 1; }
       }
       for (int c = 0; c < NKC; ++c) {
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
           for (int mb = 0; mb < NMB; ++mb) {
 #pragma unroll 1
             for (int c = 0; c < NKC; ++c) {
-              if (mb == 0 && (c & 3) == 0) {
+              if (mb == 0 && (c & 3) == 0 && !(prm.dbg & 1)) {
                 mbar_wait(&act_ready[c >> 2], ar & 1);
                 tc_fence_after();
               }
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
         // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]
 #pragma unroll 1
         for (int c = 0; c < NKC; ++c) {
-          if ((c & 3) == 0) {
+          if ((c & 3) == 0 && !(prm.dbg & 1)) {
             mbar_wait(&act_ready[c >> 2], ar & 1);
             tc_fence_after();
           }
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
         ++ar;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && !(prm.dbg & 1)) {
     // ===================== epilogue (8 warps) =================================
     // Thread = one neuron of a 128-neuron block (TMEM lane); the two warp
     // halves split the tile rows into interleaved CW-column chunks. For each
@@ -156,6 +156,14 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
     uint32_t hl = 0;  // hidden layers processed (parity source)
     uint32_t tiles_done = 0;
 
+    // Row r of a K-major SW128 operand lives at  col + (r/8)·1024 + (r%8)·128
+    // + ((u ^ r%8) − u)·16  relative to row 0 of this thread's neuron column
+    // (u = (j/4) mod 8 is the same for every block g). Precompute the XOR term.
+    int swz[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) swz[i] = ((((tid_h >> 2) & 7) ^ i) - ((tid_h >> 2) & 7)) * 16 + i * 128;
+    const int full_chunks = rows_used / CW;  // chunks with no padding rows
+
     // In-place TMEM pass for block g: v = act(pre + b) on value rows,
     // t = σ'(pre)·t on tangent rows, 0 on padding; tf32-rounded.
     auto compute_block = [&](int g, int l) {
@@ -164,26 +172,29 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
       const uint32_t tb = tmem_base + lane_base + g * kTmemStride;
       mbar_wait(&tmem_full[g], hl & 1);
       tc_fence_after();
+      if (prm.dbg & 4) return;
       float head[CW];
       tmem_ld_cw<CW>(tb, head);
       tmem_ld_wait();
       float val[P], sp[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) act_fwd(act, head[p] + bj, val[p], sp[p]);
-      for (int ch = half; ch < nch; ch += 2) {
+      if (half == 0) {  // chunk 0: value rows [0, P) then tangent rows
+#pragma unroll
+        for (int i = 0; i < CW; ++i)
+          head[i] = i < P ? to_tf32(val[i]) : (i < rows_used ? to_tf32(head[i] * sp[i % P]) : 0.0f);
+        tmem_st_cw<CW>(tb, head);
+      }
+      for (int ch = (half == 0 ? 2 : 1); ch < nch; ch += 2) {
         float v[CW];
-        if (ch == 0) {
+        tmem_ld_cw<CW>(tb + ch * CW, v);
+        tmem_ld_wait();
+        if (ch < full_chunks) {
 #pragma unroll
-          for (int i = 0; i < CW; ++i) v[i] = head[i];
+          for (int i = 0; i < CW; ++i) v[i] = to_tf32(v[i] * sp[i % P]);
         } else {
-          tmem_ld_cw<CW>(tb + ch * CW, v);
-          tmem_ld_wait();
-        }
 #pragma unroll
-        for (int i = 0; i < CW; ++i) {
-          const int c = ch * CW + i;
-          if (ch == 0 && i < P) v[i] = to_tf32(val[i]);
-          else v[i] = c < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
+          for (int i = 0; i < CW; ++i) v[i] = ch * CW + i < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
         }
         tmem_st_cw<CW>(tb + ch * CW, v);
       }
@@ -195,14 +206,13 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
       const uint32_t tb = tmem_base + lane_base + g * kTmemStride;
       mbar_wait(&in_free[g], hl & 1);
       uint8_t* col = act_s + sw128_offset(0, j, C::kChunkStride);
-      for (int ch = half; ch < nch; ch += 2) {
+      for (int ch = half; ch < nch && !(prm.dbg & 4); ch += 2) {
         float v[CW];
         tmem_ld_cw<CW>(tb + ch * CW, v);
         tmem_ld_wait();
         uint8_t* base = col + (ch * CW / 8) * 1024;
 #pragma unroll
-        for (int i = 0; i < CW; ++i)
-          *reinterpret_cast<float*>(base + ((i >> 3) * 1024 + (i & 7) * 128 + ((((j >> 2) & 7) ^ (i & 7)) - ((j >> 2) & 7)) * 16)) = v[i];
+        for (int i = 0; i < CW; ++i) *reinterpret_cast<float*>(base + (i >> 3) * 1024 + swz[i & 7]) = v[i];
       }
       tc_fence_before();
       fence_proxy_async_smem();
@@ -245,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
             if (ch == 0 && i < P) v = val[i];
             else if (c < rows_used) v = sp[i % P] * __ldg(w0r + (c - P) / P);
             else v = 0.0f;
-            *reinterpret_cast<float*>(base + ((i >> 3) * 1024 + (i & 7) * 128 + ((((j >> 2) & 7) ^ (i & 7)) - ((j >> 2) & 7)) * 16)) = to_tf32(v);
+            *reinterpret_cast<float*>(base + (i >> 3) * 1024 + swz[i & 7]) = to_tf32(v);
           }
         }
         fence_proxy_async_smem();

@@ -1,9 +1,11 @@
 // rtn_mpc.cu — C-ABI (include/rtn_mpc.h): model loader/packer, contexts and
 // the PrepareNodes/MlpBatchedEval-equivalent entry points. Every compute call
 // runs the sm_100a kernels in rtn_fused.cuh; there is no CPU fallback.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -14,6 +16,7 @@
 
 #include "../../include/rtn_mpc.h"
 #include "rtn_fused.cuh"
+#include "rtn_pair.cuh"
 
 namespace {
 
@@ -103,6 +106,11 @@ struct rtn_model {
   float* d_bh = nullptr;
   float* d_bl = nullptr;
   size_t hidden_bytes = 0;
+  // pair (cta_group::2) kernel: plain row-major tf32 weights behind TMA maps
+  float* d_wt_hidden = nullptr;  // (n_hidden-1)·wp rows x wp cols
+  float* d_wt_last = nullptr;    // 16 rows x wp cols
+  CUtensorMap tmap_h{}, tmap_l{};
+  bool has_pair = false;
   ~rtn_model() {
     int prev;
     if (cudaGetDevice(&prev) == cudaSuccess) {
@@ -113,6 +121,8 @@ struct rtn_model {
       cudaFree(d_b0);
       cudaFree(d_bh);
       cudaFree(d_bl);
+      cudaFree(d_wt_hidden);
+      cudaFree(d_wt_last);
       cudaSetDevice(prev);
     }
   }
@@ -155,6 +165,37 @@ int PaddedWidth(const std::vector<int>& sizes) {
   int w = 0;
   for (size_t l = 1; l + 1 < sizes.size(); ++l) w = std::max(w, sizes[l]);
   return ((w + 127) / 128) * 128;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn GetEncodeTiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw Error(RTN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 row-major [rows x cols] map with a {32, box_rows} box and the
+// 128-byte swizzle the UMMA descriptors expect.
+CUtensorMap MakeTmap(float* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 4};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = GetEncodeTiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RTN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
 }
 
 // Folds the normalisation into the first/last layer in fp64
@@ -251,6 +292,29 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   up(reinterpret_cast<void**>(&m->d_b0), b0.data(), b0.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bh), bh.data(), bh.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
+  if (wp >= 256) {
+    // plain row-major tf32 copies for the pair kernel's TMA maps
+    std::vector<float> th(static_cast<size_t>(std::max(H - 1, 1)) * wp * wp, 0.0f), tl(static_cast<size_t>(16) * wp, 0.0f);
+    for (int l = 1; l < H; ++l) {
+      const int rows = hm.sizes[l + 1], cols = hm.sizes[l];
+      for (int j = 0; j < rows; ++j)
+        for (int k = 0; k < cols; ++k)
+          th[(static_cast<size_t>(l - 1) * wp + j) * wp + k] =
+              RoundTf32(static_cast<float>(hm.W[l][static_cast<size_t>(j) * cols + k]));
+    }
+    {
+      const int cols = hm.sizes[L - 1];
+      for (int o = 0; o < n_out; ++o)
+        for (int k = 0; k < cols; ++k)
+          tl[static_cast<size_t>(o) * wp + k] =
+              RoundTf32(static_cast<float>(hm.out_scale[o] * hm.W[L - 1][static_cast<size_t>(o) * cols + k]));
+    }
+    up(reinterpret_cast<void**>(&m->d_wt_hidden), th.data(), th.size() * 4);
+    up(reinterpret_cast<void**>(&m->d_wt_last), tl.data(), tl.size() * 4);
+    m->tmap_h = MakeTmap(m->d_wt_hidden, static_cast<uint64_t>(std::max(H - 1, 1)) * wp, wp, 128);
+    m->tmap_l = MakeTmap(m->d_wt_last, 16, wp, 8);
+    m->has_pair = true;
+  }
   return m.release();
 }
 
@@ -338,6 +402,43 @@ void LaunchP(const rtn::KParams& prm, int grid, cudaStream_t st) {
   }
 }
 
+template <int WP, int NS, int P>
+void LaunchPairT(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStream_t st) {
+  using Cfg = rtn::PairCfg<WP, NS, P>;
+  auto kern = rtn::rtn_pair_kernel<WP, NS, P>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    attr_set = true;
+  }
+  kern<<<grid, rtn::kThreads, Cfg::kSmemBytes, st>>>(prm, m->tmap_h, m->tmap_l);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+template <int WP, int NS>
+void LaunchPairP(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStream_t st) {
+  switch (prm.P) {
+    case 1: return LaunchPairT<WP, NS, 1>(prm, m, grid, st);
+    case 2: return LaunchPairT<WP, NS, 2>(prm, m, grid, st);
+    case 4: return LaunchPairT<WP, NS, 4>(prm, m, grid, st);
+    case 8: return LaunchPairT<WP, NS, 8>(prm, m, grid, st);
+    default: return LaunchPairT<WP, NS, 16>(prm, m, grid, st);
+  }
+}
+
+// Kernel choice: the pair kernel needs a padded width of 256/512 and enough
+// pair tiles to fill the machine; small batches (latency mode) use the
+// single-CTA kernel, which spreads 4 nodes per SM. RTN_KERNEL=pair|single
+// forces one (tests use it to cover both paths).
+bool UsePair(const rtn_model* m, long long K, int P, int num_sms) {
+  if (!m->has_pair) return false;
+  if (const char* e = std::getenv("RTN_KERNEL")) {
+    if (std::strcmp(e, "pair") == 0) return true;
+    if (std::strcmp(e, "single") == 0) return false;
+  }
+  return K >= static_cast<long long>(2 * P) * num_sms;
+}
+
 void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac) {
   const rtn_model* m = c->model;
   if (K == 0) return;
@@ -355,12 +456,21 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   prm.nt = ((prm.P * (1 + m->n_in) + 7) / 8) * 8;
   if (prm.nt < 16) prm.nt = 16;
   prm.num_tiles = (K + prm.P - 1) / prm.P;
+  if (const char* d = std::getenv("RTN_DEBUG")) prm.dbg = std::atoi(d);
   prm.w_hidden = static_cast<const uint8_t*>(m->d_w_hidden);
   prm.w_last = static_cast<const uint8_t*>(m->d_w_last);
   prm.w0 = m->d_w0;
   prm.b0 = m->d_b0;
   prm.bh = m->d_bh;
   prm.bl = m->d_bl;
+  if (UsePair(m, K, prm.P, c->num_sms)) {
+    prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
+    const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+    if (m->wp == 256) LaunchPairP<256, 8>(prm, m, grid, c->stream);
+    else LaunchPairP<512, 4>(prm, m, grid, c->stream);
+    c->launches += 1;
+    return;
+  }
   const int grid = static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms));
   switch (m->wp) {
     case 128: LaunchP<128, 8>(prm, grid, c->stream); break;

@@ -1,0 +1,341 @@
+// rtn_pair.cuh — throughput kernel on CTA pairs (cta_group::2).
+//
+// Why pairs: a tcgen05 tf32 MMA with both operands in shared memory reads
+// them at ~128 B/clk/SM, so M = 128 × N = 72 runs at 72 % of the math floor
+// and, once the TMA weight stream shares the SMEM port, at ~62 %; N ≥ 128 is
+// needed to be math-bound (scripts/mma_bench.cu). Fp32 activations for a
+// 512-wide layer cap a single CTA at ~80 rows of smem, so the N = 144 tile is
+// split over two CTAs of a cluster: one pair MMA (M = 256 neurons, N = 2·72
+// rows) takes A (weights) half from each CTA and B (activations) half from
+// each CTA; each CTA's TMEM receives its 128 neurons for all 144 rows.
+//
+// Data movement per layer (everything else as in rtn_fused.cuh):
+//   weights   : 2-SM TMA tile loads (tensor map, SWIZZLE_128B), each CTA its
+//               128-neuron half, bytes counted on the leader's barrier
+//   activations: the epilogue of CTA r owns next-layer K-group q = 2·mb + r
+//               and writes its 144 rows into BOTH CTAs' operand buffers (half
+//               of them through DSMEM, st.shared::cluster)
+//   barriers  : full[s] (leader), act_ready[q] (leader, 256 arrivals from the
+//               owning CTA), empty/in_free/tmem_full/tmem_last multicast by
+//               the leader's tcgen05.commit to both CTAs.
+#pragma once
+
+#include <cuda.h>
+
+#include "rtn_kernel.cuh"
+
+namespace rtn {
+
+constexpr int kNTC = 80;            // max rows per CTA (pair N ≤ 160)
+constexpr int kTmemStride2 = 160;   // TMEM columns per 256-neuron block
+constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x 32 k
+
+template <int WP, int NSTAGE, int P>
+struct PairCfg {
+  static constexpr int kNMB = WP / 256;  // 256-neuron blocks (pair M)
+  static constexpr int kNKC = WP / 32;   // 32-wide k chunks
+  static constexpr int kNG = WP / 128;   // 128-neuron K-groups (one per CTA per block)
+  static constexpr uint32_t kChunkStride = kNTC * 128;
+  static constexpr uint32_t kActBytes = kNKC * kChunkStride;
+  static constexpr uint32_t kStageOff = kActBytes;
+  static constexpr uint32_t kBarOff = kStageOff + NSTAGE * kStageBytes;
+  static constexpr uint32_t kNumBars = 2 * NSTAGE + 13;
+  static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
+  static constexpr uint32_t kZsOff = kMiscOff + 16;
+  static constexpr uint32_t kSmemBytes = kZsOff + 2 * kNTC * 4 + 1024;
+  static_assert(kNMB >= 1 && kNMB <= 2, "pair kernel handles 256 or 512 padded width");
+  static_assert(kNMB * kTmemStride2 <= 512, "TMEM capacity");
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
+};
+
+template <int WP, int NSTAGE, int P>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    rtn_pair_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
+                    const __grid_constant__ CUtensorMap tmap_l) {
+  using C = PairCfg<WP, NSTAGE, P>;
+  constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* act_s = smem;
+  uint8_t* stage_s = smem + C::kStageOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NSTAGE;
+  uint64_t* act_ready = bars + 2 * NSTAGE;
+  uint64_t* in_free = act_ready + 4;
+  uint64_t* tmem_full = in_free + 4;
+  uint64_t* tmem_last = tmem_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kMiscOff);
+  float* zs = reinterpret_cast<float*>(smem + C::kZsOff);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int n_in = prm.n_in, ntc = prm.nt;  // rows per CTA
+  const int n_mma_layers = prm.n_hidden - 1;
+  const long long pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int g = 0; g < 4; ++g) {
+      mbar_init(&act_ready[g], 8);  // one elected arrive per epilogue warp of the owning CTA
+      mbar_init(&in_free[g], 1);
+      mbar_init(&tmem_full[g], 1);
+    }
+    mbar_init(tmem_last, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    prefetch_tmap(&tmap_h);
+    prefetch_tmap(&tmap_l);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== weight producer: 2-SM TMA, own 128-neuron half ====
+    const uint64_t pol = l2_evict_last_policy();
+    int s = 0;
+    uint32_t ph = 0;
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
+      for (int l = 0; l < n_mma_layers; ++l)
+        for (int mb = 0; mb < NMB; ++mb)
+          for (int c = 0; c < NKC; ++c) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (leader) mbar_expect_tx_elect(&full[s], 2 * kStageBytes);
+            tma_load_2sm(stage_s + s * kStageBytes, &tmap_h, c * 32, l * WP + mb * 256 + static_cast<int>(rank) * 128,
+                         &full[s], pol);
+            if (++s == NSTAGE) { s = 0; ph ^= 1; }
+          }
+      for (int c = 0; c < NKC; ++c) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (leader) mbar_expect_tx_elect(&full[s], 2 * kLastHalfBytes);
+        tma_load_2sm(stage_s + s * kStageBytes, &tmap_l, c * 32, static_cast<int>(rank) * 8, &full[s], pol);
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== pair MMA issuer (leader CTA) ======================
+    if (leader) {
+      const uint32_t idesc_h = idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_o = idesc_tf32(256, kMaxOut);
+      const uint32_t act_addr = smem_u32(act_s);
+      const uint32_t stage_addr = smem_u32(stage_s);
+      int s = 0;
+      uint32_t ph = 0, ar = 0;
+      // Before the first MMA of a layer overwrites TMEM block 0, both CTAs must
+      // have drained it: wait for K-groups 0 and 1 (one per CTA) up front.
+      auto wait_group = [&](int c) {
+        if ((c & 3) != 0) return;
+        const int g = c >> 2;
+        if (g == 0) {
+          mbar_wait_cluster(&act_ready[0], ar & 1);
+          if (NG > 1) mbar_wait_cluster(&act_ready[1], ar & 1);
+        } else if (g != 1) {
+          mbar_wait_cluster(&act_ready[g], ar & 1);
+        }
+        tc_fence_after();
+      };
+      for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
+        for (int l = 0; l < n_mma_layers; ++l) {
+#pragma unroll 1
+          for (int mb = 0; mb < NMB; ++mb) {
+#pragma unroll 1
+            for (int c = 0; c < NKC; ++c) {
+              if (mb == 0) wait_group(c);
+              mbar_wait(&full[s], ph);
+              tc_fence_after();
+              const uint64_t a = sw128_desc(stage_addr + s * kStageBytes);
+              const uint64_t b = sw128_desc(act_addr + c * C::kChunkStride);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_tf32_pair(tmem_base + mb * kTmemStride2, a + 2 * kk, b + 2 * kk, idesc_h, (c | kk) != 0);
+              mma_commit_pair(&empty[s]);
+              if (mb == NMB - 1 && (c & 3) == 3) mma_commit_pair(&in_free[c >> 2]);
+              if (++s == NSTAGE) { s = 0; ph ^= 1; }
+            }
+            mma_commit_pair(&tmem_full[mb]);
+          }
+          ++ar;
+        }
+        // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]; M = 2 x 128 rows, N = 16
+#pragma unroll 1
+        for (int c = 0; c < NKC; ++c) {
+          wait_group(c);
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t a = sw128_desc(act_addr + c * C::kChunkStride);
+          const uint64_t b = sw128_desc(stage_addr + s * kStageBytes);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) mma_tf32_pair(tmem_base, a + 2 * kk, b + 2 * kk, idesc_o, (c | kk) != 0);
+          mma_commit_pair(&empty[s]);
+          if (++s == NSTAGE) { s = 0; ph ^= 1; }
+        }
+        mma_commit_pair(tmem_last);
+        ++ar;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (8 warps per CTA) ========================
+    // Thread = one neuron (TMEM lane) of this CTA's 128-neuron half of a
+    // 256-block; warp half h owns the rows of side h (the P nodes whose
+    // operand rows live in CTA h), i.e. TMEM columns [h·ntc, (h+1)·ntc).
+    // Results stay in registers until the layer's last block has consumed
+    // the input group they overwrite (in_free), then go straight to the
+    // owning CTA's shared memory (DSMEM for the peer side).
+    const int half = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int tid_h = q * 32 + lane;
+    const int etid = threadIdx.x - 128;
+    const int act = prm.act;
+    const int rows_used = P * (1 + n_in);   // rows per side
+    const bool no_pad = rows_used == ntc;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    int swz[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) swz[i] = ((((tid_h >> 2) & 7) ^ i) - ((tid_h >> 2) & 7)) * 16 + i * 128;
+    const uint32_t act_local = smem_u32(act_s);
+    const bool local_side = half == static_cast<int>(rank);
+    const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
+    uint32_t ready_cl[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);
+    uint32_t hl = 0, tiles_done = 0;
+
+    // Activation epilogue on one side's rows: value rows → tf32(σ(pre+b)),
+    // tangent rows → tf32(σ'(pre)·t), padding → 0.
+    auto scale_side = [&](float* v, float bj) {
+      float val[P], sp[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) act_fwd(act, v[p] + bj, val[p], sp[p]);
+#pragma unroll
+      for (int p = 0; p < P; ++p) v[p] = to_tf32(val[p]);
+      if (no_pad) {
+#pragma unroll
+        for (int i = P; i < kNTC; ++i) v[i] = to_tf32(v[i] * sp[i % P]);
+      } else {
+#pragma unroll
+        for (int i = P; i < kNTC; ++i) v[i] = i < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
+      }
+    };
+    // Store one neuron column (rows 0..ntc-1) of one side into its operand buffer.
+    auto store_side = [&](const float* v, int j) {
+      const uint32_t base = side_base + sw128_offset(0, j, C::kChunkStride);
+      if (local_side) {
+#pragma unroll
+        for (int i = 0; i < kNTC; ++i)
+          if ((i & ~7) < ntc) st_shared_f32(base + (i >> 3) * 1024 + swz[i & 7], v[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < kNTC; ++i)
+          if ((i & ~7) < ntc) st_cluster_f32(base + (i >> 3) * 1024 + swz[i & 7], v[i]);
+      }
+    };
+    auto publish = [&](int grp) {
+      fence_proxy_async_cluster();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(ready_cl[grp]);
+    };
+    // Hidden block mb: TMEM (this CTA's 128 neurons, this half's side) →
+    // registers → epilogue → operand buffer of K-group 2·mb + rank.
+    auto do_block = [&](int mb, int l) {
+      const int grp = 2 * mb + static_cast<int>(rank);
+      const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
+      const float bj = __ldg(prm.bh + l * WP + j);
+      const uint32_t ts = tmem_base + lane_base + mb * kTmemStride2 + half * ntc;
+      mbar_wait(&tmem_full[mb], hl & 1);
+      tc_fence_after();
+      if (prm.dbg & 4) {
+        mbar_wait(&in_free[grp], hl & 1);
+        tc_fence_before();
+        publish(grp);
+        return;
+      }
+      float v[kNTC];
+#pragma unroll
+      for (int c0 = 0; c0 < kNTC; c0 += 8)
+        if (c0 < ntc) tmem_ld8(ts + c0, v + c0);
+      tmem_ld_wait();
+      tc_fence_before();
+      scale_side(v, bj);
+      mbar_wait(&in_free[grp], hl & 1);
+      store_side(v, j);
+      publish(grp);
+    };
+
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
+      const long long node0 = tile * (2 * P);
+      if (tiles_done > 0) {
+        mbar_wait(tmem_last, (tiles_done - 1) & 1);
+        tc_fence_after();
+      }
+      // stage z of both sides' nodes (2P) for layer 0
+      if (etid < 2 * P * n_in) {
+        const int p = etid / n_in, k = etid - p * n_in;
+        const long long node = node0 + p;
+        zs[etid] = node < prm.K ? static_cast<float>(prm.z[node * n_in + k]) : 0.0f;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // ---- layer 0 (CUDA cores): this CTA owns K-groups g ≡ rank (mod 2); half h writes side h
+      for (int g = static_cast<int>(rank); g < NG; g += 2) {
+        const int j = g * 128 + tid_h;
+        const float* w0r = prm.w0 + j * n_in;
+        const float bj = __ldg(prm.b0 + j);
+        float val[P], sp[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float pre = bj;
+          for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[(half * P + p) * n_in + k], pre);
+          act_fwd(act, pre, val[p], sp[p]);
+        }
+        float v[kNTC];
+#pragma unroll
+        for (int i = 0; i < kNTC; ++i) {
+          if (i < P) v[i] = to_tf32(val[i]);
+          else v[i] = i < rows_used ? to_tf32(sp[i % P] * __ldg(w0r + (i - P) / P)) : 0.0f;
+        }
+        store_side(v, j);
+        publish(g);
+      }
+      // ---- hidden layers
+      for (int l = 0; l < n_mma_layers; ++l, ++hl)
+        for (int mb = 0; mb < NMB; ++mb) do_block(mb, l);
+      // ---- output layer: this CTA's rows in its TMEM lanes, outputs in columns 0..15
+      mbar_wait(tmem_last, tiles_done & 1);
+      tc_fence_after();
+      if (half == 0) {
+        float o[16];
+        tmem_ld16(tmem_base + lane_base, o);
+        tmem_ld_wait();
+        const int r = tid_h;
+        const int n_out = prm.n_out;
+        const long long nbase = node0 + static_cast<long long>(rank) * P;
+        if (r < P) {
+          const long long node = nbase + r;
+          if (node < prm.K)
+            for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+        } else if (r < rows_used && prm.jac != nullptr) {
+          const int k = (r - P) / P, p = (r - P) % P;
+          const long long node = nbase + p;
+          if (node < prm.K)
+            for (int oo = 0; oo < n_out; ++oo) prm.jac[(node * n_out + oo) * n_in + k] = static_cast<double>(o[oo]);
+        }
+      }
+      tc_fence_before();
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+}  // namespace rtn

@@ -52,3 +52,38 @@ for r in data:
     mix[o] = mix.get(o, 0) + float(r[i_e] or 0)
 for o, n in sorted(mix.items(), key=lambda x: -x[1])[:top]:
     print(f"  {o:12s} {n / tot_e * 100:5.1f}%  {n:.3e}")
+
+# ---- per CUDA source line (needs -lineinfo)
+txt = ncu("--page", "source", "--csv", "--print-source=cuda,sass")
+cur_file = "?"
+lines = []
+for r in csv.reader(io.StringIO(txt)):
+    if not r:
+        continue
+    if r[0] == "File Path":
+        cur_file = r[1].split("/")[-1]
+        continue
+    if r[0] in ("Function Name", "Line No") or r[0] == "":
+        if r[0] == "Line No":
+            hdrl = r
+        continue
+    try:
+        ln = int(r[0])
+    except ValueError:
+        continue
+    def num(x):
+        try:
+            return float(x)
+        except ValueError:
+            return 0.0
+    s = num(r[hdrl.index("Warp Stall Sampling (All Samples)")])
+    e = num(r[hdrl.index("Instructions Executed")])
+    lines.append((s, e, cur_file, ln, r[1].strip()[:70]))
+ts = sum(x[0] for x in lines) or 1
+te = sum(x[1] for x in lines) or 1
+print("\n-- top CUDA lines by stall samples (samples%, executed%)")
+for s, e, f, ln, src in sorted(lines, key=lambda x: -x[0])[:top]:
+    print(f"{s / ts * 100:5.1f}% {e / te * 100:5.1f}%  {f}:{ln:<5d} {src}")
+print("\n-- top CUDA lines by executed warp-instructions")
+for s, e, f, ln, src in sorted(lines, key=lambda x: -x[1])[:top]:
+    print(f"{s / ts * 100:5.1f}% {e / te * 100:5.1f}%  {f}:{ln:<5d} {src}")

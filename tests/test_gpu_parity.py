@@ -15,6 +15,13 @@ TF32_TOL = 1e-3
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["single", "pair"])
+def kernel(request, monkeypatch):
+    """Both device kernels: single-CTA (latency/small K) and CTA-pair (throughput)."""
+    monkeypatch.setenv("RTN_KERNEL", request.param)
+    return request.param
+
+
 def _blocks(f, jac):
     return {"f": f, "A": jac[:, :, :13], "B": jac[:, :, 13:]}
 
@@ -42,15 +49,15 @@ def test_cfg1_tanh_2x64():
     _check([17, 64, 64, 6], "tanh", 10)
 
 
-def test_cfg2_silu_5x256_latency_shape():
+def test_cfg2_silu_5x256_latency_shape(kernel):
     _check([17] + [256] * 5 + [6], "silu", 20)
 
 
-def test_cfg3_silu_12x512():
+def test_cfg3_silu_12x512(kernel):
     _check([17] + [512] * 12 + [6], "silu", 20)
 
 
-def test_ragged_tile_counts():
+def test_ragged_tile_counts(kernel):
     # K not a multiple of the nodes-per-tile, and more tiles than SMs
     for k in (1, 3, 5, 7, 13, 601):
         _check([17, 128, 128, 6], "silu", k)
@@ -64,7 +71,7 @@ def test_reference_shapes_small_nets():
     _check([3, 10, 2], "relu", 20)
 
 
-def test_batch_rows_equal_single_calls():
+def test_batch_rows_equal_single_calls(kernel):
     # neural.hpp:65-67 contract within the device kernel family: a row of a
     # batch is bit-identical to the single-node call.
     from paper_2203_07747_b200 import mlp_batched_eval, mlp_jacobian, mlp_forward, EvalOrder
@@ -79,5 +86,5 @@ def test_batch_rows_equal_single_calls():
     assert np.array_equal(b.values[0], b.values[12])
 
 
-def test_throughput_shape_cfg4_subset():
+def test_throughput_shape_cfg4_subset(kernel):
     _check([17] + [256] * 5 + [6], "silu", 4096)
