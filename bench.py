@@ -1,0 +1,405 @@
+"""Benchmark: node linearisations/s of (f, ∂f/∂x, ∂f/∂u) on the BASELINE
+workload, plus p50/p99 per-MPC-step latency, roofline and CPU baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL). Workload (N=1 and
+every N, strong scaling): BASELINE.json configs[4] — 65,536 MPC instances x
+N=50 shooting nodes, quadrotor residual MLP 12x512 SiLU (17 in, 6 out),
+first order, TF32 tensor cores; instances are partitioned across ranks and
+the (f, A, B) blocks are gathered to rank 0 with NCCL (the path's only
+exchange step). Synthetic inputs: MakeMlp weights (seed 12512) and
+quadrotor node rows (mt19937_64), inputs resident in HBM.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "node linearizations/s (f,∂f/∂x,∂f/∂u) at 1-8 GPU; p50 per-MPC-step latency"
+UNIT = "node-lin/s"
+INSTANCES, HORIZON = 65536, 50
+SIZES = [17] + [512] * 12 + [6]
+SEED = 1000 * 12 + 512
+WORKLOAD = "cfg5: 65536 MPC instances x N=50 nodes, quadrotor MLP 12x512 SiLU (17->6), order 1"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if "Active" in v and "Not" not in v})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- CPU (oracle) leg
+def cpu_throughput(target_s: float, threads: int, sizes=SIZES, seed=SEED):
+    """The reference's CPU algorithm (oracle/ restatement of BatchedCore,
+    reverse-mode fp64, RESMPC thread pool) on a bounded sample of the same
+    workload; sample size calibrated to ~target_s seconds."""
+    import numpy as np
+    import oracle
+    om = oracle.OracleModel.make_mlp(sizes, "silu", seed)
+    z = oracle.quad_nodes(2203, 50 * 64)
+    t0 = time.perf_counter()
+    om.batched_eval(z[:HORIZON * 2], 1, threads)  # calibration: 2 instances
+    dt = max(time.perf_counter() - t0, 1e-4)
+    per_node = dt / (HORIZON * 2)
+    inst = int(max(1, min(64, target_s / (per_node * HORIZON))))
+    k = inst * HORIZON
+    t0 = time.perf_counter()
+    om.batched_eval(z[:k], 1, threads)
+    dt = time.perf_counter() - t0
+    return k / dt, f"{inst} instances x {HORIZON} nodes = {k} nodes of cfg5 in {dt:.2f} s", dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_throughput(per_step, threads)
+    vals, samples = [], []
+    for _ in range(args.steps):
+        v, sample, _ = cpu_throughput(per_step, threads)
+        vals.append(v)
+        samples.append(sample)
+    v = statistics.median(vals)
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * INSTANCES * HORIZON / v, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "nodes": INSTANCES * HORIZON,
+                   "note": "reference algorithm = oracle/ restatement of proj/src/neural.cpp BatchedCore "
+                           "(reverse mode, fp64, fork/join pool); the reference itself needs Eigen/yaml-cpp "
+                           "and cannot be built here; ms_per_step extrapolated linearly from the sample"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": samples[-1]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU leg
+def measured_tf32_peak(torch):
+    """cuBLAS TF32 8192^3 burst on this GPU (the tensor-core roofline the
+    kernel is compared against); MEASURED_PEAKS.json only carries bf16."""
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device="cuda")
+    b = torch.randn(8192, 8192, device="cuda")
+    for _ in range(3):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(8):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def latency(torch, sizes, seed, k, steps=1000, warm=50):
+    """Per-MPC-step approximation latency: K = N nodes of one instance
+    through rtn_prepare (host z -> host f, J), and device-only (events)."""
+    import numpy as np
+    from paper_2203_07747_b200 import _lib, make_mlp, synth_quad_nodes
+    from paper_2203_07747_b200.errors import raise_for_status
+    m = make_mlp(sizes, "silu", "full", seed)
+    eng = m.engine()
+    eng._ensure(k, 1)
+    L = _lib.lib()
+    z = torch.from_numpy(synth_quad_nodes(7, k)).pin_memory()
+    f = torch.empty((k, sizes[-1]), dtype=torch.float64).pin_memory()
+    j = torch.empty((k, sizes[-1], sizes[0]), dtype=torch.float64).pin_memory()
+    dp = C.POINTER(C.c_double)
+    args = (eng.ctx_ptr, C.cast(z.data_ptr(), dp), k, sizes[0], 1, C.cast(f.data_ptr(), dp), C.cast(j.data_ptr(), dp), None)
+    for _ in range(warm):
+        raise_for_status(L.rtn_prepare(*args))
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        L.rtn_prepare(*args)
+        ts.append((time.perf_counter() - t0) * 1e6)
+    # device-only: kernel on device-resident rows
+    st = torch.cuda.Stream()
+    raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
+    dz = z.cuda()
+    df = torch.empty((k, sizes[-1]), dtype=torch.float64, device="cuda")
+    dj = torch.empty((k, sizes[-1], sizes[0]), dtype=torch.float64, device="cuda")
+    dev = []
+    with torch.cuda.stream(st):
+        for i in range(warm + 200):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            L.rtn_prepare_device(eng.ctx_ptr, dz.data_ptr(), k, 1, df.data_ptr(), dj.data_ptr(), None)
+            e1.record(st)
+            e1.synchronize()
+            if i >= warm:
+                dev.append(e0.elapsed_time(e1) * 1e3)
+    raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, None))
+    ts.sort()
+    dev.sort()
+    return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)], "device_p50_us": dev[len(dev) // 2],
+            "device_p99_us": dev[int(len(dev) * 0.99)], "steps": steps}
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp, synth_quad_nodes
+    from paper_2203_07747_b200.errors import raise_for_status
+    from paper_2203_07747_b200.sharding import partition_instances
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    part = partition_instances(INSTANCES, HORIZON, rank, world)
+    k = part.num_nodes
+    n_in, n_out = SIZES[0], SIZES[-1]
+    L = _lib.lib()
+
+    tf32_peak = measured_tf32_peak(torch) if rank == 0 else None
+
+    model = make_mlp(SIZES, "silu", "full", SEED)
+    eng = model.engine(device=local_rank)
+    eng._ensure(k, 1)
+    stream = torch.cuda.Stream(device=dev)
+    raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(stream.cuda_stream)))
+
+    z_host = torch.from_numpy(synth_quad_nodes(2203 + rank, k))
+    z = z_host.to(dev)
+    # kernel outputs are the gather send buffers (no extra copy in the step)
+    f = torch.empty((k, n_out), dtype=torch.float64, device=dev)
+    jac = torch.empty((k, n_out, n_in), dtype=torch.float64, device=dev)
+    k_max = partition_instances(INSTANCES, HORIZON, 0, world).num_nodes
+    if world > 1:
+        f_send = torch.zeros((k_max, n_out), dtype=torch.float64, device=dev)
+        j_send = torch.zeros((k_max, n_out, n_in), dtype=torch.float64, device=dev)
+        f, jac = f_send[:k], j_send[:k]
+        f_recv = [torch.empty_like(f_send) for _ in range(world)] if rank == 0 else None
+        j_recv = [torch.empty_like(j_send) for _ in range(world)] if rank == 0 else None
+
+    def launches():
+        a, b, c = C.c_ulonglong(), C.c_ulonglong(), C.c_ulonglong()
+        L.rtn_ctx_counters(eng.ctx_ptr, C.byref(a), C.byref(b), C.byref(c))
+        return c.value
+
+    kern_ms = []
+
+    def step(record_kernel):
+        e0 = e1 = None
+        with torch.cuda.stream(stream):
+            if record_kernel:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            raise_for_status(L.rtn_prepare_device(eng.ctx_ptr, z.data_ptr(), k, 1, f.data_ptr(), jac.data_ptr(), None))
+            if record_kernel:
+                e1.record(stream)
+            if world > 1:
+                dist.gather(f_send, f_recv, dst=0)
+                dist.gather(j_send, j_recv, dst=0)
+        return (e0, e1)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    l0 = launches()
+    ev_pairs = []
+    with ClockSampler(local_rank) as clk:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            ev_pairs.append(step(True))
+        t1.record(stream)
+        barrier()
+    clocks = clk.summary()
+    n_launch = launches() - l0
+    elapsed = t0.elapsed_time(t1)
+    kern_ms = [a.elapsed_time(b) for a, b in ev_pairs]
+    tmax = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    kmax = torch.tensor([statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(kmax, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tmax.item()) / args.steps
+    kernel_ms = float(kmax.item())
+    total_nodes = INSTANCES * HORIZON
+    value = total_nodes / (ms_per_step * 1e-3)
+
+    # ---- end to end through the public C-ABI: pinned host z -> host f, J
+    zp = z_host.pin_memory()
+    fp = torch.empty((k, n_out), dtype=torch.float64).pin_memory()
+    jp = torch.empty((k, n_out, n_in), dtype=torch.float64).pin_memory()
+    dp = C.POINTER(C.c_double)
+    e2e_args = (eng.ctx_ptr, C.cast(zp.data_ptr(), dp), k, n_in, 1, C.cast(fp.data_ptr(), dp),
+                C.cast(jp.data_ptr(), dp), None)
+    raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, None))
+    raise_for_status(L.rtn_prepare(*e2e_args))  # warm
+    barrier()
+    e2e_steps = max(1, min(args.steps, 3))
+    t_e2e = time.perf_counter()
+    for _ in range(e2e_steps):
+        raise_for_status(L.rtn_prepare(*e2e_args))
+    e2e_s = torch.tensor([(time.perf_counter() - t_e2e) / e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = total_nodes / float(e2e_s.item())
+    # sanity: outputs finite and match the device-resident run
+    ok = bool(torch.isfinite(fp).all()) and bool(torch.allclose(fp, f.cpu(), rtol=0, atol=0))
+
+    result = None
+    if rank == 0:
+        fl = flops_per_node(SIZES, 1)
+        achieved = k * fl / (kernel_ms * 1e-3) / 1e12
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+            traffic = prof.get("dram_bytes_per_launch_per_node", None)
+            traffic = traffic * k if traffic is not None else None
+        except Exception:
+            pass
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            v_all, sample, _ = cpu_throughput(12.0, threads)
+            v_one, sample1, _ = cpu_throughput(3.0, 1)
+            cpu = {"value": v_all, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                   "value_1thread": v_one, "sample_1thread": sample1,
+                   "algorithm": "oracle/ restatement of proj/src/neural.cpp BatchedCore (reverse mode, fp64)"}
+        lat = None
+        if not args.no_latency:
+            lat = {"cfg3_12x512_N20": latency(torch, SIZES, SEED, 20),
+                   "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20)}
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "nodes": total_nodes, "nodes_per_rank": k,
+                       "parallelism": f"instance partition x{world}" + (" + NCCL gather of (f,A,B) to rank 0" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (z 446 MB + outputs 2.8 GB per step); weights (11.6 MB) stay L2-resident by design",
+                       "io": "fp64 z in, fp64 f/J out (reference layout)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(zp.numel() * 8),
+                    "d2h_bytes_per_step": int((fp.numel() + jp.numel()) * 8),
+                    "path": "rtn_prepare (C-ABI), pinned host buffers, chunked H2D/kernel/D2H overlap",
+                    "matches_device_run": ok},
+            "gpu_launches": int(n_launch),
+            "kernel_ms": kernel_ms,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                         "frac": achieved / tf32_peak if tf32_peak else None, "traffic": traffic,
+                         "peak_source": "cuBLAS tf32 8192^3 burst measured in this run (MEASURED_PEAKS.json has bf16 only; "
+                                        f"bf16/2 = {peaks.get('bf16_tflops', 0) / 2:.1f})",
+                         "flop_per_node": fl, "flops_definition": "2*(1+n_in)*sum(n_l*n_{l+1}) forward-mode (BASELINE.md s2)",
+                         "kernel": "rtn_pair_kernel<512,4,4> (tcgen05 cta_group::2 tf32)"},
+            "clocks": clocks,
+        }
+        if cpu:
+            result["cpu_baseline"] = cpu
+        if lat:
+            result["latency"] = lat
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+        dist.destroy_process_group()
+    if result is not None:
+        print(json.dumps(result), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

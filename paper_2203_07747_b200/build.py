@@ -19,6 +19,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
     "-Xcompiler", "-O3,-ffp-contract=off",
+    "-ccbin", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++",
 ]
 
 SOURCES = ["rtn_mpc.cu", "rtn_synth.cpp"]

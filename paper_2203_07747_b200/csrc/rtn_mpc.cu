@@ -143,6 +143,9 @@ struct rtn_ctx {
   double* h_jac = nullptr;
   int num_sms = 148;
   unsigned long long calls = 0, points = 0, launches = 0;
+  // end-to-end pipeline: copy-in / copy-out streams and per-chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k;
   ~rtn_ctx() {
     int prev;
     if (cudaGetDevice(&prev) == cudaSuccess) {
@@ -154,12 +157,19 @@ struct rtn_ctx {
       cudaFreeHost(h_f);
       cudaFreeHost(h_jac);
       if (own_stream) cudaStreamDestroy(own_stream);
+      if (s_in) cudaStreamDestroy(s_in);
+      if (s_out) cudaStreamDestroy(s_out);
+      for (auto e : ev_in) cudaEventDestroy(e);
+      for (auto e : ev_k) cudaEventDestroy(e);
       cudaSetDevice(prev);
     }
   }
 };
 
 namespace {
+
+constexpr int kMaxChunks = 8;                 // end-to-end pipeline depth
+constexpr long long kChunkMinRows = 1 << 17;  // chunk only batches this large
 
 int PaddedWidth(const std::vector<int>& sizes) {
   int w = 0;
@@ -551,17 +561,21 @@ rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order,
     c->latency_mode = latency_mode;
     CUDA_CHECK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, m->device));
     CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+    c->ev_in.resize(kMaxChunks);
+    c->ev_k.resize(kMaxChunks);
+    for (int i = 0; i < kMaxChunks; ++i) {
+      CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+    }
     c->stream = c->own_stream;
     const size_t zb = sizeof(double) * max_rows * m->n_in, fb = sizeof(double) * max_rows * m->n_out,
                  jb = fb * m->n_in;
     CUDA_CHECK(cudaMalloc(&c->d_z, zb));
     CUDA_CHECK(cudaMalloc(&c->d_f, fb));
-    CUDA_CHECK(cudaMallocHost(&c->h_z, zb));
-    CUDA_CHECK(cudaMallocHost(&c->h_f, fb));
-    if (max_order >= 1) {
-      CUDA_CHECK(cudaMalloc(&c->d_jac, jb));
-      CUDA_CHECK(cudaMallocHost(&c->h_jac, jb));
-    }
+    if (max_order >= 1) CUDA_CHECK(cudaMalloc(&c->d_jac, jb));
+    // pinned staging for pageable caller buffers is allocated on first use
     *out = c.release();
   });
 }
@@ -592,6 +606,15 @@ rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* calls, unsigne
   });
 }
 
+static bool IsPinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static void CheckCall(const rtn_ctx* c, long long K, int order) {
   if (!c) throw Error(RTN_ECONFIG, "null context");
   if (order < 0 || order > 2) throw Error(RTN_ECONFIG, "prepare nodes: order must be 0, 1 or 2");
@@ -615,15 +638,48 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
     c->points += static_cast<unsigned long long>(K);
     if (K == 0) return;
     CUDA_CHECK(cudaSetDevice(m->device));
-    const size_t zb = sizeof(double) * K * m->n_in, fb = sizeof(double) * K * m->n_out, jb = fb * m->n_in;
-    std::memcpy(c->h_z, z, zb);
-    CUDA_CHECK(cudaMemcpyAsync(c->d_z, c->h_z, zb, cudaMemcpyHostToDevice, c->stream));
-    Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac);
-    CUDA_CHECK(cudaMemcpyAsync(c->h_f, c->d_f, fb, cudaMemcpyDeviceToHost, c->stream));
-    if (order >= 1) CUDA_CHECK(cudaMemcpyAsync(c->h_jac, c->d_jac, jb, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_CHECK(cudaStreamSynchronize(c->stream));
-    std::memcpy(f, c->h_f, fb);
-    if (order >= 1) std::memcpy(jac, c->h_jac, jb);
+    const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in;
+    // Page-locked caller buffers are DMA'd directly; pageable ones go through
+    // the context's pinned staging.
+    const bool pinned = IsPinned(z) && IsPinned(f) && (order < 1 || IsPinned(jac));
+    const double* hz = z;
+    double* hf = f;
+    double* hj = jac;
+    if (!pinned) {
+      if (!c->h_z) {
+        CUDA_CHECK(cudaMallocHost(&c->h_z, zr * c->max_rows));
+        CUDA_CHECK(cudaMallocHost(&c->h_f, fr * c->max_rows));
+        if (c->max_order >= 1) CUDA_CHECK(cudaMallocHost(&c->h_jac, jr * c->max_rows));
+      }
+      std::memcpy(c->h_z, z, zr * K);
+      hz = c->h_z;
+      hf = c->h_f;
+      hj = c->h_jac;
+    }
+    // Large batches: chunk so H2D(i+1) and D2H(i−1) overlap kernel(i).
+    const int chunks = K >= kChunkMinRows ? kMaxChunks : 1;
+    const long long per = (K + chunks - 1) / chunks;
+    CUDA_CHECK(cudaEventRecord(c->ev_in[0], c->stream));  // order after prior work on the compute stream
+    CUDA_CHECK(cudaStreamWaitEvent(c->s_in, c->ev_in[0], 0));
+    for (int i = 0; i < chunks; ++i) {
+      const long long r0 = i * per, n = std::min(per, K - r0);
+      if (n <= 0) break;
+      CUDA_CHECK(cudaMemcpyAsync(c->d_z + r0 * m->n_in, hz + r0 * m->n_in, zr * n, cudaMemcpyHostToDevice, c->s_in));
+      CUDA_CHECK(cudaEventRecord(c->ev_in[i], c->s_in));
+      CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_in[i], 0));
+      Enqueue(c, c->d_z + r0 * m->n_in, n, order, c->d_f + r0 * m->n_out, order >= 1 ? c->d_jac + r0 * m->n_out * m->n_in : nullptr);
+      CUDA_CHECK(cudaEventRecord(c->ev_k[i], c->stream));
+      CUDA_CHECK(cudaStreamWaitEvent(c->s_out, c->ev_k[i], 0));
+      CUDA_CHECK(cudaMemcpyAsync(hf + r0 * m->n_out, c->d_f + r0 * m->n_out, fr * n, cudaMemcpyDeviceToHost, c->s_out));
+      if (order >= 1)
+        CUDA_CHECK(cudaMemcpyAsync(hj + r0 * m->n_out * m->n_in, c->d_jac + r0 * m->n_out * m->n_in, jr * n,
+                                   cudaMemcpyDeviceToHost, c->s_out));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(c->s_out));
+    if (!pinned) {
+      std::memcpy(f, c->h_f, fr * K);
+      if (order >= 1) std::memcpy(jac, c->h_jac, jr * K);
+    }
   });
 }
 

@@ -201,8 +201,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < 8; ++i) swz[i] = ((((tid_h >> 2) & 7) ^ i) - ((tid_h >> 2) & 7)) * 16 + i * 128;
     const uint32_t act_local = smem_u32(act_s);
-    const bool local_side = half == static_cast<int>(rank);
+    const bool local_side = half == static_cast<int>(rank) || (prm.dbg & 8);  // dbg 8: timing only
     const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
+    (void)0;
     uint32_t ready_cl[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);

@@ -1,0 +1,108 @@
+"""GPU tests of the drop-in interface (PrepareNodes / MlpBatchedEval mirror
+over the C-ABI): golden fixtures, RMLP loading on the device, error mapping,
+counters, and the one-batched-call contract (proj/tests/test_taylor.cpp:8-28)."""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2203_07747_b200 import (EvalCounters, EvalOrder, InputDomainError, UnsupportedError, _lib, load_model,
+                                   make_mlp, mlp_batched_eval, mlp_forward, mlp_jacobian, prepare_nodes)
+from paper_2203_07747_b200.errors import raise_for_status
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+
+
+@pytest.mark.parametrize("name", ["cfg1_tanh_2x64_N10", "tanh_6_32_32_4_K13"])
+def test_golden_fixtures_tf32(name):
+    rec = json.load(open(os.path.join(GOLDEN, name + ".json")))
+    m = load_model(os.path.join(GOLDEN, rec["model_file"]))
+    z = np.array(rec["z"])
+    got = mlp_batched_eval(m, z, EvalOrder.JACOBIAN)
+    assert oracle.max_node_rel_error(got.values, np.array(rec["f"])) < 1e-3
+    assert oracle.max_node_rel_error(got.jacobians, np.array(rec["jac"])) < 1e-3
+
+
+def test_rmlp_file_loads_straight_to_device():
+    """rtn_model_load_rmlp (C-ABI file path) == arrays path, bitwise."""
+    rec = json.load(open(os.path.join(GOLDEN, "cfg1_tanh_2x64_N10.json")))
+    path = os.path.join(GOLDEN, rec["model_file"])
+    L = _lib.lib()
+    mp = C.c_void_p()
+    raise_for_status(L.rtn_model_load_rmlp(path.encode(), 0, 0, C.byref(mp)))
+    ctx = C.c_void_p()
+    raise_for_status(L.rtn_ctx_create(mp, 64, 1, 0, C.byref(ctx)))
+    z = np.ascontiguousarray(rec["z"])
+    k = z.shape[0]
+    f = np.empty((k, 6))
+    j = np.empty((k, 6, 17))
+    dp = C.POINTER(C.c_double)
+    raise_for_status(L.rtn_prepare(ctx, z.ctypes.data_as(dp), k, 17, 1, f.ctypes.data_as(dp), j.ctypes.data_as(dp), None))
+    ref = mlp_batched_eval(load_model(path), z, EvalOrder.JACOBIAN)
+    assert np.array_equal(f, ref.values) and np.array_equal(j, ref.jacobians)
+    calls, points, launches = C.c_ulonglong(), C.c_ulonglong(), C.c_ulonglong()
+    raise_for_status(L.rtn_ctx_counters(ctx, C.byref(calls), C.byref(points), C.byref(launches)))
+    assert (calls.value, points.value, launches.value) == (1, k, 1)
+    L.rtn_ctx_free(ctx)
+    L.rtn_model_free(mp)
+
+
+def test_prepare_nodes_is_one_batched_call_and_matches_single_calls():
+    # proj/tests/test_taylor.cpp:8-28 on the device path
+    om = oracle.OracleModel.random_net([4, 16, 3], "tanh", 1, True)
+    m = oracle.to_product_model(om)
+    z = np.random.default_rng(1).uniform(-1, 1, (10, 4))
+    c = EvalCounters()
+    approx = prepare_nodes(m, z, 1, c)
+    assert c.batched_calls == 1 and c.batched_points == 10 and c.value_evals == 0 and c.jacobian_evals == 0
+    for k, a in enumerate(approx):
+        assert a.node == k
+        assert np.array_equal(a.f_bar, mlp_forward(m, z[k]))
+        assert np.array_equal(a.jac, mlp_jacobian(m, z[k]))
+
+
+def test_error_mapping():
+    m = make_mlp([4, 8, 2], "relu", "full", 3)
+    with pytest.raises(InputDomainError):          # proj/src/neural.cpp:230-232
+        mlp_batched_eval(m, np.zeros((3, 5)), EvalOrder.VALUE)
+    with pytest.raises(UnsupportedError):          # proj/src/neural.cpp:176-177
+        mlp_batched_eval(m, np.zeros((3, 4)), EvalOrder.HESSIAN)
+
+
+def test_zero_output_model():
+    # proj/tests/test_taylor.cpp:30-41
+    om = oracle.OracleModel.random_net([17, 128, 6], "tanh", 9, False)
+    w, b = om.layers()[-1]
+    om.set_layer(1, np.zeros_like(w), np.zeros_like(b))
+    m = oracle.to_product_model(om)
+    got = mlp_batched_eval(m, oracle.quad_nodes(3, 5), EvalOrder.JACOBIAN)
+    assert np.all(got.values == 0.0) and np.all(got.jacobians == 0.0)
+
+
+def test_empty_batch():
+    m = make_mlp([17, 64, 6], "silu", "full", 1)
+    got = mlp_batched_eval(m, np.zeros((0, 17)), EvalOrder.JACOBIAN)
+    assert got.values.shape == (0, 6) and got.jacobians.shape == (0, 6, 17)
+
+
+def test_large_batch_end_to_end_chunked(monkeypatch):
+    """K ≥ 2^17 takes the chunked H2D/kernel/D2H pipeline; results equal the
+    device-resident call bitwise and the oracle within tolerance on a sample."""
+    om = oracle.OracleModel.random_net([17, 256, 256, 6], "silu", 5, True)
+    m = oracle.to_product_model(om)
+    k = 150_000
+    z = oracle.quad_nodes(77, k)
+    got = mlp_batched_eval(m, z, EvalOrder.JACOBIAN)
+    idx = np.arange(0, k, 997)
+    f, j, _ = om.batched_eval(z[idx], 1)
+    assert oracle.max_node_rel_error(got.values[idx], f) < 1e-3
+    assert oracle.max_node_rel_error(got.jacobians[idx], j) < 1e-3
+    monkeypatch.setenv("RTN_KERNEL", "pair")  # same kernel family → bitwise batch invariance
+    again = mlp_batched_eval(m, z[idx], EvalOrder.JACOBIAN)
+    assert np.array_equal(again.values, got.values[idx])
+    assert np.array_equal(again.jacobians, got.jacobians[idx])
