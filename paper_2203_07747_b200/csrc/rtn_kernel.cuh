@@ -55,6 +55,7 @@ struct KParams {
   int n_in, n_out, n_hidden, act, order;
   int P;             // nodes per tile (power of two)
   int nt;            // tile rows used (= roundup8(P·(1+n_in))), MMA N
+  unsigned long long* trace;  // optional event timestamps (RTN_TRACE), pair 0 only
   int dbg;           // perf-isolation switches (RTN_DEBUG): 1 = MMA ignores act_ready, 2 = 1 KB weight copies
   const uint8_t* w_hidden;  // (n_hidden-1) x NMB x NKC blocks of kStageBytes
   const uint8_t* w_last;    // NKC blocks of kLastBlockBytes
@@ -66,6 +67,12 @@ struct KParams {
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -82,6 +89,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+
+// Long-suspend wait for threads with nothing else to do (epilogue warps
+// waiting on the tensor core): the hint lets the scheduler park the warp until
+// the phase completes instead of re-polling, keeping issue slots free for the
+// producer and MMA warps that share the sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 
@@ -380,4 +401,34 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
+}  // namespace rtn
+
+namespace rtn {
+// One weight stage of a pair MMA layer in a single asm block: 4 K-steps
+// (32 B each: tf32 K=8) with one elect, then a multicast commit of the stage's
+// empty barrier (and, if `bar2` is non-zero, a second barrier such as in_free
+// or tmem_full). Keeping the 4 MMAs + commit together lets ptxas convert the
+// operands to uniform registers once per stage instead of once per MMA.
+__device__ __forceinline__ void mma4_tf32_pair_commit(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                      uint32_t accumulate, uint32_t bar, uint32_t bar2) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b16 m;\n\t"
+      "mov.b16 m, 3;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a3, b3, %3, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], m;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], m;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2)
+      : "memory");
+}
 }  // namespace rtn

@@ -168,6 +168,7 @@ struct rtn_ctx {
 
 namespace {
 
+unsigned long long* trace_buf = nullptr;  // RTN_TRACE device buffer
 constexpr int kMaxChunks = 8;                 // end-to-end pipeline depth
 constexpr long long kChunkMinRows = 1 << 17;  // chunk only batches this large
 
@@ -412,10 +413,10 @@ void LaunchP(const rtn::KParams& prm, int grid, cudaStream_t st) {
   }
 }
 
-template <int WP, int NS, int P>
+template <int WP, int NS, int P, int NTC = 80>
 void LaunchPairT(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStream_t st) {
-  using Cfg = rtn::PairCfg<WP, NS, P>;
-  auto kern = rtn::rtn_pair_kernel<WP, NS, P>;
+  using Cfg = rtn::PairCfg<WP, NS, P, NTC>;
+  auto kern = rtn::rtn_pair_kernel<WP, NS, P, NTC>;
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
@@ -436,17 +437,24 @@ void LaunchPairP(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStre
   }
 }
 
-// Kernel choice: the pair kernel needs a padded width of 256/512 and enough
-// pair tiles to fill the machine; small batches (latency mode) use the
-// single-CTA kernel, which spreads 4 nodes per SM. RTN_KERNEL=pair|single
-// forces one (tests use it to cover both paths).
-bool UsePair(const rtn_model* m, long long K, int P, int num_sms) {
-  if (!m->has_pair) return false;
+// Kernel choice (padded width 256/512; RTN_KERNEL=pair|latency|single forces one):
+//   throughput: pair kernel, P = 4 nodes per CTA (N = 144), when the batch
+//               fills at least half the pairs;
+//   latency   : pair kernel, P = 1 node per CTA (N = 48), one node per SM,
+//               deep weight pipeline — small batches (one MPC step, K = N);
+//   single    : one-CTA kernel (padded width 128, or forced).
+enum class Kern { kSingle, kPair, kLatency };
+Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
+  const bool lat_ok = m->has_pair && m->n_in + 1 <= 24;
   if (const char* e = std::getenv("RTN_KERNEL")) {
-    if (std::strcmp(e, "pair") == 0) return true;
-    if (std::strcmp(e, "single") == 0) return false;
+    if (std::strcmp(e, "pair") == 0 && m->has_pair) return Kern::kPair;
+    if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
+    if (std::strcmp(e, "single") == 0) return Kern::kSingle;
   }
-  return K >= static_cast<long long>(2 * P) * num_sms;
+  if (!m->has_pair) return Kern::kSingle;
+  if (K >= static_cast<long long>(P) * num_sms) return Kern::kPair;
+  if (lat_ok && K <= num_sms) return Kern::kLatency;
+  return Kern::kPair;
 }
 
 void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac) {
@@ -467,13 +475,29 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   if (prm.nt < 16) prm.nt = 16;
   prm.num_tiles = (K + prm.P - 1) / prm.P;
   if (const char* d = std::getenv("RTN_DEBUG")) prm.dbg = std::atoi(d);
+  if (std::getenv("RTN_TRACE")) {  // per-event timestamps of pair 0 (profiling aid)
+    if (!trace_buf) CUDA_CHECK(cudaMalloc(&trace_buf, 256 * 8));
+    CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 256 * 8, c->stream));
+    prm.trace = trace_buf;
+  }
   prm.w_hidden = static_cast<const uint8_t*>(m->d_w_hidden);
   prm.w_last = static_cast<const uint8_t*>(m->d_w_last);
   prm.w0 = m->d_w0;
   prm.b0 = m->d_b0;
   prm.bh = m->d_bh;
   prm.bl = m->d_bl;
-  if (UsePair(m, K, prm.P, c->num_sms)) {
+  const Kern kern = Choose(m, K, prm.P, c->num_sms);
+  if (kern == Kern::kLatency) {
+    prm.P = 1;
+    prm.nt = ((1 + m->n_in + 7) / 8) * 8;
+    prm.num_tiles = (K + 1) / 2;  // pair tiles of 2 nodes
+    const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+    if (m->wp == 256) LaunchPairT<256, 8, 1, 24>(prm, m, grid, c->stream);
+    else LaunchPairT<512, 8, 1, 24>(prm, m, grid, c->stream);
+    c->launches += 1;
+    return;
+  }
+  if (kern == Kern::kPair) {
     prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
     if (m->wp == 256) LaunchPairP<256, 8>(prm, m, grid, c->stream);
@@ -496,6 +520,13 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
 extern "C" {
 
 const char* rtn_last_error(void) { return g_err.c_str(); }
+
+// Profiling aid (not part of the C-ABI contract): copies the RTN_TRACE buffer
+// (256 globaltimer stamps of pair 0's first tile) after a synchronised call.
+int rtn_debug_trace(unsigned long long* out, int n) {
+  if (!trace_buf || n > 256) return 1;
+  return cudaMemcpy(out, trace_buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
 
 rtn_status rtn_model_load_rmlp(const char* path, int device, rtn_precision p, rtn_model** out) {
   return Guard([&] {

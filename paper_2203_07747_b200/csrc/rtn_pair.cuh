@@ -26,33 +26,36 @@
 
 namespace rtn {
 
-constexpr int kNTC = 80;            // max rows per CTA (pair N ≤ 160)
-constexpr int kTmemStride2 = 160;   // TMEM columns per 256-neuron block
+constexpr int kTmemStride2 = 160;   // TMEM columns per 256-neuron block (pair N ≤ 160)
 constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x 32 k
 
-template <int WP, int NSTAGE, int P>
+// NTC = operand row stride per CTA (max rows per CTA): 80 for throughput
+// tiles (P = 4 quadrotor nodes = 72 rows), 24 for latency tiles (P = 1).
+template <int WP, int NSTAGE, int P, int NTC>
 struct PairCfg {
   static constexpr int kNMB = WP / 256;  // 256-neuron blocks (pair M)
   static constexpr int kNKC = WP / 32;   // 32-wide k chunks
   static constexpr int kNG = WP / 128;   // 128-neuron K-groups (one per CTA per block)
-  static constexpr uint32_t kChunkStride = kNTC * 128;
+  static constexpr uint32_t kChunkStride = NTC * 128;
   static constexpr uint32_t kActBytes = kNKC * kChunkStride;
   static constexpr uint32_t kStageOff = kActBytes;
   static constexpr uint32_t kBarOff = kStageOff + NSTAGE * kStageBytes;
   static constexpr uint32_t kNumBars = 2 * NSTAGE + 13;
   static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
   static constexpr uint32_t kZsOff = kMiscOff + 16;
-  static constexpr uint32_t kSmemBytes = kZsOff + 2 * kNTC * 4 + 1024;
+  static constexpr uint32_t kSmemBytes = kZsOff + 2 * NTC * 4 + 1024;
   static_assert(kNMB >= 1 && kNMB <= 2, "pair kernel handles 256 or 512 padded width");
   static_assert(kNMB * kTmemStride2 <= 512, "TMEM capacity");
   static_assert(kSmemBytes <= 232448, "shared memory budget");
+  // the output layer's M = 128-row A reads run past the last chunk into the stage ring
+  static_assert((128 - NTC) * 128 <= NSTAGE * kStageBytes, "A-operand overrun must stay in smem");
 };
 
-template <int WP, int NSTAGE, int P>
+template <int WP, int NSTAGE, int P, int NTC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_pair_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
-  using C = PairCfg<WP, NSTAGE, P>;
+  using C = PairCfg<WP, NSTAGE, P, NTC>;
   constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -97,27 +100,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (prm.trace && pair == 0 && threadIdx.x == 0) {
+    prm.trace[196 + rank] = globaltimer();
+    prm.trace[250 + rank] = clock64();
+  }
 
+  static_assert(NKC % NSTAGE == 0, "every 256-block starts at stage 0 (static stage indices)");
   if (warp == 0) {
     // ===================== weight producer: 2-SM TMA, own 128-neuron half ====
+    // Chunk loops are fully unrolled: stage indices, phases and coordinates
+    // are compile-time, so this single warp is not instruction-latency bound
+    // at small N (scripts/mma_bench.cu variants).
     const uint64_t pol = l2_evict_last_policy();
-    int s = 0;
     uint32_t ph = 0;
+    const int yr = static_cast<int>(rank) * 128;
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
       for (int l = 0; l < n_mma_layers; ++l)
-        for (int mb = 0; mb < NMB; ++mb)
+        for (int mb = 0; mb < NMB; ++mb) {
+          const int y = l * WP + mb * 256 + yr;
+#pragma unroll
           for (int c = 0; c < NKC; ++c) {
-            mbar_wait(&empty[s], ph ^ 1);
-            if (leader) mbar_expect_tx_elect(&full[s], 2 * kStageBytes);
-            tma_load_2sm(stage_s + s * kStageBytes, &tmap_h, c * 32, l * WP + mb * 256 + static_cast<int>(rank) * 128,
-                         &full[s], pol);
-            if (++s == NSTAGE) { s = 0; ph ^= 1; }
+            const int st = c % NSTAGE;
+            mbar_wait(&empty[st], ph ^ 1);
+            if (leader) mbar_expect_tx_elect(&full[st], 2 * kStageBytes);
+            tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * 32, y, &full[st], pol);
+            if (st == NSTAGE - 1) ph ^= 1;
           }
+        }
+#pragma unroll
       for (int c = 0; c < NKC; ++c) {
-        mbar_wait(&empty[s], ph ^ 1);
-        if (leader) mbar_expect_tx_elect(&full[s], 2 * kLastHalfBytes);
-        tma_load_2sm(stage_s + s * kStageBytes, &tmap_l, c * 32, static_cast<int>(rank) * 8, &full[s], pol);
-        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+        const int st = c % NSTAGE;
+        mbar_wait(&empty[st], ph ^ 1);
+        if (leader) mbar_expect_tx_elect(&full[st], 2 * kLastHalfBytes);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * 32, static_cast<int>(rank) * 8, &full[st], pol);
+        if (st == NSTAGE - 1) ph ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -125,15 +141,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (leader) {
       const uint32_t idesc_h = idesc_tf32(256, 2 * ntc);
       const uint32_t idesc_o = idesc_tf32(256, kMaxOut);
-      const uint32_t act_addr = smem_u32(act_s);
-      const uint32_t stage_addr = smem_u32(stage_s);
-      int s = 0;
+      // descriptors advance by (bytes >> 4) in the start-address field
+      const uint64_t a0 = sw128_desc(smem_u32(stage_s));
+      const uint64_t b0 = sw128_desc(smem_u32(act_s));
+      constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4;
       uint32_t ph = 0, ar = 0;
       // Before the first MMA of a layer overwrites TMEM block 0, both CTAs must
       // have drained it: wait for K-groups 0 and 1 (one per CTA) up front.
-      auto wait_group = [&](int c) {
-        if ((c & 3) != 0) return;
-        const int g = c >> 2;
+      auto wait_group = [&](int g) {
+        if (prm.dbg & 128) return;  // dbg 128: stream only (timing)
         if (g == 0) {
           mbar_wait_cluster(&act_ready[0], ar & 1);
           if (NG > 1) mbar_wait_cluster(&act_ready[1], ar & 1);
@@ -146,42 +162,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int l = 0; l < n_mma_layers; ++l) {
 #pragma unroll 1
           for (int mb = 0; mb < NMB; ++mb) {
-#pragma unroll 1
-            for (int c = 0; c < NKC; ++c) {
-              if (mb == 0) wait_group(c);
-              mbar_wait(&full[s], ph);
-              tc_fence_after();
-              const uint64_t a = sw128_desc(stage_addr + s * kStageBytes);
-              const uint64_t b = sw128_desc(act_addr + c * C::kChunkStride);
+            const uint32_t d = tmem_base + mb * kTmemStride2;
+            if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2] = globaltimer();
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma_tf32_pair(tmem_base + mb * kTmemStride2, a + 2 * kk, b + 2 * kk, idesc_h, (c | kk) != 0);
-              mma_commit_pair(&empty[s]);
-              if (mb == NMB - 1 && (c & 3) == 3) mma_commit_pair(&in_free[c >> 2]);
-              if (++s == NSTAGE) { s = 0; ph ^= 1; }
+            for (int c = 0; c < NKC; ++c) {
+              const int st = c % NSTAGE;
+              if ((c & 3) == 0 && mb == 0) wait_group(c >> 2);
+              mbar_wait(&full[st], ph);
+              tc_fence_after();
+              // second commit: in_free after the last block consumed K-group c/4
+              const uint32_t bar2 = (mb == NMB - 1 && (c & 3) == 3) ? smem_u32(&in_free[c >> 2]) : 0u;
+              mma4_tf32_pair_commit(d, a0 + st * kStageD, b0 + c * kChunkD, idesc_h, c != 0, smem_u32(&empty[st]), bar2);
+              if (st == NSTAGE - 1) ph ^= 1;
             }
             mma_commit_pair(&tmem_full[mb]);
+            if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2 + 1] = globaltimer();
           }
           ++ar;
         }
         // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]; M = 2 x 128 rows, N = 16
-#pragma unroll 1
-        for (int c = 0; c < NKC; ++c) {
-          wait_group(c);
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint64_t a = sw128_desc(act_addr + c * C::kChunkStride);
-          const uint64_t b = sw128_desc(stage_addr + s * kStageBytes);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) mma_tf32_pair(tmem_base, a + 2 * kk, b + 2 * kk, idesc_o, (c | kk) != 0);
-          mma_commit_pair(&empty[s]);
-          if (++s == NSTAGE) { s = 0; ph ^= 1; }
+        for (int c = 0; c < NKC; ++c) {
+          const int st = c % NSTAGE;
+          if ((c & 3) == 0) wait_group(c >> 2);
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          mma4_tf32_pair_commit(tmem_base, b0 + c * kChunkD, a0 + st * kStageD, idesc_o, c != 0, smem_u32(&empty[st]), 0);
+          if (st == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_pair(tmem_last);
         ++ar;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && !(prm.dbg & 128)) {
     // ===================== epilogue (8 warps per CTA) ========================
     // Thread = one neuron (TMEM lane) of this CTA's 128-neuron half of a
     // 256-block; warp half h owns the rows of side h (the P nodes whose
@@ -219,10 +232,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int p = 0; p < P; ++p) v[p] = to_tf32(val[p]);
       if (no_pad) {
 #pragma unroll
-        for (int i = P; i < kNTC; ++i) v[i] = to_tf32(v[i] * sp[i % P]);
+        for (int i = P; i < NTC; ++i) v[i] = to_tf32(v[i] * sp[i % P]);
       } else {
 #pragma unroll
-        for (int i = P; i < kNTC; ++i) v[i] = i < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
+        for (int i = P; i < NTC; ++i) v[i] = i < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
       }
     };
     // Store one neuron column (rows 0..ntc-1) of one side into its operand buffer.
@@ -230,11 +243,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t base = side_base + sw128_offset(0, j, C::kChunkStride);
       if (local_side) {
 #pragma unroll
-        for (int i = 0; i < kNTC; ++i)
+        for (int i = 0; i < NTC; ++i)
           if ((i & ~7) < ntc) st_shared_f32(base + (i >> 3) * 1024 + swz[i & 7], v[i]);
       } else {
 #pragma unroll
-        for (int i = 0; i < kNTC; ++i)
+        for (int i = 0; i < NTC; ++i)
           if ((i & ~7) < ntc) st_cluster_f32(base + (i >> 3) * 1024 + swz[i & 7], v[i]);
       }
     };
@@ -250,30 +263,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
       const float bj = __ldg(prm.bh + l * WP + j);
       const uint32_t ts = tmem_base + lane_base + mb * kTmemStride2 + half * ntc;
-      mbar_wait(&tmem_full[mb], hl & 1);
+      mbar_wait_sleep(&tmem_full[mb], hl & 1);
       tc_fence_after();
+      const bool tr = prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0;
+      unsigned long long* tp = tr ? prm.trace + 64 + rank * 64 + (l * 2 + mb) * 3 : nullptr;
+      if (tr) tp[0] = globaltimer();
       if (prm.dbg & 4) {
-        mbar_wait(&in_free[grp], hl & 1);
+        mbar_wait_sleep(&in_free[grp], hl & 1);
         tc_fence_before();
         publish(grp);
         return;
       }
-      float v[kNTC];
+      float v[NTC];
 #pragma unroll
-      for (int c0 = 0; c0 < kNTC; c0 += 8)
+      for (int c0 = 0; c0 < NTC; c0 += 8)
         if (c0 < ntc) tmem_ld8(ts + c0, v + c0);
       tmem_ld_wait();
       tc_fence_before();
       scale_side(v, bj);
-      mbar_wait(&in_free[grp], hl & 1);
+      mbar_wait_sleep(&in_free[grp], hl & 1);
+      if (tr) tp[1] = globaltimer();
       store_side(v, j);
       publish(grp);
+      if (tr) tp[2] = globaltimer();
     };
 
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
       const long long node0 = tile * (2 * P);
       if (tiles_done > 0) {
-        mbar_wait(tmem_last, (tiles_done - 1) & 1);
+        mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
         tc_fence_after();
       }
       // stage z of both sides' nodes (2P) for layer 0
@@ -295,21 +313,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[(half * P + p) * n_in + k], pre);
           act_fwd(act, pre, val[p], sp[p]);
         }
-        float v[kNTC];
+        float v[NTC];
 #pragma unroll
-        for (int i = 0; i < kNTC; ++i) {
+        for (int i = 0; i < NTC; ++i) {
           if (i < P) v[i] = to_tf32(val[i]);
           else v[i] = i < rows_used ? to_tf32(sp[i % P] * __ldg(w0r + (i - P) / P)) : 0.0f;
         }
         store_side(v, j);
         publish(g);
       }
+      if (prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0) prm.trace[192 + rank] = globaltimer();
       // ---- hidden layers
       for (int l = 0; l < n_mma_layers; ++l, ++hl)
         for (int mb = 0; mb < NMB; ++mb) do_block(mb, l);
       // ---- output layer: this CTA's rows in its TMEM lanes, outputs in columns 0..15
-      mbar_wait(tmem_last, tiles_done & 1);
+      mbar_wait_sleep(tmem_last, tiles_done & 1);
       tc_fence_after();
+      if (prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0) prm.trace[194 + rank] = globaltimer();
       if (half == 0) {
         float o[16];
         tmem_ld16(tmem_base + lane_base, o);
@@ -330,6 +350,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
     }
+  }
+  if (prm.trace && pair == 0 && threadIdx.x == 0) {
+    prm.trace[252 + rank] = globaltimer();
+    prm.trace[254 + rank] = clock64();
   }
   tc_fence_before();
   cluster_sync();

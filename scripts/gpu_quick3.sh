@@ -1,0 +1,8 @@
+timeout 600 python -m pytest tests -q -m gpu -x 2>&1 | tail -3
+timeout 60 python scripts/trace_latency.py 2>&1 | sed -n 2,5p
+timeout 200 python scripts/perf_probe.py 2>&1 | grep -v "K=20"
+timeout 300 python - <<'PY'
+import sys, json; sys.path.insert(0,'.')
+import torch, bench
+print(json.dumps({"cfg3": bench.latency(torch, bench.SIZES, bench.SEED, 20), "cfg2": bench.latency(torch, [17]+[256]*5+[6], 5256, 20)}))
+PY

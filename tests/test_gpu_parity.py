@@ -15,9 +15,9 @@ TF32_TOL = 1e-3
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["single", "pair"])
+@pytest.fixture(params=["single", "pair", "latency"])
 def kernel(request, monkeypatch):
-    """Both device kernels: single-CTA (latency/small K) and CTA-pair (throughput)."""
+    """Every device kernel: single-CTA, CTA-pair throughput (P=4) and CTA-pair latency (P=1)."""
     monkeypatch.setenv("RTN_KERNEL", request.param)
     return request.param
 
