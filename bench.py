@@ -172,7 +172,7 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50):
     from paper_2203_07747_b200 import _lib, make_mlp, synth_quad_nodes
     from paper_2203_07747_b200.errors import raise_for_status
     m = make_mlp(sizes, "silu", "full", seed)
-    eng = m.engine()
+    eng = m.engine(latency_mode=1)  # graph-captured H2D -> kernel -> D2H per step
     eng._ensure(k, 1)
     L = _lib.lib()
     z = torch.from_numpy(synth_quad_nodes(7, k)).pin_memory()

@@ -146,6 +146,13 @@ struct rtn_ctx {
   // end-to-end pipeline: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_k;
+  // latency mode: one captured graph (H2D, kernel, D2H) per (K, order)
+  struct Graph {
+    long long K;
+    int order;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Graph> graphs;
   ~rtn_ctx() {
     int prev;
     if (cudaGetDevice(&prev) == cudaSuccess) {
@@ -161,6 +168,7 @@ struct rtn_ctx {
       if (s_out) cudaStreamDestroy(s_out);
       for (auto e : ev_in) cudaEventDestroy(e);
       for (auto e : ev_k) cudaEventDestroy(e);
+      for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
       cudaSetDevice(prev);
     }
   }
@@ -170,6 +178,7 @@ namespace {
 
 unsigned long long* trace_buf = nullptr;  // RTN_TRACE device buffer
 constexpr int kMaxChunks = 8;                 // end-to-end pipeline depth
+constexpr long long kGraphMaxRows = 4096;     // latency mode: graph-captured steps up to this K
 constexpr long long kChunkMinRows = 1 << 17;  // chunk only batches this large
 
 int PaddedWidth(const std::vector<int>& sizes) {
@@ -637,6 +646,15 @@ rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* calls, unsigne
   });
 }
 
+static void EnsureStaging(rtn_ctx* c) {
+  if (c->h_z) return;
+  const rtn_model* m = c->model;
+  const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in;
+  CUDA_CHECK(cudaMallocHost(&c->h_z, zr * c->max_rows));
+  CUDA_CHECK(cudaMallocHost(&c->h_f, fr * c->max_rows));
+  if (c->max_order >= 1) CUDA_CHECK(cudaMallocHost(&c->h_jac, jr * c->max_rows));
+}
+
 static bool IsPinned(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -670,6 +688,36 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
     if (K == 0) return;
     CUDA_CHECK(cudaSetDevice(m->device));
     const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in;
+    if (c->latency_mode && K <= kGraphMaxRows) {
+      // One MPC step: pinned staging + a CUDA graph of H2D → kernel → D2H,
+      // so the call costs one graph launch and one synchronisation.
+      EnsureStaging(c);
+      std::memcpy(c->h_z, z, zr * K);
+      cudaGraphExec_t exec = nullptr;
+      for (auto& g : c->graphs)
+        if (g.K == K && g.order == order) exec = g.exec;
+      if (!exec) {
+        Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac);  // first launch outside capture (attributes, checks)
+        CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        cudaGraph_t graph;
+        CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        CUDA_CHECK(cudaMemcpyAsync(c->d_z, c->h_z, zr * K, cudaMemcpyHostToDevice, c->stream));
+        Enqueue(c, c->d_z, K, order, c->d_f, order >= 1 ? c->d_jac : nullptr);
+        CUDA_CHECK(cudaMemcpyAsync(c->h_f, c->d_f, fr * K, cudaMemcpyDeviceToHost, c->stream));
+        if (order >= 1) CUDA_CHECK(cudaMemcpyAsync(c->h_jac, c->d_jac, jr * K, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_CHECK(cudaStreamEndCapture(c->stream, &graph));
+        CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+        CUDA_CHECK(cudaGraphDestroy(graph));
+        c->graphs.push_back({K, order, exec});
+      } else {
+        c->launches += 1;  // the graph's kernel node
+      }
+      CUDA_CHECK(cudaGraphLaunch(exec, c->stream));
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      std::memcpy(f, c->h_f, fr * K);
+      if (order >= 1) std::memcpy(jac, c->h_jac, jr * K);
+      return;
+    }
     // Page-locked caller buffers are DMA'd directly; pageable ones go through
     // the context's pinned staging.
     const bool pinned = IsPinned(z) && IsPinned(f) && (order < 1 || IsPinned(jac));
@@ -677,11 +725,7 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
     double* hf = f;
     double* hj = jac;
     if (!pinned) {
-      if (!c->h_z) {
-        CUDA_CHECK(cudaMallocHost(&c->h_z, zr * c->max_rows));
-        CUDA_CHECK(cudaMallocHost(&c->h_f, fr * c->max_rows));
-        if (c->max_order >= 1) CUDA_CHECK(cudaMallocHost(&c->h_jac, jr * c->max_rows));
-      }
+      EnsureStaging(c);
       std::memcpy(c->h_z, z, zr * K);
       hz = c->h_z;
       hf = c->h_f;

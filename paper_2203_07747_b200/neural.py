@@ -108,11 +108,11 @@ class MlpModel:
             eng.close()
         self._engines.clear()
 
-    def engine(self, device: int = 0, precision: int = _lib.RTN_TF32) -> "Engine":
-        key = (device, precision)
+    def engine(self, device: int = 0, precision: int = _lib.RTN_TF32, latency_mode: int = 0) -> "Engine":
+        key = (device, precision, latency_mode)
         eng = self._engines.get(key)
         if eng is None:
-            eng = Engine(self, device, precision)
+            eng = Engine(self, device, precision, latency_mode=latency_mode)
             self._engines[key] = eng
         return eng
 

@@ -106,3 +106,19 @@ def test_large_batch_end_to_end_chunked(monkeypatch):
     again = mlp_batched_eval(m, z[idx], EvalOrder.JACOBIAN)
     assert np.array_equal(again.values, got.values[idx])
     assert np.array_equal(again.jacobians, got.jacobians[idx])
+
+
+def test_latency_mode_graph_path_matches_direct_path():
+    """latency_mode contexts replay a captured H2D→kernel→D2H graph per (K, order);
+    results equal the direct path bitwise, across repeated calls and K changes."""
+    om = oracle.OracleModel.random_net([17] + [512] * 4 + [6], "silu", 31, True)
+    m = oracle.to_product_model(om)
+    direct = m.engine(latency_mode=0)
+    graph = m.engine(latency_mode=1)
+    for k in (20, 20, 7, 20, 50):
+        z = oracle.quad_nodes(100 + k, k)
+        a = direct.prepare(z, 1)
+        b = graph.prepare(z, 1)
+        assert np.array_equal(a.values, b.values) and np.array_equal(a.jacobians, b.jacobians)
+    calls, points, launches = graph.counters()
+    assert calls == 5 and points == 117 and launches >= 5
