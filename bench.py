@@ -210,6 +210,39 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50):
             "device_p99_us": dev[int(len(dev) * 0.99)], "steps": steps}
 
 
+def precision_modes(torch, z, k, sizes, steps=2):
+    """Same workload in the split-precision modes (device-resident, 1 warm-up
+    + `steps` timed launches each). Accuracy per mode is pinned by
+    tests/test_gpu_precision.py."""
+    from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp
+    from paper_2203_07747_b200.errors import raise_for_status
+    L = _lib.lib()
+    out = {}
+    fl = flops_per_node(sizes, 1)
+    for name in ("bf16x3", "3xtf32"):
+        m = make_mlp(sizes, "silu", "full", SEED)
+        eng = m.engine(precision=_lib.PRECISIONS[name])
+        eng._ensure(k, 1)
+        st = torch.cuda.Stream()
+        raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
+        f = torch.empty((k, sizes[-1]), dtype=torch.float64, device="cuda")
+        j = torch.empty((k, sizes[-1], sizes[0]), dtype=torch.float64, device="cuda")
+        run = lambda: raise_for_status(L.rtn_prepare_device(eng.ctx_ptr, z.data_ptr(), k, 1, f.data_ptr(), j.data_ptr(), None))
+        with torch.cuda.stream(st):
+            run()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(steps):
+                run()
+            e1.record(st)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": k * fl / (ms * 1e-3) / 1e12}
+        eng.close()
+        del f, j
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -345,6 +378,9 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": v_all, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                    "value_1thread": v_one, "sample_1thread": sample1,
                    "algorithm": "oracle/ restatement of proj/src/neural.cpp BatchedCore (reverse mode, fp64)"}
+        modes = None
+        if world == 1 and not args.no_modes:
+            modes = precision_modes(torch, z, k, SIZES)
         lat = None
         if not args.no_latency:
             lat = {"cfg3_12x512_N20": latency(torch, SIZES, SEED, 20),
@@ -373,6 +409,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if cpu:
             result["cpu_baseline"] = cpu
+        if modes:
+            result["precision_modes"] = modes
         if lat:
             result["latency"] = lat
     if world > 1:
@@ -391,6 +429,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-modes", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = _env_int("RANK", 0)

@@ -51,10 +51,11 @@ typedef enum {
 } rtn_status;
 
 typedef enum {
-  RTN_TF32 = 0,   /* tcgen05 kind::tf32, fp32 accumulate (tolerance 1e-3)     */
-  RTN_3XTF32 = 1, /* split hi/lo operands, 3 tf32 MMAs per product (1e-5)      */
-  RTN_BF16 = 2    /* reserved */
+  RTN_TF32 = 0,   /* one tcgen05 kind::tf32 pass, fp32 accumulate               */
+  RTN_3XTF32 = 1, /* tf32 hi/lo split operands, 3 kind::tf32 passes (1e-5 class) */
+  RTN_BF16X3 = 2  /* bf16 hi/lo split operands, 3 kind::f16 passes (1e-4 class) */
 } rtn_precision;
+#define RTN_BF16 RTN_BF16X3 /* older name */
 
 typedef enum { RTN_ACT_TANH = 0, RTN_ACT_RELU = 1, RTN_ACT_SILU = 2 } rtn_activation;
 

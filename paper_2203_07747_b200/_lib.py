@@ -12,7 +12,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librtn_mpc.so")
 
 RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL = range(6)
-RTN_TF32, RTN_3XTF32, RTN_BF16 = range(3)
+RTN_TF32, RTN_3XTF32, RTN_BF16X3 = range(3)
+RTN_BF16 = RTN_BF16X3
+PRECISIONS = {"tf32": RTN_TF32, "3xtf32": RTN_3XTF32, "bf16x3": RTN_BF16X3}
 
 # Every symbol include/rtn_mpc.h declares (checked by tests/test_abi.py).
 EXPORTS = (

@@ -22,8 +22,9 @@ NVCC_FLAGS = [
     "-ccbin", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++",
 ]
 
-SOURCES = ["rtn_mpc.cu", "rtn_synth.cpp"]
-DEPS = SOURCES + ["rtn_kernel.cuh", "rtn_fused.cuh", "rtn_pair.cuh"]
+SOURCES = ["rtn_mpc.cu", "rtn_pair_tf32.cu", "rtn_pair_3xtf32.cu", "rtn_pair_bf16x3.cu", "rtn_synth.cpp"]
+HEADERS = ["rtn_kernel.cuh", "rtn_fused.cuh", "rtn_pair.cuh", "rtn_pair_launch.cuh", "rtn_launch.h"]
+DEPS = SOURCES + HEADERS
 
 
 def _nvcc() -> str:
@@ -41,12 +42,29 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
+    """Compiles each translation unit in parallel (the per-precision pair
+    kernels are the slow ones), then links librtn_mpc.so."""
     deps = [os.path.join(CSRC, s) for s in DEPS] + [os.path.join(ROOT, "include", "rtn_mpc.h")]
-    if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
+    if not (force or _stale(LIB, deps)):
+        return LIB
+    objdir = os.path.join(HERE, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        objs.append(obj)
+        cmd = [_nvcc(), *compile_flags, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        procs.append((src, subprocess.Popen(cmd)))
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise RuntimeError(f"nvcc failed for {failed}")
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", NVCC_FLAGS[-1], *objs, "-o", LIB]
+    if verbose:
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     return LIB
 
 

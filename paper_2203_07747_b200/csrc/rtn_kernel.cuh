@@ -46,6 +46,9 @@ constexpr int kLastBlockBytes = 2048;  // output-layer block: 16 outputs x 32 k
 constexpr int kThreads = 384;       // 4 control warps + 8 epilogue warps
 constexpr int kMaxOut = 16;
 
+// Precision modes of the pair kernel (rtn_pair.cuh): tf32, 3xtf32, bf16x3.
+enum : int { kTF32 = 0, k3xTF32 = 1, kBF16x3 = 2 };
+
 struct KParams {
   const double* z;   // K x n_in
   double* f;         // K x n_out
@@ -55,6 +58,7 @@ struct KParams {
   int n_in, n_out, n_hidden, act, order;
   int P;             // nodes per tile (power of two)
   int nt;            // tile rows used (= roundup8(P·(1+n_in))), MMA N
+  int lo_rows;       // pair kernel split modes: row offset of the lo weight tiles in the stacked map
   unsigned long long* trace;  // optional event timestamps (RTN_TRACE), pair 0 only
   int dbg;           // perf-isolation switches (RTN_DEBUG): 1 = MMA ignores act_ready, 2 = 1 KB weight copies
   const uint8_t* w_hidden;  // (n_hidden-1) x NMB x NKC blocks of kStageBytes
@@ -292,9 +296,10 @@ __device__ __forceinline__ void act_fwd(int act, float pre, float& val, float& s
     val = pre > 0.0f ? pre : 0.0f;
     sp = pre > 0.0f ? 1.0f : 0.0f;
   } else {
-    // σ via the SFU: __expf (≈2 ulp) and an IEEE reciprocal; exp(−x) → ∞ for
-    // x ≪ 0 gives σ = 0 exactly, matching the limit.
-    const float s = __frcp_rn(1.0f + __expf(-pre));
+    // σ with the accurate expf (the fast __expf's error grows with |x| and is
+    // amplified through deep nets; this runs only on value rows) and an IEEE
+    // reciprocal; exp(−x) → ∞ for x ≪ 0 gives σ = 0 exactly, matching the limit.
+    const float s = __frcp_rn(1.0f + expf(-pre));
     val = pre * s;
     sp = s * (1.0f + pre * (1.0f - s));
   }
@@ -431,4 +436,66 @@ __device__ __forceinline__ void mma4_tf32_pair_commit(uint32_t d_tmem, uint64_t 
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2)
       : "memory");
 }
+}  // namespace rtn
+
+namespace rtn {
+// Split-operand pair MMA step (3xTF32 / BF16x3): with A = A_hi + A_lo and
+// B = B_hi + B_lo, D += A_hi·B_hi + A_hi·B_lo + A_lo·B_hi (the lo·lo term is
+// below the representation error). 3 passes x 4 K-steps of 32 bytes, one
+// elect, then multicast commits of the two weight stages (and bar2 if set).
+#define RTN_MMA12(KIND)                                                                                              \
+  asm volatile(                                                                                                    \
+      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 x, y;\n\t.reg .b16 m;\n\t"                                        \
+      "mov.b16 m, 3;\n\tsetp.ne.b32 p, %7, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"             \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                           \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %1, %3, %6, p;\n\t"                                      \
+      "add.s64 x, %1, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "add.s64 x, %1, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "add.s64 x, %1, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %1, %4, %6, t;\n\t"                                      \
+      "add.s64 x, %1, 2;\n\tadd.s64 y, %4, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "add.s64 x, %1, 4;\n\tadd.s64 y, %4, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "add.s64 x, %1, 6;\n\tadd.s64 y, %4, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %2, %3, %6, t;\n\t"                                      \
+      "add.s64 x, %2, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "add.s64 x, %2, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "add.s64 x, %2, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n\t"  \
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%9], m;\n\t"  \
+      "and.pred q, q, e;\n\t"                                                                                     \
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%10], m;\n\t}" \
+      ::"r"(d_tmem), "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(0), "r"(idesc), "r"(accumulate), "r"(bar0),     \
+      "r"(bar1), "r"(bar2)                                                                                       \
+      : "memory")
+
+__device__ __forceinline__ void mma12_tf32_pair_commit(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
+                                                       uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
+                                                       uint32_t bar0, uint32_t bar1, uint32_t bar2) {
+  RTN_MMA12("tf32");
+}
+__device__ __forceinline__ void mma12_bf16_pair_commit(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
+                                                       uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
+                                                       uint32_t bar0, uint32_t bar1, uint32_t bar2) {
+  RTN_MMA12("f16");
+}
+#undef RTN_MMA12
+
+// Instruction descriptor: D f32, A/B bf16, both K-major (kind::f16).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+// bf16 round-to-nearest-even of a finite fp32, and back.
+__device__ __forceinline__ uint16_t bf16_rn_bits(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
 }  // namespace rtn

@@ -1,0 +1,29 @@
+// rtn_launch.h — host-side launchers of the pair kernel, one translation unit
+// per precision mode (rtn_pair_{tf32,3xtf32,bf16x3}.cu) so they compile in
+// parallel; rtn_mpc.cu dispatches.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "rtn_kernel.cuh"
+
+namespace rtn {
+
+struct PairGeom {
+  int P;        // nodes per CTA
+  int ntc_max;  // NTC template (row stride per CTA)
+};
+
+// Tile geometry of the pair kernel for a mode / width / batch regime.
+PairGeom PairGeometry(int mode, int wp, bool latency, int n_in);
+
+// Launch status: cudaSuccess or the launch error.
+cudaError_t LaunchPairTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
+                           int grid, cudaStream_t st);
+cudaError_t LaunchPair3xTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
+                             int grid, cudaStream_t st);
+cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
+                             int grid, cudaStream_t st);
+
+}  // namespace rtn

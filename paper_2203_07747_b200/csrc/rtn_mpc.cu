@@ -16,7 +16,7 @@
 
 #include "../../include/rtn_mpc.h"
 #include "rtn_fused.cuh"
-#include "rtn_pair.cuh"
+#include "rtn_launch.h"
 
 namespace {
 
@@ -92,6 +92,21 @@ float RoundTf32(float x) {
   return r;
 }
 
+// Round an fp32 to bf16 (round-to-nearest-even), kept as fp32 / as bits.
+float RoundBf16(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+uint16_t Bf16Bits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return static_cast<uint16_t>(u >> 16);
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------------------
@@ -107,10 +122,12 @@ struct rtn_model {
   float* d_bl = nullptr;
   size_t hidden_bytes = 0;
   // pair (cta_group::2) kernel: plain row-major tf32 weights behind TMA maps
-  float* d_wt_hidden = nullptr;  // (n_hidden-1)·wp rows x wp cols
-  float* d_wt_last = nullptr;    // 16 rows x wp cols
+  void* d_wt_hidden = nullptr;  // split x (n_hidden-1)·wp rows x wp cols (fp32 or bf16)
+  void* d_wt_last = nullptr;    // split x 16 rows x wp cols
   CUtensorMap tmap_h{}, tmap_l{};
   bool has_pair = false;
+  int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3
+  int lo_rows = 0;     // row offset of the lo tiles in the stacked hidden map
   ~rtn_model() {
     int prev;
     if (cudaGetDevice(&prev) == cudaSuccess) {
@@ -203,15 +220,17 @@ EncodeTiledFn GetEncodeTiled() {
   return fn;
 }
 
-// 2-D fp32 row-major [rows x cols] map with a {32, box_rows} box and the
-// 128-byte swizzle the UMMA descriptors expect.
-CUtensorMap MakeTmap(float* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// 2-D row-major [rows x cols] map (fp32 or bf16) with a {128 B, box_rows}
+// box and the 128-byte swizzle the UMMA descriptors expect.
+CUtensorMap MakeTmap(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, bool bf16) {
   CUtensorMap m{};
+  const uint32_t eb = bf16 ? 2 : 4;
   const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {cols * 4};
-  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint64_t strides[1] = {cols * eb};
+  const cuuint32_t box[2] = {128 / eb, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = GetEncodeTiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+  const CUresult r = GetEncodeTiled()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      base, dims, strides, box, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(RTN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
@@ -226,11 +245,13 @@ CUtensorMap MakeTmap(float* base, uint64_t rows, uint64_t cols, uint32_t box_row
 // the exact order the kernel streams them.
 rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   Validate(hm);
-  if (prec != RTN_TF32) throw Error(RTN_EUNSUPPORTED, "precision mode not implemented yet (TF32 only)");
+  if (prec != RTN_TF32 && prec != RTN_3XTF32 && prec != RTN_BF16X3) throw Error(RTN_ECONFIG, "unknown precision mode");
+  const int mode = prec == RTN_TF32 ? rtn::kTF32 : (prec == RTN_3XTF32 ? rtn::k3xTF32 : rtn::kBF16x3);
   const int L = static_cast<int>(hm.sizes.size()) - 1;
   const int n_in = hm.sizes.front(), n_out = hm.sizes.back();
   if (L < 2) throw Error(RTN_EUNSUPPORTED, "device path needs at least one hidden layer");
-  const int wp = PaddedWidth(hm.sizes);
+  // split modes run only on the pair kernel, which needs a padded width of 256/512
+  const int wp = mode == rtn::kTF32 ? PaddedWidth(hm.sizes) : std::max(256, PaddedWidth(hm.sizes));
   if (wp > 512) throw Error(RTN_EUNSUPPORTED, "hidden width > 512 not supported by the fused kernel");
   if (n_out > rtn::kMaxOut) throw Error(RTN_EUNSUPPORTED, "n_out > 16 not supported");
   if (1 + n_in > rtn::kNT) throw Error(RTN_EUNSUPPORTED, "n_in > 79 not supported");
@@ -313,27 +334,50 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   up(reinterpret_cast<void**>(&m->d_bh), bh.data(), bh.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
   if (wp >= 256) {
-    // plain row-major tf32 copies for the pair kernel's TMA maps
-    std::vector<float> th(static_cast<size_t>(std::max(H - 1, 1)) * wp * wp, 0.0f), tl(static_cast<size_t>(16) * wp, 0.0f);
+    // Row-major operand copies for the pair kernel's TMA maps: [hi; lo] stacked
+    // (split modes) in tf32-rounded fp32 or bf16.
+    const int split = mode == rtn::kTF32 ? 1 : 2;
+    const bool bf16 = mode == rtn::kBF16x3;
+    const size_t hid_rows = static_cast<size_t>(std::max(H - 1, 1)) * wp;
+    std::vector<float> th(split * hid_rows * wp, 0.0f), tl(static_cast<size_t>(split) * 16 * wp, 0.0f);
+    auto put = [&](std::vector<float>& dst, size_t row, size_t col, double w) {
+      // hi part, then the residual in the second half of the stack
+      if (bf16) {
+        const float h = RoundBf16(static_cast<float>(w));
+        dst[row * wp + col] = h;
+        if (split == 2) dst[(row + dst.size() / (2 * wp)) * wp + col] = RoundBf16(static_cast<float>(w - h));
+      } else {
+        const float h = RoundTf32(static_cast<float>(w));
+        dst[row * wp + col] = h;
+        if (split == 2) dst[(row + dst.size() / (2 * wp)) * wp + col] = RoundTf32(static_cast<float>(w - h));
+      }
+    };
     for (int l = 1; l < H; ++l) {
       const int rows = hm.sizes[l + 1], cols = hm.sizes[l];
       for (int j = 0; j < rows; ++j)
         for (int k = 0; k < cols; ++k)
-          th[(static_cast<size_t>(l - 1) * wp + j) * wp + k] =
-              RoundTf32(static_cast<float>(hm.W[l][static_cast<size_t>(j) * cols + k]));
+          put(th, static_cast<size_t>(l - 1) * wp + j, k, hm.W[l][static_cast<size_t>(j) * cols + k]);
     }
     {
       const int cols = hm.sizes[L - 1];
       for (int o = 0; o < n_out; ++o)
-        for (int k = 0; k < cols; ++k)
-          tl[static_cast<size_t>(o) * wp + k] =
-              RoundTf32(static_cast<float>(hm.out_scale[o] * hm.W[L - 1][static_cast<size_t>(o) * cols + k]));
+        for (int k = 0; k < cols; ++k) put(tl, o, k, hm.out_scale[o] * hm.W[L - 1][static_cast<size_t>(o) * cols + k]);
     }
-    up(reinterpret_cast<void**>(&m->d_wt_hidden), th.data(), th.size() * 4);
-    up(reinterpret_cast<void**>(&m->d_wt_last), tl.data(), tl.size() * 4);
-    m->tmap_h = MakeTmap(m->d_wt_hidden, static_cast<uint64_t>(std::max(H - 1, 1)) * wp, wp, 128);
-    m->tmap_l = MakeTmap(m->d_wt_last, 16, wp, 8);
+    if (bf16) {
+      std::vector<uint16_t> bh16(th.size()), bl16(tl.size());
+      for (size_t i = 0; i < th.size(); ++i) bh16[i] = Bf16Bits(th[i]);
+      for (size_t i = 0; i < tl.size(); ++i) bl16[i] = Bf16Bits(tl[i]);
+      up(&m->d_wt_hidden, bh16.data(), bh16.size() * 2);
+      up(&m->d_wt_last, bl16.data(), bl16.size() * 2);
+    } else {
+      up(&m->d_wt_hidden, th.data(), th.size() * 4);
+      up(&m->d_wt_last, tl.data(), tl.size() * 4);
+    }
+    m->tmap_h = MakeTmap(m->d_wt_hidden, split * hid_rows, wp, 128, bf16);
+    m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(split) * 16, wp, 8, bf16);
     m->has_pair = true;
+    m->pair_mode = mode;
+    m->lo_rows = static_cast<int>(hid_rows);
   }
   return m.release();
 }
@@ -422,30 +466,6 @@ void LaunchP(const rtn::KParams& prm, int grid, cudaStream_t st) {
   }
 }
 
-template <int WP, int NS, int P, int NTC = 80>
-void LaunchPairT(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStream_t st) {
-  using Cfg = rtn::PairCfg<WP, NS, P, NTC>;
-  auto kern = rtn::rtn_pair_kernel<WP, NS, P, NTC>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
-    attr_set = true;
-  }
-  kern<<<grid, rtn::kThreads, Cfg::kSmemBytes, st>>>(prm, m->tmap_h, m->tmap_l);
-  CUDA_CHECK(cudaGetLastError());
-}
-
-template <int WP, int NS>
-void LaunchPairP(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStream_t st) {
-  switch (prm.P) {
-    case 1: return LaunchPairT<WP, NS, 1>(prm, m, grid, st);
-    case 2: return LaunchPairT<WP, NS, 2>(prm, m, grid, st);
-    case 4: return LaunchPairT<WP, NS, 4>(prm, m, grid, st);
-    case 8: return LaunchPairT<WP, NS, 8>(prm, m, grid, st);
-    default: return LaunchPairT<WP, NS, 16>(prm, m, grid, st);
-  }
-}
-
 // Kernel choice (padded width 256/512; RTN_KERNEL=pair|latency|single forces one):
 //   throughput: pair kernel, P = 4 nodes per CTA (N = 144), when the batch
 //               fills at least half the pairs;
@@ -455,6 +475,13 @@ void LaunchPairP(const rtn::KParams& prm, const rtn_model* m, int grid, cudaStre
 enum class Kern { kSingle, kPair, kLatency };
 Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
   const bool lat_ok = m->has_pair && m->n_in + 1 <= 24;
+  if (m->pair_mode != rtn::kTF32) {  // split precisions exist only on the pair kernel
+    if (const char* e = std::getenv("RTN_KERNEL"))
+      if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
+    if (const char* e = std::getenv("RTN_KERNEL"))
+      if (std::strcmp(e, "pair") == 0) return Kern::kPair;
+    return (lat_ok && K <= num_sms) ? Kern::kLatency : Kern::kPair;
+  }
   if (const char* e = std::getenv("RTN_KERNEL")) {
     if (std::strcmp(e, "pair") == 0 && m->has_pair) return Kern::kPair;
     if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
@@ -496,21 +523,20 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   prm.bh = m->d_bh;
   prm.bl = m->d_bl;
   const Kern kern = Choose(m, K, prm.P, c->num_sms);
-  if (kern == Kern::kLatency) {
-    prm.P = 1;
-    prm.nt = ((1 + m->n_in + 7) / 8) * 8;
-    prm.num_tiles = (K + 1) / 2;  // pair tiles of 2 nodes
-    const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
-    if (m->wp == 256) LaunchPairT<256, 8, 1, 24>(prm, m, grid, c->stream);
-    else LaunchPairT<512, 8, 1, 24>(prm, m, grid, c->stream);
-    c->launches += 1;
-    return;
-  }
-  if (kern == Kern::kPair) {
+  if (kern != Kern::kSingle) {
+    const bool lat = kern == Kern::kLatency;
+    const rtn::PairGeom g = rtn::PairGeometry(m->pair_mode, m->wp, lat, m->n_in);
+    prm.P = g.P;
+    prm.nt = ((g.P * (1 + m->n_in) + 7) / 8) * 8;
+    if (prm.nt > g.ntc_max) throw Error(RTN_EUNSUPPORTED, "node rows exceed the pair tile");
+    prm.lo_rows = m->lo_rows;
     prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
-    if (m->wp == 256) LaunchPairP<256, 8>(prm, m, grid, c->stream);
-    else LaunchPairP<512, 4>(prm, m, grid, c->stream);
+    cudaError_t e;
+    if (m->pair_mode == rtn::kTF32) e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->wp, lat, grid, c->stream);
+    else if (m->pair_mode == rtn::k3xTF32) e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->wp, lat, grid, c->stream);
+    else e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->wp, lat, grid, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }

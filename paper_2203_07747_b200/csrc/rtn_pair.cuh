@@ -1,4 +1,4 @@
-// rtn_pair.cuh — throughput kernel on CTA pairs (cta_group::2).
+// rtn_pair.cuh — throughput / latency kernel on CTA pairs (cta_group::2).
 //
 // Why pairs: a tcgen05 tf32 MMA with both operands in shared memory reads
 // them at ~128 B/clk/SM, so M = 128 × N = 72 runs at 72 % of the math floor
@@ -9,15 +9,23 @@
 // rows) takes A (weights) half from each CTA and B (activations) half from
 // each CTA; each CTA's TMEM receives its 128 neurons for all 144 rows.
 //
-// Data movement per layer (everything else as in rtn_fused.cuh):
-//   weights   : 2-SM TMA tile loads (tensor map, SWIZZLE_128B), each CTA its
-//               128-neuron half, bytes counted on the leader's barrier
+// Precision modes (MODE):
+//   kTF32   : one kind::tf32 pass; operands rounded to tf32 (RNA).
+//   k3xTF32 : A = A_hi + A_lo, B = B_hi + B_lo (both tf32), three kind::tf32
+//             passes hi·hi + hi·lo + lo·hi; fp32-grade (1e-5 class).
+//   kBF16x3 : same split in bf16 (8+8 mantissa bits), three kind::f16 passes
+//             at twice the tf32 rate; operand bytes equal to tf32 mode.
+//
+// Data movement per layer:
+//   weights    : 2-SM TMA tile loads (tensor map, SWIZZLE_128B), each CTA its
+//                128-neuron half (hi and lo tiles in split modes), bytes
+//                counted on the leader's barrier
 //   activations: the epilogue of CTA r owns next-layer K-group q = 2·mb + r
-//               and writes its 144 rows into BOTH CTAs' operand buffers (half
-//               of them through DSMEM, st.shared::cluster)
-//   barriers  : full[s] (leader), act_ready[q] (leader, 256 arrivals from the
-//               owning CTA), empty/in_free/tmem_full/tmem_last multicast by
-//               the leader's tcgen05.commit to both CTAs.
+//                and writes its rows into BOTH CTAs' operand buffers (the
+//                peer's half through DSMEM, st.shared::cluster)
+//   barriers   : full[s] (leader), act_ready[q] (leader, 8 warp arrivals from
+//                the owning CTA), empty/in_free/tmem_full/tmem_last multicast
+//                by the leader's tcgen05.commit to both CTAs.
 #pragma once
 
 #include <cuda.h>
@@ -26,18 +34,25 @@
 
 namespace rtn {
 
-constexpr int kTmemStride2 = 160;   // TMEM columns per 256-neuron block (pair N ≤ 160)
-constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x 32 k
+constexpr int kTmemStride2 = 160;     // TMEM columns per 256-neuron block (pair N ≤ 160)
+constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x 128 B
 
 // NTC = operand row stride per CTA (max rows per CTA): 80 for throughput
-// tiles (P = 4 quadrotor nodes = 72 rows), 24 for latency tiles (P = 1).
-template <int WP, int NSTAGE, int P, int NTC>
+// tiles (P = 4 quadrotor nodes = 72 rows; P = 2 in 3xTF32 at width 512),
+// 24 for latency tiles (P = 1).
+template <int WP, int NSTAGE, int P, int NTC, int MODE>
 struct PairCfg {
-  static constexpr int kNMB = WP / 256;  // 256-neuron blocks (pair M)
-  static constexpr int kNKC = WP / 32;   // 32-wide k chunks
-  static constexpr int kNG = WP / 128;   // 128-neuron K-groups (one per CTA per block)
+  static constexpr int kEB = MODE == kBF16x3 ? 2 : 4;  // operand element bytes
+  static constexpr int kCK = 128 / kEB;                // k per 128-byte chunk row
+  static constexpr int kNKC = WP / kCK;                // chunks per layer input
+  static constexpr int kSplit = MODE == kTF32 ? 1 : 2; // operand buffers (hi[, lo])
+  static constexpr int kCPG = 128 / kCK;               // chunks per 128-neuron K-group
+  static constexpr int kNMB = WP / 256;                // 256-neuron blocks (pair M)
+  static constexpr int kNG = WP / 128;                 // 128-neuron K-groups
+  static constexpr int kStagesPerMB = kNKC * kSplit;
   static constexpr uint32_t kChunkStride = NTC * 128;
-  static constexpr uint32_t kActBytes = kNKC * kChunkStride;
+  static constexpr uint32_t kSplitStride = kNKC * kChunkStride;
+  static constexpr uint32_t kActBytes = kSplit * kSplitStride;
   static constexpr uint32_t kStageOff = kActBytes;
   static constexpr uint32_t kBarOff = kStageOff + NSTAGE * kStageBytes;
   static constexpr uint32_t kNumBars = 2 * NSTAGE + 13;
@@ -47,16 +62,17 @@ struct PairCfg {
   static_assert(kNMB >= 1 && kNMB <= 2, "pair kernel handles 256 or 512 padded width");
   static_assert(kNMB * kTmemStride2 <= 512, "TMEM capacity");
   static_assert(kSmemBytes <= 232448, "shared memory budget");
+  static_assert(kStagesPerMB % NSTAGE == 0, "every 256-block starts at stage 0 (static stage indices)");
   // the output layer's M = 128-row A reads run past the last chunk into the stage ring
   static_assert((128 - NTC) * 128 <= NSTAGE * kStageBytes, "A-operand overrun must stay in smem");
 };
 
-template <int WP, int NSTAGE, int P, int NTC>
+template <int WP, int NSTAGE, int P, int NTC, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_pair_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
-  using C = PairCfg<WP, NSTAGE, P, NTC>;
-  constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG;
+  using C = PairCfg<WP, NSTAGE, P, NTC, MODE>;
+  constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG, SPLIT = C::kSplit, CPG = C::kCPG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* act_s = smem;
@@ -105,12 +121,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     prm.trace[250 + rank] = clock64();
   }
 
-  static_assert(NKC % NSTAGE == 0, "every 256-block starts at stage 0 (static stage indices)");
   if (warp == 0) {
     // ===================== weight producer: 2-SM TMA, own 128-neuron half ====
     // Chunk loops are fully unrolled: stage indices, phases and coordinates
     // are compile-time, so this single warp is not instruction-latency bound
-    // at small N (scripts/mma_bench.cu variants).
+    // at small N (scripts/mma_bench.cu variants). Split modes stream the hi
+    // tile then the lo tile of each chunk (lo rows start at prm.lo_rows).
     const uint64_t pol = l2_evict_last_policy();
     uint32_t ph = 0;
     const int yr = static_cast<int>(rank) * 128;
@@ -119,32 +135,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int mb = 0; mb < NMB; ++mb) {
           const int y = l * WP + mb * 256 + yr;
 #pragma unroll
-          for (int c = 0; c < NKC; ++c) {
-            const int st = c % NSTAGE;
+          for (int i = 0; i < NKC * SPLIT; ++i) {
+            const int c = i / SPLIT, sp = i % SPLIT, st = i % NSTAGE;
             mbar_wait(&empty[st], ph ^ 1);
             if (leader) mbar_expect_tx_elect(&full[st], 2 * kStageBytes);
-            tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * 32, y, &full[st], pol);
+            tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * C::kCK, y + sp * prm.lo_rows, &full[st], pol);
             if (st == NSTAGE - 1) ph ^= 1;
           }
         }
 #pragma unroll
-      for (int c = 0; c < NKC; ++c) {
-        const int st = c % NSTAGE;
+      for (int i = 0; i < NKC * SPLIT; ++i) {
+        const int c = i / SPLIT, sp = i % SPLIT, st = i % NSTAGE;
         mbar_wait(&empty[st], ph ^ 1);
         if (leader) mbar_expect_tx_elect(&full[st], 2 * kLastHalfBytes);
-        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * 32, static_cast<int>(rank) * 8, &full[st], pol);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * C::kCK, sp * 16 + static_cast<int>(rank) * 8, &full[st],
+                     pol);
         if (st == NSTAGE - 1) ph ^= 1;
       }
     }
   } else if (warp == 1) {
     // ===================== pair MMA issuer (leader CTA) ======================
     if (leader) {
-      const uint32_t idesc_h = idesc_tf32(256, 2 * ntc);
-      const uint32_t idesc_o = idesc_tf32(256, kMaxOut);
+      const uint32_t idesc_h = MODE == kBF16x3 ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_o = MODE == kBF16x3 ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
       // descriptors advance by (bytes >> 4) in the start-address field
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
-      constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4;
+      constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4, kSplitD = C::kSplitStride >> 4;
       uint32_t ph = 0, ar = 0;
       // Before the first MMA of a layer overwrites TMEM block 0, both CTAs must
       // have drained it: wait for K-groups 0 and 1 (one per CTA) up front.
@@ -158,6 +175,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         tc_fence_after();
       };
+      // One chunk: weights from stage(s) st0[/st1], activations chunk (hi[, lo]).
+      auto chunk_mma = [&](uint32_t d, uint64_t wa, uint64_t wb, int st0, int st1, uint64_t xa, uint64_t xb,
+                           uint32_t idesc, uint32_t acc, uint32_t bar2, bool weights_are_a) {
+        if constexpr (MODE == kTF32) {
+          if (weights_are_a)
+            mma4_tf32_pair_commit(d, wa, xa, idesc, acc, smem_u32(&empty[st0]), bar2);
+          else
+            mma4_tf32_pair_commit(d, xa, wa, idesc, acc, smem_u32(&empty[st0]), bar2);
+        } else {
+          const uint64_t ah = weights_are_a ? wa : xa, al = weights_are_a ? wb : xb;
+          const uint64_t bh = weights_are_a ? xa : wa, bl = weights_are_a ? xb : wb;
+          if constexpr (MODE == k3xTF32)
+            mma12_tf32_pair_commit(d, ah, al, bh, bl, idesc, acc, smem_u32(&empty[st0]), smem_u32(&empty[st1]), bar2);
+          else
+            mma12_bf16_pair_commit(d, ah, al, bh, bl, idesc, acc, smem_u32(&empty[st0]), smem_u32(&empty[st1]), bar2);
+        }
+      };
       for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
         for (int l = 0; l < n_mma_layers; ++l) {
 #pragma unroll 1
@@ -166,14 +200,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2] = globaltimer();
 #pragma unroll
             for (int c = 0; c < NKC; ++c) {
-              const int st = c % NSTAGE;
-              if ((c & 3) == 0 && mb == 0) wait_group(c >> 2);
-              mbar_wait(&full[st], ph);
+              const int st0 = (c * SPLIT) % NSTAGE, st1 = (c * SPLIT + SPLIT - 1) % NSTAGE;
+              if ((c % CPG) == 0 && mb == 0) wait_group(c / CPG);
+              mbar_wait(&full[st0], ph);
+              if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
               tc_fence_after();
-              // second commit: in_free after the last block consumed K-group c/4
-              const uint32_t bar2 = (mb == NMB - 1 && (c & 3) == 3) ? smem_u32(&in_free[c >> 2]) : 0u;
-              mma4_tf32_pair_commit(d, a0 + st * kStageD, b0 + c * kChunkD, idesc_h, c != 0, smem_u32(&empty[st]), bar2);
-              if (st == NSTAGE - 1) ph ^= 1;
+              // extra commit: in_free after the last block consumed K-group c/CPG
+              const uint32_t bar2 = (mb == NMB - 1 && (c % CPG) == CPG - 1) ? smem_u32(&in_free[c / CPG]) : 0u;
+              chunk_mma(d, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD,
+                        b0 + kSplitD + c * kChunkD, idesc_h, c != 0, bar2, true);
+              if (st1 == NSTAGE - 1) ph ^= 1;
             }
             mma_commit_pair(&tmem_full[mb]);
             if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2 + 1] = globaltimer();
@@ -183,12 +219,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]; M = 2 x 128 rows, N = 16
 #pragma unroll
         for (int c = 0; c < NKC; ++c) {
-          const int st = c % NSTAGE;
-          if ((c & 3) == 0) wait_group(c >> 2);
-          mbar_wait(&full[st], ph);
+          const int st0 = (c * SPLIT) % NSTAGE, st1 = (c * SPLIT + SPLIT - 1) % NSTAGE;
+          if ((c % CPG) == 0) wait_group(c / CPG);
+          mbar_wait(&full[st0], ph);
+          if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
           tc_fence_after();
-          mma4_tf32_pair_commit(tmem_base, b0 + c * kChunkD, a0 + st * kStageD, idesc_o, c != 0, smem_u32(&empty[st]), 0);
-          if (st == NSTAGE - 1) ph ^= 1;
+          chunk_mma(tmem_base, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD,
+                    b0 + kSplitD + c * kChunkD, idesc_o, c != 0, 0u, false);
+          if (st1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_pair(tmem_last);
         ++ar;
@@ -210,45 +248,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int rows_used = P * (1 + n_in);   // rows per side
     const bool no_pad = rows_used == ntc;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    // Row r of a K-major SW128 operand lives at  col + (r/8)·1024 + (r%8)·128
+    // + ((u ^ r%8) − u)·16  relative to row 0 of this thread's neuron column,
+    // with u the neuron's 16-byte unit inside its 128-byte chunk row.
+    const int u = ((tid_h * C::kEB) >> 4) & 7;
     int swz[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) swz[i] = ((((tid_h >> 2) & 7) ^ i) - ((tid_h >> 2) & 7)) * 16 + i * 128;
+    for (int i = 0; i < 8; ++i) swz[i] = ((u ^ i) - u) * 16 + i * 128;
     const uint32_t act_local = smem_u32(act_s);
     const bool local_side = half == static_cast<int>(rank) || (prm.dbg & 8);  // dbg 8: timing only
     const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
-    (void)0;
     uint32_t ready_cl[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);
     uint32_t hl = 0, tiles_done = 0;
 
-    // Activation epilogue on one side's rows: value rows → tf32(σ(pre+b)),
-    // tangent rows → tf32(σ'(pre)·t), padding → 0.
+    // Activation epilogue on one side's rows (fp32): value rows → σ(pre+b),
+    // tangent rows → σ'(pre)·t, padding → 0.
     auto scale_side = [&](float* v, float bj) {
       float val[P], sp[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) act_fwd(act, v[p] + bj, val[p], sp[p]);
 #pragma unroll
-      for (int p = 0; p < P; ++p) v[p] = to_tf32(val[p]);
+      for (int p = 0; p < P; ++p) v[p] = val[p];
       if (no_pad) {
 #pragma unroll
-        for (int i = P; i < NTC; ++i) v[i] = to_tf32(v[i] * sp[i % P]);
+        for (int i = P; i < NTC; ++i) v[i] = v[i] * sp[i % P];
       } else {
 #pragma unroll
-        for (int i = P; i < NTC; ++i) v[i] = i < rows_used ? to_tf32(v[i] * sp[i % P]) : 0.0f;
+        for (int i = P; i < NTC; ++i) v[i] = i < rows_used ? v[i] * sp[i % P] : 0.0f;
       }
     };
-    // Store one neuron column (rows 0..ntc-1) of one side into its operand buffer.
+    // Store one neuron column (rows 0..ntc-1) of one side into its operand
+    // buffer(s), rounding / splitting per precision mode.
     auto store_side = [&](const float* v, int j) {
-      const uint32_t base = side_base + sw128_offset(0, j, C::kChunkStride);
-      if (local_side) {
+      const uint32_t base =
+          side_base + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) + ((j * C::kEB) & 15);
 #pragma unroll
-        for (int i = 0; i < NTC; ++i)
-          if ((i & ~7) < ntc) st_shared_f32(base + (i >> 3) * 1024 + swz[i & 7], v[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < NTC; ++i)
-          if ((i & ~7) < ntc) st_cluster_f32(base + (i >> 3) * 1024 + swz[i & 7], v[i]);
+      for (int i = 0; i < NTC; ++i) {
+        if ((i & ~7) >= ntc) continue;
+        const uint32_t a = base + (i >> 3) * 1024 + swz[i & 7];
+        if constexpr (MODE == kTF32) {
+          const float h = to_tf32(v[i]);
+          if (local_side) st_shared_f32(a, h);
+          else st_cluster_f32(a, h);
+        } else if constexpr (MODE == k3xTF32) {
+          const float h = to_tf32(v[i]);
+          const float lo = to_tf32(v[i] - h);
+          if (local_side) {
+            st_shared_f32(a, h);
+            st_shared_f32(a + C::kSplitStride, lo);
+          } else {
+            st_cluster_f32(a, h);
+            st_cluster_f32(a + C::kSplitStride, lo);
+          }
+        } else {
+          const uint16_t h = bf16_rn_bits(v[i]);
+          const uint16_t lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
+          if (local_side) {
+            st_shared_u16(a, h);
+            st_shared_u16(a + C::kSplitStride, lo);
+          } else {
+            st_cluster_u16(a, h);
+            st_cluster_u16(a + C::kSplitStride, lo);
+          }
+        }
       }
     };
     auto publish = [&](int grp) {
@@ -316,8 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float v[NTC];
 #pragma unroll
         for (int i = 0; i < NTC; ++i) {
-          if (i < P) v[i] = to_tf32(val[i]);
-          else v[i] = i < rows_used ? to_tf32(sp[i % P] * __ldg(w0r + (i - P) / P)) : 0.0f;
+          if (i < P) v[i] = val[i];
+          else v[i] = i < rows_used ? sp[i % P] * __ldg(w0r + (i - P) / P) : 0.0f;
         }
         store_side(v, j);
         publish(g);

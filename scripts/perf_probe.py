@@ -11,9 +11,9 @@ from paper_2203_07747_b200 import _lib, make_mlp, synth_quad_nodes, flops_per_no
 from paper_2203_07747_b200.errors import raise_for_status  # noqa: E402
 
 
-def probe(sizes, act, k, reps=5):
+def probe(sizes, act, k, reps=5, prec=0):
     m = make_mlp(sizes, act, "full", 1000 * (len(sizes) - 2) + sizes[1])
-    eng = m.engine()
+    eng = m.engine(precision=prec)
     eng._ensure(k, 1)
     L = _lib.lib()
     z = torch.from_numpy(synth_quad_nodes(2203, k)).cuda()
@@ -35,7 +35,7 @@ def probe(sizes, act, k, reps=5):
         ts.append(e0.elapsed_time(e1))
     t = float(np.median(ts))
     fl = flops_per_node(sizes) * k
-    print(f"{sizes[1]}x{len(sizes)-2} {act} K={k}: {t:.3f} ms  {k/t*1e3/1e6:.2f} M nodes/s  {fl/t/1e9:.1f} TFLOP/s", flush=True)
+    print(f"prec {prec} {sizes[1]}x{len(sizes)-2} {act} K={k}: {t:.3f} ms  {k/t*1e3/1e6:.2f} M nodes/s  {fl/t/1e9:.1f} TFLOP/s", flush=True)
 
 
 if __name__ == "__main__":
@@ -51,8 +51,11 @@ if __name__ == "__main__":
         e0.record(); a @ b; e1.record(); torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
     print(f"cuBLAS tf32 8192^3: {2*8192**3/best/1e9:.1f} TFLOP/s", flush=True)
-    probe([17] + [256] * 5 + [6], "silu", 81920)
-    probe([17] + [512] * 12 + [6], "silu", 20)
-    probe([17] + [256] * 5 + [6], "silu", 20)
-    probe([17] + [512] * 12 + [6], "silu", 3276800 // 8)
-    probe([17] + [512] * 12 + [6], "silu", 3276800, reps=3)
+    precs = [int(x) for x in sys.argv[1:]] or [0]
+    for pr in precs:
+        probe([17] + [256] * 5 + [6], "silu", 81920, prec=pr)
+        probe([17] + [512] * 12 + [6], "silu", 20, prec=pr)
+        probe([17] + [256] * 5 + [6], "silu", 20, prec=pr)
+        probe([17] + [512] * 12 + [6], "silu", 3276800 // 8, prec=pr)
+    if precs == [0]:
+        probe([17] + [512] * 12 + [6], "silu", 3276800, reps=3)

@@ -1,9 +1,10 @@
-"""TF32 error of the device path vs the fp64 oracle on well-conditioned nets."""
+"""Device error vs the fp64 oracle per precision mode and kernel, on
+well-conditioned nets (hidden weights x gain so f and J are O(1))."""
 import os, sys
 sys.path.insert(0, ".")
 import numpy as np
 import oracle
-from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
+from paper_2203_07747_b200 import _lib
 
 def net(sizes, act, gain, seed=11):
     om = oracle.OracleModel.random_net(sizes, act, seed, True)
@@ -12,12 +13,18 @@ def net(sizes, act, gain, seed=11):
             om.set_layer(l, w * gain, b)
     return om
 
-for kern in ("single", "pair"):
-    os.environ["RTN_KERNEL"] = kern
-    for sizes, act, gains in (([17]+[512]*12+[6], "silu", (1.0, 2.0, 2.5, 3.0)), ([17]+[256]*5+[6], "silu", (1.0, 2.0, 2.5, 3.0)), ([17, 64, 64, 6], "tanh", (1.0, 2.0, 3.0))):
-        for g in gains:
+cases = [([17]+[512]*12+[6], "silu", 2.5), ([17]+[256]*5+[6], "silu", 2.5), ([17, 64, 64, 6], "tanh", 3.0),
+         ([17]+[512]*12+[6], "silu", 1.0)]
+for prec in ("tf32", "3xtf32", "bf16x3"):
+    for kern in ("pair", "latency"):
+        os.environ["RTN_KERNEL"] = kern
+        for sizes, act, g in cases:
             om = net(sizes, act, g)
-            z = oracle.quad_nodes(2203, 64)
+            z = oracle.quad_nodes(2203, 64 if kern == "pair" else 20)
             f, j, _ = om.batched_eval(z, 1)
-            got = mlp_batched_eval(oracle.to_product_model(om), z, EvalOrder.JACOBIAN)
-            print(f"{kern:6s} {sizes[1]}x{len(sizes)-2} {act} gain {g}: |J|max {abs(j).max():8.3g}  err f {oracle.max_node_rel_error(got.values, f):.2e}  A {oracle.max_node_rel_error(got.jacobians[:,:,:13], j[:,:,:13]):.2e}  B {oracle.max_node_rel_error(got.jacobians[:,:,13:], j[:,:,13:]):.2e}", flush=True)
+            m = oracle.to_product_model(om)
+            got = m.engine(precision=_lib.PRECISIONS[prec]).prepare(z, 1)
+            ef = oracle.max_node_rel_error(got.values, f)
+            ea = oracle.max_node_rel_error(got.jacobians[:, :, :13], j[:, :, :13])
+            eb = oracle.max_node_rel_error(got.jacobians[:, :, 13:], j[:, :, 13:])
+            print(f"{prec:6s} {kern:7s} {sizes[1]}x{len(sizes)-2} {act} gain {g}: f {ef:.2e} A {ea:.2e} B {eb:.2e}", flush=True)
