@@ -165,21 +165,23 @@ def measured_tf32_peak(torch):
     return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
 
 
-def latency(torch, sizes, seed, k, steps=1000, warm=50):
+def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0):
     """Per-MPC-step approximation latency: K = N nodes of one instance
     through rtn_prepare (host z -> host f, J), and device-only (events)."""
     import numpy as np
     from paper_2203_07747_b200 import _lib, make_mlp, synth_quad_nodes
     from paper_2203_07747_b200.errors import raise_for_status
     m = make_mlp(sizes, "silu", "full", seed)
-    eng = m.engine(latency_mode=1)  # graph-captured H2D -> kernel -> D2H per step
-    eng._ensure(k, 1)
+    eng = m.engine(latency_mode=1, precision=precision)  # graph-captured H2D -> kernel -> D2H per step
+    eng._ensure(k, order)
     L = _lib.lib()
     z = torch.from_numpy(synth_quad_nodes(7, k)).pin_memory()
     f = torch.empty((k, sizes[-1]), dtype=torch.float64).pin_memory()
     j = torch.empty((k, sizes[-1], sizes[0]), dtype=torch.float64).pin_memory()
+    h = torch.empty((k, sizes[-1], sizes[0], sizes[0]), dtype=torch.float64).pin_memory() if order == 2 else None
     dp = C.POINTER(C.c_double)
-    args = (eng.ctx_ptr, C.cast(z.data_ptr(), dp), k, sizes[0], 1, C.cast(f.data_ptr(), dp), C.cast(j.data_ptr(), dp), None)
+    args = (eng.ctx_ptr, C.cast(z.data_ptr(), dp), k, sizes[0], order, C.cast(f.data_ptr(), dp), C.cast(j.data_ptr(), dp),
+            C.cast(h.data_ptr(), dp) if h is not None else None)
     for _ in range(warm):
         raise_for_status(L.rtn_prepare(*args))
     ts = []
@@ -193,12 +195,14 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50):
     dz = z.cuda()
     df = torch.empty((k, sizes[-1]), dtype=torch.float64, device="cuda")
     dj = torch.empty((k, sizes[-1], sizes[0]), dtype=torch.float64, device="cuda")
+    dh = torch.empty((k, sizes[-1], sizes[0], sizes[0]), dtype=torch.float64, device="cuda") if order == 2 else None
     dev = []
     with torch.cuda.stream(st):
         for i in range(warm + 200):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            L.rtn_prepare_device(eng.ctx_ptr, dz.data_ptr(), k, 1, df.data_ptr(), dj.data_ptr(), None)
+            L.rtn_prepare_device(eng.ctx_ptr, dz.data_ptr(), k, order, df.data_ptr(), dj.data_ptr(),
+                                 dh.data_ptr() if dh is not None else None)
             e1.record(st)
             e1.synchronize()
             if i >= warm:
@@ -384,7 +388,10 @@ def run_ours(args, rank, world, local_rank):
         lat = None
         if not args.no_latency:
             lat = {"cfg3_12x512_N20": latency(torch, SIZES, SEED, 20),
-                   "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20)}
+                   "cfg3_12x512_N20_order2": latency(torch, SIZES, SEED, 20, steps=300, order=2),
+                   "cfg3_12x512_N20_bf16x3": latency(torch, SIZES, SEED, 20, steps=300, precision=2),
+                   "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20),
+                   "cfg1_2x64_N10": latency(torch, [17, 64, 64, 6], 2064, 10, steps=300)}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",

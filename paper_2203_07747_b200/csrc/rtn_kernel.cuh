@@ -53,6 +53,7 @@ struct KParams {
   const double* z;   // K x n_in
   double* f;         // K x n_out
   double* jac;       // K x n_out x n_in (may be null for order 0)
+  double* hess;      // K x n_out x n_in x n_in (order 2 only)
   long long K;
   long long num_tiles;
   int n_in, n_out, n_hidden, act, order;
@@ -498,4 +499,76 @@ __device__ __forceinline__ uint16_t bf16_rn_bits(float x) {
   return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
 }
 __device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+}  // namespace rtn
+
+namespace rtn {
+// ---- second order (Hessian rows) -------------------------------------------
+// Packed upper-triangle index p of the pair (a, b), a ≤ b, over n inputs:
+// p = 0 → (0,0), 1 → (0,1), …, n-1 → (0,n-1), n → (1,1), …
+struct PairAB {
+  int a, b;
+};
+__host__ __device__ constexpr PairAB pair_ab(int p, int n) {
+  int a = 0;
+  while (p >= n - a) {
+    p -= n - a;
+    ++a;
+  }
+  return PairAB{a, a + p};
+}
+constexpr int kNin2 = 17;                         // order-2 device path: quadrotor inputs
+constexpr int kPairs2 = kNin2 * (kNin2 + 1) / 2;  // 153 packed Hessian rows per node
+constexpr int kCarrier2 = 1 + kNin2;              // value + tangent rows carried by every tile
+constexpr int kNtc2 = 48;                         // rows per CTA side in order-2 tiles
+constexpr int kSlots2 = 2 * kNtc2 - kCarrier2;    // 78 Hessian rows per tile → 2 tiles per node
+
+// Activation value, slope and curvature (second-order tangents need σ'').
+__device__ __forceinline__ void act_fwd2(int act, float pre, float& val, float& sp, float& spp) {
+  if (act == 0) {
+    const float t = tanhf(pre);
+    val = t;
+    sp = 1.0f - t * t;
+    spp = -2.0f * t * sp;
+  } else {
+    const float s = __frcp_rn(1.0f + expf(-pre));
+    val = pre * s;
+    sp = s * (1.0f + pre * (1.0f - s));
+    spp = s * (1.0f - s) * (2.0f + pre * (1.0f - 2.0f * s));
+  }
+}
+}  // namespace rtn
+
+#include <utility>
+
+namespace rtn {
+// Second-order epilogue rows with compile-time (a, b): h' = σ'·h + σ''·T_a·T_b
+// (hidden layers, T = pre-activation tangents) or h = σ''·T_a·T_b (layer 0,
+// where the incoming second-order tangents are zero). P2 ≥ 153 is padding.
+template <int P2>
+__device__ __forceinline__ float hrow(float h, const float* T, float sp, float spp) {
+  if constexpr (P2 < kPairs2) {
+    constexpr PairAB ab = pair_ab(P2, kNin2);
+    return fmaf(spp, T[ab.a] * T[ab.b], sp * h);
+  } else {
+    return 0.0f;
+  }
+}
+template <int P2>
+__device__ __forceinline__ float hrow0(const float* T, float spp) {
+  if constexpr (P2 < kPairs2) {
+    constexpr PairAB ab = pair_ab(P2, kNin2);
+    return spp * (T[ab.a] * T[ab.b]);
+  } else {
+    return 0.0f;
+  }
+}
+// v[OFF + s] for s in S...: pair index BASE + s.
+template <int BASE, int OFF, int... S>
+__device__ __forceinline__ void hrows(float* v, const float* T, float sp, float spp, std::integer_sequence<int, S...>) {
+  ((v[OFF + S] = hrow<BASE + S>(v[OFF + S], T, sp, spp)), ...);
+}
+template <int BASE, int OFF, int... S>
+__device__ __forceinline__ void hrows0(float* v, const float* T, float spp, std::integer_sequence<int, S...>) {
+  ((v[OFF + S] = hrow0<BASE + S>(T, spp)), ...);
+}
 }  // namespace rtn

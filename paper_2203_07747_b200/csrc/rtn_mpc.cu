@@ -114,6 +114,8 @@ struct rtn_model {
   int device = 0;
   rtn_precision prec = RTN_TF32;
   int n_in = 0, n_out = 0, n_layers = 0, n_hidden = 0, act = 0, wp = 0;
+  int pair_wp = 0;            // padded width of the pair-kernel packs (256 or 512)
+  float* d_bh_pair = nullptr; // hidden biases with pair_wp stride
   void* d_w_hidden = nullptr;  // packed SW128 blocks
   void* d_w_last = nullptr;
   float* d_w0 = nullptr;
@@ -140,6 +142,7 @@ struct rtn_model {
       cudaFree(d_bl);
       cudaFree(d_wt_hidden);
       cudaFree(d_wt_last);
+      cudaFree(d_bh_pair);
       cudaSetDevice(prev);
     }
   }
@@ -155,6 +158,8 @@ struct rtn_ctx {
   double* d_z = nullptr;
   double* d_f = nullptr;
   double* d_jac = nullptr;
+  double* d_hess = nullptr;
+  double* h_hess = nullptr;
   double* h_z = nullptr;  // pinned staging
   double* h_f = nullptr;
   double* h_jac = nullptr;
@@ -177,6 +182,8 @@ struct rtn_ctx {
       cudaFree(d_z);
       cudaFree(d_f);
       cudaFree(d_jac);
+      cudaFree(d_hess);
+      cudaFreeHost(h_hess);
       cudaFreeHost(h_z);
       cudaFreeHost(h_f);
       cudaFreeHost(h_jac);
@@ -250,16 +257,18 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   const int L = static_cast<int>(hm.sizes.size()) - 1;
   const int n_in = hm.sizes.front(), n_out = hm.sizes.back();
   if (L < 2) throw Error(RTN_EUNSUPPORTED, "device path needs at least one hidden layer");
-  // split modes run only on the pair kernel, which needs a padded width of 256/512
-  const int wp = mode == rtn::kTF32 ? PaddedWidth(hm.sizes) : std::max(256, PaddedWidth(hm.sizes));
+  // single-CTA kernel: padded width 128/256/512 (TF32 only); pair kernel
+  // (every precision, order 2): 256/512
+  const int wp = PaddedWidth(hm.sizes);
   if (wp > 512) throw Error(RTN_EUNSUPPORTED, "hidden width > 512 not supported by the fused kernel");
+  const int pwp = std::max(256, wp);
   if (n_out > rtn::kMaxOut) throw Error(RTN_EUNSUPPORTED, "n_out > 16 not supported");
   if (1 + n_in > rtn::kNT) throw Error(RTN_EUNSUPPORTED, "n_in > 79 not supported");
   const int H = L - 1;  // hidden layers (each followed by the activation)
   const int nkc = wp / 32, nmb = wp / 128;
 
   // layer 0 (CUDA cores, fp32)
-  std::vector<float> w0(static_cast<size_t>(wp) * n_in, 0.0f), b0(wp, 0.0f);
+  std::vector<float> w0(static_cast<size_t>(pwp) * n_in, 0.0f), b0(pwp, 0.0f);
   for (int j = 0; j < hm.sizes[1]; ++j) {
     double acc = hm.b[0][j];
     for (int k = 0; k < n_in; ++k) {
@@ -333,7 +342,15 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   up(reinterpret_cast<void**>(&m->d_b0), b0.data(), b0.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bh), bh.data(), bh.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
-  if (wp >= 256) {
+  {
+    std::vector<float> bh2(static_cast<size_t>(std::max(H - 1, 1)) * pwp, 0.0f);
+    for (int l = 1; l < H; ++l)
+      for (int j = 0; j < hm.sizes[l + 1]; ++j) bh2[static_cast<size_t>(l - 1) * pwp + j] = static_cast<float>(hm.b[l][j]);
+    up(reinterpret_cast<void**>(&m->d_bh_pair), bh2.data(), bh2.size() * 4);
+  }
+  m->pair_wp = pwp;
+  {
+    const int wp = pwp;  // pair packs use the pair width
     // Row-major operand copies for the pair kernel's TMA maps: [hi; lo] stacked
     // (split modes) in tf32-rounded fp32 or bf16.
     const int split = mode == rtn::kTF32 ? 1 : 2;
@@ -379,6 +396,7 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
     m->pair_mode = mode;
     m->lo_rows = static_cast<int>(hid_rows);
   }
+  if (mode != rtn::kTF32) m->wp = pwp;  // split precisions exist only on the pair kernel
   return m.release();
 }
 
@@ -493,7 +511,8 @@ Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
   return Kern::kPair;
 }
 
-void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac) {
+void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac,
+             double* d_hess = nullptr) {
   const rtn_model* m = c->model;
   if (K == 0) return;
   rtn::KParams prm{};
@@ -522,10 +541,25 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   prm.b0 = m->d_b0;
   prm.bh = m->d_bh;
   prm.bl = m->d_bl;
+  prm.hess = nullptr;
+  if (order == 2) {
+    prm.P = 1;
+    prm.nt = rtn::kNtc2;
+    prm.lo_rows = m->lo_rows;
+    prm.bh = m->d_bh_pair;
+    prm.hess = d_hess;
+    prm.num_tiles = 2 * K;  // two Hessian groups per node
+    const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+    const cudaError_t e = rtn::LaunchPairOrder2(m->pair_mode, prm, m->tmap_h, m->tmap_l, m->pair_wp, grid, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("order-2 kernel launch: ") + cudaGetErrorString(e));
+    c->launches += 1;
+    return;
+  }
   const Kern kern = Choose(m, K, prm.P, c->num_sms);
   if (kern != Kern::kSingle) {
+    prm.bh = m->d_bh_pair;
     const bool lat = kern == Kern::kLatency;
-    const rtn::PairGeom g = rtn::PairGeometry(m->pair_mode, m->wp, lat, m->n_in);
+    const rtn::PairGeom g = rtn::PairGeometry(m->pair_mode, m->pair_wp, lat, m->n_in);
     prm.P = g.P;
     prm.nt = ((g.P * (1 + m->n_in) + 7) / 8) * 8;
     if (prm.nt > g.ntc_max) throw Error(RTN_EUNSUPPORTED, "node rows exceed the pair tile");
@@ -533,9 +567,9 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
     cudaError_t e;
-    if (m->pair_mode == rtn::kTF32) e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->wp, lat, grid, c->stream);
-    else if (m->pair_mode == rtn::k3xTF32) e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->wp, lat, grid, c->stream);
-    else e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->wp, lat, grid, c->stream);
+    if (m->pair_mode == rtn::kTF32) e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+    else if (m->pair_mode == rtn::k3xTF32) e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+    else e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
@@ -617,7 +651,8 @@ rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order,
     if (max_order == 2) {
       if (m->act == RTN_ACT_RELU)
         throw Error(RTN_EUNSUPPORTED, "mlp hessian: relu networks are not twice differentiable");
-      throw Error(RTN_EUNSUPPORTED, "second-order device path not implemented yet");
+      if (m->n_in != rtn::kNin2 || m->n_out > rtn::kMaxOut)
+        throw Error(RTN_EUNSUPPORTED, "second-order device path is built for 17 inputs (quadrotor z = [x; u])");
     }
     CUDA_CHECK(cudaSetDevice(m->device));
     std::unique_ptr<rtn_ctx> c(new rtn_ctx());
@@ -641,6 +676,7 @@ rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order,
     CUDA_CHECK(cudaMalloc(&c->d_z, zb));
     CUDA_CHECK(cudaMalloc(&c->d_f, fb));
     if (max_order >= 1) CUDA_CHECK(cudaMalloc(&c->d_jac, jb));
+    if (max_order >= 2) CUDA_CHECK(cudaMalloc(&c->d_hess, jb * m->n_in));
     // pinned staging for pageable caller buffers is allocated on first use
     *out = c.release();
   });
@@ -679,6 +715,7 @@ static void EnsureStaging(rtn_ctx* c) {
   CUDA_CHECK(cudaMallocHost(&c->h_z, zr * c->max_rows));
   CUDA_CHECK(cudaMallocHost(&c->h_f, fr * c->max_rows));
   if (c->max_order >= 1) CUDA_CHECK(cudaMallocHost(&c->h_jac, jr * c->max_rows));
+  if (c->max_order >= 2) CUDA_CHECK(cudaMallocHost(&c->h_hess, jr * m->n_in * c->max_rows));
 }
 
 static bool IsPinned(const void* p) {
@@ -708,12 +745,12 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
       throw Error(RTN_EDOMAIN, "mlp eval: feature dim " + std::to_string(n_cols) + " does not match model input " +
                                    std::to_string(m->n_in));
     if (hess != nullptr && order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless order == 2");
-    if (K > 0 && (!z || !f || (order >= 1 && !jac))) throw Error(RTN_ECONFIG, "null buffer");
+    if (K > 0 && (!z || !f || (order >= 1 && !jac) || (order == 2 && !hess))) throw Error(RTN_ECONFIG, "null buffer");
     c->calls += 1;
     c->points += static_cast<unsigned long long>(K);
     if (K == 0) return;
     CUDA_CHECK(cudaSetDevice(m->device));
-    const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in;
+    const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in, hr = jr * m->n_in;
     if (c->latency_mode && K <= kGraphMaxRows) {
       // One MPC step: pinned staging + a CUDA graph of H2D → kernel → D2H,
       // so the call costs one graph launch and one synchronisation.
@@ -723,14 +760,15 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
       for (auto& g : c->graphs)
         if (g.K == K && g.order == order) exec = g.exec;
       if (!exec) {
-        Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac);  // first launch outside capture (attributes, checks)
+        Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac, c->d_hess);  // first launch outside capture (attributes, checks)
         CUDA_CHECK(cudaStreamSynchronize(c->stream));
         cudaGraph_t graph;
         CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         CUDA_CHECK(cudaMemcpyAsync(c->d_z, c->h_z, zr * K, cudaMemcpyHostToDevice, c->stream));
-        Enqueue(c, c->d_z, K, order, c->d_f, order >= 1 ? c->d_jac : nullptr);
+        Enqueue(c, c->d_z, K, order, c->d_f, order >= 1 ? c->d_jac : nullptr, order == 2 ? c->d_hess : nullptr);
         CUDA_CHECK(cudaMemcpyAsync(c->h_f, c->d_f, fr * K, cudaMemcpyDeviceToHost, c->stream));
         if (order >= 1) CUDA_CHECK(cudaMemcpyAsync(c->h_jac, c->d_jac, jr * K, cudaMemcpyDeviceToHost, c->stream));
+        if (order == 2) CUDA_CHECK(cudaMemcpyAsync(c->h_hess, c->d_hess, hr * K, cudaMemcpyDeviceToHost, c->stream));
         CUDA_CHECK(cudaStreamEndCapture(c->stream, &graph));
         CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
         CUDA_CHECK(cudaGraphDestroy(graph));
@@ -742,20 +780,23 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
       CUDA_CHECK(cudaStreamSynchronize(c->stream));
       std::memcpy(f, c->h_f, fr * K);
       if (order >= 1) std::memcpy(jac, c->h_jac, jr * K);
+      if (order == 2) std::memcpy(hess, c->h_hess, hr * K);
       return;
     }
     // Page-locked caller buffers are DMA'd directly; pageable ones go through
     // the context's pinned staging.
-    const bool pinned = IsPinned(z) && IsPinned(f) && (order < 1 || IsPinned(jac));
+    const bool pinned = IsPinned(z) && IsPinned(f) && (order < 1 || IsPinned(jac)) && (order < 2 || IsPinned(hess));
     const double* hz = z;
     double* hf = f;
     double* hj = jac;
+    double* hh = hess;
     if (!pinned) {
       EnsureStaging(c);
       std::memcpy(c->h_z, z, zr * K);
       hz = c->h_z;
       hf = c->h_f;
       hj = c->h_jac;
+      hh = c->h_hess;
     }
     // Large batches: chunk so H2D(i+1) and D2H(i−1) overlap kernel(i).
     const int chunks = K >= kChunkMinRows ? kMaxChunks : 1;
@@ -768,18 +809,23 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
       CUDA_CHECK(cudaMemcpyAsync(c->d_z + r0 * m->n_in, hz + r0 * m->n_in, zr * n, cudaMemcpyHostToDevice, c->s_in));
       CUDA_CHECK(cudaEventRecord(c->ev_in[i], c->s_in));
       CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_in[i], 0));
-      Enqueue(c, c->d_z + r0 * m->n_in, n, order, c->d_f + r0 * m->n_out, order >= 1 ? c->d_jac + r0 * m->n_out * m->n_in : nullptr);
+      const long long nh = static_cast<long long>(m->n_out) * m->n_in * m->n_in;
+      Enqueue(c, c->d_z + r0 * m->n_in, n, order, c->d_f + r0 * m->n_out,
+              order >= 1 ? c->d_jac + r0 * m->n_out * m->n_in : nullptr, order == 2 ? c->d_hess + r0 * nh : nullptr);
       CUDA_CHECK(cudaEventRecord(c->ev_k[i], c->stream));
       CUDA_CHECK(cudaStreamWaitEvent(c->s_out, c->ev_k[i], 0));
       CUDA_CHECK(cudaMemcpyAsync(hf + r0 * m->n_out, c->d_f + r0 * m->n_out, fr * n, cudaMemcpyDeviceToHost, c->s_out));
       if (order >= 1)
         CUDA_CHECK(cudaMemcpyAsync(hj + r0 * m->n_out * m->n_in, c->d_jac + r0 * m->n_out * m->n_in, jr * n,
                                    cudaMemcpyDeviceToHost, c->s_out));
+      if (order == 2)
+        CUDA_CHECK(cudaMemcpyAsync(hh + r0 * nh, c->d_hess + r0 * nh, hr * n, cudaMemcpyDeviceToHost, c->s_out));
     }
     CUDA_CHECK(cudaStreamSynchronize(c->s_out));
     if (!pinned) {
       std::memcpy(f, c->h_f, fr * K);
       if (order >= 1) std::memcpy(jac, c->h_jac, jr * K);
+      if (order == 2) std::memcpy(hess, c->h_hess, hr * K);
     }
   });
 }
@@ -789,11 +835,12 @@ rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int or
   return Guard([&] {
     CheckCall(c, K, order);
     if (d_hess != nullptr && order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless order == 2");
-    if (K > 0 && (!d_z || !d_f || (order >= 1 && !d_jac))) throw Error(RTN_ECONFIG, "null buffer");
+    if (K > 0 && (!d_z || !d_f || (order >= 1 && !d_jac) || (order == 2 && !d_hess)))
+      throw Error(RTN_ECONFIG, "null buffer");
     c->calls += 1;
     c->points += static_cast<unsigned long long>(K);
     CUDA_CHECK(cudaSetDevice(c->model->device));
-    Enqueue(c, d_z, K, order, d_f, d_jac);
+    Enqueue(c, d_z, K, order, d_f, d_jac, d_hess);
   });
 }
 

@@ -40,7 +40,7 @@ constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x
 // NTC = operand row stride per CTA (max rows per CTA): 80 for throughput
 // tiles (P = 4 quadrotor nodes = 72 rows; P = 2 in 3xTF32 at width 512),
 // 24 for latency tiles (P = 1).
-template <int WP, int NSTAGE, int P, int NTC, int MODE>
+template <int WP, int NSTAGE, int P, int NTC, int MODE, bool ORD2 = false>
 struct PairCfg {
   static constexpr int kEB = MODE == kBF16x3 ? 2 : 4;  // operand element bytes
   static constexpr int kCK = 128 / kEB;                // k per 128-byte chunk row
@@ -67,11 +67,12 @@ struct PairCfg {
   static_assert((128 - NTC) * 128 <= NSTAGE * kStageBytes, "A-operand overrun must stay in smem");
 };
 
-template <int WP, int NSTAGE, int P, int NTC, int MODE>
+template <int WP, int NSTAGE, int P, int NTC, int MODE, bool ORD2 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_pair_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
-  using C = PairCfg<WP, NSTAGE, P, NTC, MODE>;
+  using C = PairCfg<WP, NSTAGE, P, NTC, MODE, ORD2>;
+  static_assert(!ORD2 || NTC == kNtc2, "order-2 tiles are 2 x 48 rows");
   constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG, SPLIT = C::kSplit, CPG = C::kCPG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -232,7 +233,164 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ++ar;
       }
     }
-  } else if (warp >= 4 && !(prm.dbg & 128)) {
+  } else if (warp >= 4) {
+   if constexpr (ORD2) {
+    // ===================== order-2 epilogue ==================================
+    // Pair-tile t holds node t/2, Hessian group g = t%2: side 0 rows 0..17 are
+    // the carrier (value + 17 tangents), side-0 rows 18..47 and side-1 rows
+    // 0..47 are packed Hessian rows g·78 + slot. Every thread sees all 96
+    // columns of its neuron in TMEM, so the carrier's pre-activations (value,
+    // tangents T_a) are at hand for h' = σ'·H + σ''·T_a·T_b.
+    const int half = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int tid_h = q * 32 + lane;
+    const int etid = threadIdx.x - 128;
+    const int act = prm.act;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const int u = ((tid_h * C::kEB) >> 4) & 7;
+    int swz[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) swz[i] = ((u ^ i) - u) * 16 + i * 128;
+    const uint32_t act_local = smem_u32(act_s);
+    const bool local_side = half == static_cast<int>(rank);
+    const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
+    uint32_t ready_cl[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);
+    uint32_t hl = 0, tiles_done = 0;
+    using Seq0 = std::make_integer_sequence<int, kNtc2 - kCarrier2>;  // side-0 Hessian slots
+    using Seq1 = std::make_integer_sequence<int, kNtc2>;              // side-1 Hessian slots
+
+    auto store_side = [&](const float* v, int j) {
+      const uint32_t base =
+          side_base + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) + ((j * C::kEB) & 15);
+#pragma unroll
+      for (int i = 0; i < NTC; ++i) {
+        const uint32_t a = base + (i >> 3) * 1024 + swz[i & 7];
+        if constexpr (MODE == kTF32) {
+          if (local_side) st_shared_f32(a, to_tf32(v[i]));
+          else st_cluster_f32(a, to_tf32(v[i]));
+        } else if constexpr (MODE == k3xTF32) {
+          const float h = to_tf32(v[i]), lo = to_tf32(v[i] - h);
+          if (local_side) { st_shared_f32(a, h); st_shared_f32(a + C::kSplitStride, lo); }
+          else { st_cluster_f32(a, h); st_cluster_f32(a + C::kSplitStride, lo); }
+        } else {
+          const uint16_t h = bf16_rn_bits(v[i]), lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
+          if (local_side) { st_shared_u16(a, h); st_shared_u16(a + C::kSplitStride, lo); }
+          else { st_cluster_u16(a, h); st_cluster_u16(a + C::kSplitStride, lo); }
+        }
+      }
+    };
+    auto publish = [&](int grp) {
+      fence_proxy_async_cluster();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(ready_cl[grp]);
+    };
+    // v: this half's 48 rows; T: carrier tangents (pre-activation); hg: Hessian group.
+    auto epi_rows = [&](float* v, const float* T, float val, float sp, float spp, int hg) {
+      if (half == 0) {
+        v[0] = val;
+#pragma unroll
+        for (int a = 0; a < kNin2; ++a) v[1 + a] = sp * T[a];
+        if (hg == 0) hrows<0, kCarrier2>(v, T, sp, spp, Seq0{});
+        else hrows<kSlots2, kCarrier2>(v, T, sp, spp, Seq0{});
+      } else {
+        if (hg == 0) hrows<kNtc2 - kCarrier2, 0>(v, T, sp, spp, Seq1{});
+        else hrows<kSlots2 + kNtc2 - kCarrier2, 0>(v, T, sp, spp, Seq1{});
+      }
+    };
+    auto do_block = [&](int mb, int l, int hg) {
+      const int grp = 2 * mb + static_cast<int>(rank);
+      const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
+      const float bj = __ldg(prm.bh + l * WP + j);
+      const uint32_t tb = tmem_base + lane_base + mb * kTmemStride2;
+      mbar_wait_sleep(&tmem_full[mb], hl & 1);
+      tc_fence_after();
+      float v[kNtc2], car[24];
+#pragma unroll
+      for (int c0 = 0; c0 < kNtc2; c0 += 8) tmem_ld8(tb + half * kNtc2 + c0, v + c0);
+#pragma unroll
+      for (int c0 = 0; c0 < 24; c0 += 8) tmem_ld8(tb + c0, car + c0);
+      tmem_ld_wait();
+      tc_fence_before();
+      float val, sp, spp;
+      act_fwd2(act, car[0] + bj, val, sp, spp);
+      epi_rows(v, car + 1, val, sp, spp, hg);
+      mbar_wait_sleep(&in_free[grp], hl & 1);
+      store_side(v, j);
+      publish(grp);
+    };
+
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
+      const long long node = tile >> 1;
+      const int hg = static_cast<int>(tile & 1);
+      if (tiles_done > 0) {
+        mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
+        tc_fence_after();
+      }
+      if (etid < kNin2) zs[etid] = node < prm.K ? static_cast<float>(prm.z[node * kNin2 + etid]) : 0.0f;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // ---- layer 0: v = σ(pre), t_a = σ'·W0'[:,a], h_ab = σ''·W0'[:,a]·W0'[:,b]
+      for (int g = static_cast<int>(rank); g < NG; g += 2) {
+        const int j = g * 128 + tid_h;
+        float w[kNin2];
+        float pre = __ldg(prm.b0 + j);
+#pragma unroll
+        for (int k = 0; k < kNin2; ++k) {
+          w[k] = __ldg(prm.w0 + j * kNin2 + k);
+          pre = fmaf(w[k], zs[k], pre);
+        }
+        float val, sp, spp;
+        act_fwd2(act, pre, val, sp, spp);
+        float v[kNtc2];
+        if (half == 0) {
+          v[0] = val;
+#pragma unroll
+          for (int a = 0; a < kNin2; ++a) v[1 + a] = sp * w[a];
+          if (hg == 0) hrows0<0, kCarrier2>(v, w, spp, Seq0{});
+          else hrows0<kSlots2, kCarrier2>(v, w, spp, Seq0{});
+        } else {
+          if (hg == 0) hrows0<kNtc2 - kCarrier2, 0>(v, w, spp, Seq1{});
+          else hrows0<kSlots2 + kNtc2 - kCarrier2, 0>(v, w, spp, Seq1{});
+        }
+        store_side(v, j);
+        publish(g);
+      }
+      for (int l = 0; l < n_mma_layers; ++l, ++hl)
+        for (int mb = 0; mb < NMB; ++mb) do_block(mb, l, hg);
+      // ---- output layer: lane = this CTA side's row; columns = outputs
+      mbar_wait_sleep(tmem_last, tiles_done & 1);
+      tc_fence_after();
+      if (half == 0) {
+        float o[16];
+        tmem_ld16(tmem_base + lane_base, o);
+        tmem_ld_wait();
+        const int r = tid_h, n_out = prm.n_out;
+        if (node < prm.K && r < kNtc2) {
+          if (rank == 0 && r < kCarrier2) {
+            if (hg == 0) {
+              if (r == 0)
+                for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+              else
+                for (int oo = 0; oo < n_out; ++oo) prm.jac[(node * n_out + oo) * kNin2 + (r - 1)] = static_cast<double>(o[oo]);
+            }
+          } else {
+            const int slot = rank == 0 ? r - kCarrier2 : (kNtc2 - kCarrier2) + r;
+            const int p2 = hg * kSlots2 + slot;
+            if (p2 < kPairs2 && prm.hess != nullptr) {
+              const PairAB ab = pair_ab(p2, kNin2);
+              for (int oo = 0; oo < n_out; ++oo) {
+                double* h = prm.hess + (node * n_out + oo) * kNin2 * kNin2;
+                h[ab.a * kNin2 + ab.b] = static_cast<double>(o[oo]);
+                h[ab.b * kNin2 + ab.a] = static_cast<double>(o[oo]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+    }
+   } else if (!(prm.dbg & 128)) {
     // ===================== epilogue (8 warps per CTA) ========================
     // Thread = one neuron (TMEM lane) of this CTA's 128-neuron half of a
     // 256-block; warp half h owns the rows of side h (the P nodes whose
@@ -414,6 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
     }
+   }
   }
   if (prm.trace && pair == 0 && threadIdx.x == 0) {
     prm.trace[252 + rank] = globaltimer();

@@ -7,10 +7,10 @@
 
 namespace rtn {
 
-template <int WP, int NS, int P, int NTC, int MODE>
+template <int WP, int NS, int P, int NTC, int MODE, bool ORD2 = false>
 cudaError_t LaunchPairT(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
-  using Cfg = PairCfg<WP, NS, P, NTC, MODE>;
-  auto kern = rtn_pair_kernel<WP, NS, P, NTC, MODE>;
+  using Cfg = PairCfg<WP, NS, P, NTC, MODE, ORD2>;
+  auto kern = rtn_pair_kernel<WP, NS, P, NTC, MODE, ORD2>;
   static bool attr_set = false;  // per instantiation, per process
   if (!attr_set) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
