@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librtn_mpc.so")
+# RTN_LIB overrides the library path (A/B comparisons of builds on one box).
+LIB_PATH = os.environ.get("RTN_LIB", os.path.join(_HERE, "librtn_mpc.so"))
 
 RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL = range(6)
 RTN_TF32, RTN_3XTF32, RTN_BF16X3 = range(3)
