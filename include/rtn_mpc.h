@@ -47,7 +47,8 @@ typedef enum {
   RTN_EDOMAIN = 2,      /* InputDomainError: feature dim mismatch, K out of range */
   RTN_EUNSUPPORTED = 3, /* UnsupportedError: e.g. Hessians of a relu net */
   RTN_ECUDA = 4,        /* CUDA runtime failure (or no sm_100 device) */
-  RTN_ENCCL = 5         /* reserved for the multi-GPU gather */
+  RTN_ENCCL = 5,        /* reserved for the multi-GPU gather */
+  RTN_ERUNTIME = 6      /* std::runtime_error of BuildQp: "build qp: node k: ..." (sqp_rti.cpp:134-138) */
 } rtn_status;
 
 typedef enum {
@@ -105,6 +106,88 @@ rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* batched_calls,
                             unsigned long long* batched_points, unsigned long long* kernel_launches);
 
 const char* rtn_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Continuity-block builder (the step after PrepareNodes).
+ * Replaces the node loop of
+ *   QpData resmpc::BuildQp(const Plant&, const OcpConfig&, const Iterate&,
+ *       const ReferenceWindow&, const std::vector<TaylorApprox>* approxes, ...)
+ *       -- /root/reference/proj/include/resmpc/sqp_rti.hpp:56-59
+ *          /root/reference/proj/src/sqp_rti.cpp:59-155
+ * for the quadrotor plant (MakeQuadrotorPlant, proj/src/plant.cpp:34-85) with
+ * the 'full' residual variant (z = [x; u], 17 -> 6), in rtn mode, batched over
+ * n_inst independent MPC instances of horizon N. All arithmetic is fp64.
+ * Per node: RK4 sensitivities of f_F + embed·EvalTaylor (integrator.cpp:41-89).
+ * Errors: ConfigError -> RTN_ECONFIG (same messages as QuadParams::Validate,
+ * OcpConfig::Validate); a quaternion-domain or non-finite stage derivative at
+ * any node -> RTN_ERUNTIME with the reference's message for the lowest failing
+ * node ("build qp: node k: ..."; "instance i: " prefixed when n_inst > 1).
+ * ------------------------------------------------------------------------- */
+typedef struct { /* resmpc::QuadParams, proj/include/resmpc/dynamics.hpp:50-62 */
+  double mass;
+  double inertia[3];
+  double arm_length;
+  double torque_coeff;
+  double thrust_max;
+  double rotor_sign[4];
+} rtn_quad_params;
+
+typedef struct { /* resmpc::OcpConfig at quadrotor dims, sqp_rti.hpp:22-34 */
+  int horizon; /* N */
+  double dt;
+  double q_diag[13];
+  double r_diag[4];
+  int has_q_terminal; /* 0: TerminalWeight() = q_diag */
+  double q_terminal[13];
+  double u_min[4];
+  double u_max[4];
+  int taylor_order; /* 1 or 2 */
+} rtn_ocp_config;
+
+typedef struct { /* Iterate + ReferenceWindow, row-major, instance-major */
+  const double* xs;     /* n_inst x (N+1) x 13 */
+  const double* us;     /* n_inst x N x 4 */
+  const double* ref_xs; /* n_inst x (N+1) x 13 */
+  const double* ref_us; /* n_inst x N x 4 */
+} rtn_iterate;
+
+typedef struct { /* one TaylorApprox per node, K = n_inst*N rows (taylor.hpp:13-24) */
+  const double* z0;    /* K x 17 */
+  const double* f_bar; /* K x 6 */
+  const double* jac;   /* K x 6 x 17 */
+  const double* hess;  /* K x 6 x 17 x 17, taylor_order 2 only (else NULL) */
+} rtn_approx;
+
+typedef struct { /* QpData (proj/include/resmpc/qp.hpp:13-28); any pointer may be NULL = not wanted */
+  double* a;       /* K x 13 x 13 */
+  double* b;       /* K x 13 x 4 */
+  double* phi_res; /* K x 13 */
+  double* q;       /* n_inst x (N+1) x 13 */
+  double* r;       /* K x 4 */
+  double* hx_diag; /* n_inst x (N+1) x 13 */
+  double* hu_diag; /* K x 4 */
+  double* du_lb;   /* K x 4 */
+  double* du_ub;   /* K x 4 */
+} rtn_qp_blocks;
+
+/* BuildQp from prepared approximations (host buffers, blocking). fevals, if
+ * non-NULL, receives FevalCounter {values, jacobians} (+= 4 each per node). */
+rtn_status rtn_build_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
+                        const rtn_iterate* it, const rtn_approx* ap, rtn_qp_blocks* out,
+                        unsigned long long* fevals);
+
+/* Same with device pointers; enqueued on the context stream, then waits for
+ * the error word only (one 8-byte read) so errors surface like the reference. */
+rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg,
+                               long long n_inst, const rtn_iterate* d_it, const rtn_approx* d_ap,
+                               rtn_qp_blocks* d_out);
+
+/* Phases 1+2 of RtiController::Cycle fused on the device (sqp_rti.cpp:219-231):
+ * features z_k = [x_k; u_k] -> PrepareNodes(order = cfg->taylor_order) -> BuildQp.
+ * The context's model must be 17 -> 6. The approximations are returned too
+ * if f/jac/hess are non-NULL. Counts one batched call of K points. */
+rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
+                        const rtn_iterate* it, rtn_qp_blocks* out, double* f, double* jac, double* hess);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
 TEST_BIN = os.path.join(HERE, "build", "test_oracle")
+TEST_BLOCKS_BIN = os.path.join(HERE, "build", "test_blocks")
 ACTS = ("tanh", "relu", "silu")
 
 _lib = None
@@ -52,6 +53,10 @@ def lib() -> C.CDLL:
         L.oracle_quad_nodes.restype = None
         L.oracle_random_vector.argtypes = [C.c_ulonglong, C.c_int, C.c_double, C.c_double, _dp]
         L.oracle_random_vector.restype = None
+        L.oracle_blocks_last_error.restype = C.c_char_p
+        L.oracle_build_qp_quad.argtypes = ([_dp, _dp, C.c_int, C.c_int, C.c_int, C.c_longlong] + [_dp] * 8 +
+                                           [_dp] * 9 + [C.POINTER(C.c_ulonglong)])
+        L.oracle_quad_dynamics.argtypes = [_dp] * 6
         _lib = L
     return _lib
 
@@ -198,3 +203,43 @@ def to_product_model(om: OracleModel):
     layers = om.layers()
     im, isc, outm, outs = om.norm()
     return MlpModel(sizes, [w for w, _ in layers], [b for _, b in layers], act, "full", im, isc, outm, outs, 0)
+
+
+# ---------------------------------------------------------------------------
+# Continuity-block builder oracle (blocks_oracle.h): BuildQp for the quadrotor
+# 'full' plant, batched over instances (instance-major rows).
+def build_qp_quad(params_flat, cfg_flat, horizon, has_qf, order, xs, us, ref_xs, ref_us, z0, f_bar, jac, hess=None):
+    """Returns dict of QpData arrays + 'f_evals'. Raises OracleError with the
+    reference's message ("build qp: node k: ...") on failure."""
+    n = int(horizon)
+    xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, n + 1, 13)
+    n_inst = xs.shape[0]
+    k = n_inst * n
+    cast = lambda a, s: np.ascontiguousarray(a, dtype=np.float64).reshape(s)
+    ins = [cast(params_flat, (11,)), cast(cfg_flat, (39,))]
+    arrs = [xs, cast(us, (n_inst, n, 4)), cast(ref_xs, (n_inst, n + 1, 13)), cast(ref_us, (n_inst, n, 4)),
+            cast(z0, (k, 17)), cast(f_bar, (k, 6)), cast(jac, (k, 6, 17)),
+            cast(hess, (k, 6, 17, 17)) if order == 2 else None]
+    out = {"a": np.empty((n_inst, n, 13, 13)), "b": np.empty((n_inst, n, 13, 4)), "phi_res": np.empty((n_inst, n, 13)),
+           "q": np.empty((n_inst, n + 1, 13)), "r": np.empty((n_inst, n, 4)), "hx_diag": np.empty((n_inst, n + 1, 13)),
+           "hu_diag": np.empty((n_inst, n, 4)), "du_lb": np.empty((n_inst, n, 4)), "du_ub": np.empty((n_inst, n, 4))}
+    fe = (C.c_ulonglong * 2)()
+    st = lib().oracle_build_qp_quad(_p(ins[0]), _p(ins[1]), n, int(has_qf), int(order), n_inst,
+                                    *[_p(a) for a in arrs], *[_p(out[k_]) for k_ in
+                                                              ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag",
+                                                               "du_lb", "du_ub")], fe)
+    if st != 0:
+        raise OracleError(st, lib().oracle_blocks_last_error().decode())
+    out["f_evals"] = (fe[0], fe[1])
+    return out
+
+
+def quad_dynamics(params_flat, x, u):
+    """(dx, fx, fu) of the nominal quadrotor (dynamics.cpp:64-86, integrator.cpp:91-123)."""
+    dx, fx, fu = np.empty(13), np.empty((13, 13)), np.empty((13, 4))
+    st = lib().oracle_quad_dynamics(_p(np.ascontiguousarray(params_flat, dtype=np.float64)),
+                                    _p(np.ascontiguousarray(x, dtype=np.float64)),
+                                    _p(np.ascontiguousarray(u, dtype=np.float64)), _p(dx), _p(fx), _p(fu))
+    if st != 0:
+        raise OracleError(st, lib().oracle_blocks_last_error().decode())
+    return dx, fx, fu

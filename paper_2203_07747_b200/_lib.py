@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # RTN_LIB overrides the library path (A/B comparisons of builds on one box).
 LIB_PATH = os.environ.get("RTN_LIB", os.path.join(_HERE, "librtn_mpc.so"))
 
-RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL = range(6)
+RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL, RTN_ERUNTIME = range(7)
 RTN_TF32, RTN_3XTF32, RTN_BF16X3 = range(3)
 RTN_BF16 = RTN_BF16X3
 PRECISIONS = {"tf32": RTN_TF32, "3xtf32": RTN_3XTF32, "bf16x3": RTN_BF16X3}
@@ -22,7 +22,33 @@ EXPORTS = (
     "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info",
     "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
     "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_last_error",
+    "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp",
 )
+
+
+# Continuity-block builder structs (include/rtn_mpc.h). Pointers are void* so
+# the same structs carry host (rtn_build_qp) or device (rtn_build_qp_device) buffers.
+class QuadParamsC(C.Structure):
+    _fields_ = [("mass", C.c_double), ("inertia", C.c_double * 3), ("arm_length", C.c_double),
+                ("torque_coeff", C.c_double), ("thrust_max", C.c_double), ("rotor_sign", C.c_double * 4)]
+
+
+class OcpConfigC(C.Structure):
+    _fields_ = [("horizon", C.c_int), ("dt", C.c_double), ("q_diag", C.c_double * 13), ("r_diag", C.c_double * 4),
+                ("has_q_terminal", C.c_int), ("q_terminal", C.c_double * 13), ("u_min", C.c_double * 4),
+                ("u_max", C.c_double * 4), ("taylor_order", C.c_int)]
+
+
+class IterateC(C.Structure):
+    _fields_ = [("xs", C.c_void_p), ("us", C.c_void_p), ("ref_xs", C.c_void_p), ("ref_us", C.c_void_p)]
+
+
+class ApproxC(C.Structure):
+    _fields_ = [("z0", C.c_void_p), ("f_bar", C.c_void_p), ("jac", C.c_void_p), ("hess", C.c_void_p)]
+
+
+class QpBlocksC(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag", "du_lb", "du_ub")]
 
 _lib = None
 
@@ -58,6 +84,13 @@ def lib() -> C.CDLL:
     L.rtn_ctx_synchronize.argtypes = [_vp]
     L.rtn_ctx_counters.argtypes = [_vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong),
                                    C.POINTER(C.c_ulonglong)]
+    L.rtn_build_qp.argtypes = [_vp, C.POINTER(QuadParamsC), C.POINTER(OcpConfigC), C.c_longlong,
+                               C.POINTER(IterateC), C.POINTER(ApproxC), C.POINTER(QpBlocksC),
+                               C.POINTER(C.c_ulonglong)]
+    L.rtn_build_qp_device.argtypes = [_vp, C.POINTER(QuadParamsC), C.POINTER(OcpConfigC), C.c_longlong,
+                                      C.POINTER(IterateC), C.POINTER(ApproxC), C.POINTER(QpBlocksC)]
+    L.rtn_cycle_qp.argtypes = [_vp, C.POINTER(QuadParamsC), C.POINTER(OcpConfigC), C.c_longlong,
+                               C.POINTER(IterateC), C.POINTER(QpBlocksC), _vp, _vp, _vp]
     L.rtn_make_mlp.argtypes = [_ip, C.c_int, C.c_ulonglong, C.POINTER(_dp), C.POINTER(_dp)]
     L.rtn_synth_quad_nodes.argtypes = [C.c_ulonglong, C.c_longlong, _dp]
     L.rtn_synth_quad_nodes.restype = None

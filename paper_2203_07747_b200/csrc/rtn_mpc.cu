@@ -4,7 +4,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -15,6 +18,7 @@
 #include <vector>
 
 #include "../../include/rtn_mpc.h"
+#include "rtn_blocks.h"
 #include "rtn_fused.cuh"
 #include "rtn_launch.h"
 
@@ -175,6 +179,23 @@ struct rtn_ctx {
     cudaGraphExec_t exec;
   };
   std::vector<Graph> graphs;
+  // continuity-block builder: contiguous device in/out areas and pinned
+  // staging, grown on demand; the per-call error word; cycle graphs.
+  double* d_qin = nullptr;
+  double* d_qout = nullptr;
+  double* h_qin = nullptr;
+  double* h_qout = nullptr;
+  size_t qin_cap = 0, qout_cap = 0, hqin_cap = 0, hqout_cap = 0;  // doubles
+  unsigned long long* d_bad = nullptr;
+  unsigned long long* h_bad = nullptr;
+  struct QpGraph {
+    long long n_inst;
+    int N, order;
+    unsigned mask;
+    cudaGraphExec_t exec;
+    unsigned long long kernels;  // kernel nodes per replay
+  };
+  std::vector<QpGraph> qp_graphs;
   ~rtn_ctx() {
     int prev;
     if (cudaGetDevice(&prev) == cudaSuccess) {
@@ -193,6 +214,13 @@ struct rtn_ctx {
       for (auto e : ev_in) cudaEventDestroy(e);
       for (auto e : ev_k) cudaEventDestroy(e);
       for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+      for (auto& g : qp_graphs) cudaGraphExecDestroy(g.exec);
+      cudaFree(d_qin);
+      cudaFree(d_qout);
+      cudaFreeHost(h_qin);
+      cudaFreeHost(h_qout);
+      cudaFree(d_bad);
+      cudaFreeHost(h_bad);
       cudaSetDevice(prev);
     }
   }
@@ -841,6 +869,373 @@ rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int or
     c->points += static_cast<unsigned long long>(K);
     CUDA_CHECK(cudaSetDevice(c->model->device));
     Enqueue(c, d_z, K, order, d_f, d_jac, d_hess);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Continuity-block builder host side (resmpc::BuildQp, sqp_rti.cpp:59-155).
+namespace {
+
+constexpr int kNx = 13, kNu = 4, kNf = 17, kNr = 6;
+
+// QuadParams::Validate (proj/src/dynamics.cpp:29-40), same messages.
+void ValidateQuad(const rtn_quad_params& p) {
+  if (!(p.mass > 0.0) || !(p.arm_length > 0.0) || !(p.torque_coeff > 0.0) || !(p.thrust_max > 0.0))
+    throw Error(RTN_ECONFIG, "quad params: mass, arm_length, torque_coeff, thrust_max must be positive");
+  if (!(std::min(p.inertia[0], std::min(p.inertia[1], p.inertia[2])) > 0.0))
+    throw Error(RTN_ECONFIG, "quad params: inertia must be positive");
+  double sum = 0.0;
+  for (int i = 0; i < 4; ++i) {
+    if (p.rotor_sign[i] != 1.0 && p.rotor_sign[i] != -1.0)
+      throw Error(RTN_ECONFIG, "quad params: rotor_sign entries must be +1 or -1");
+    sum += p.rotor_sign[i];
+  }
+  if (sum != 0.0) throw Error(RTN_ECONFIG, "quad params: need two rotors of each spin direction");
+}
+
+// OcpConfig::Validate(13, 4) (proj/src/sqp_rti.cpp:27-42), same messages.
+void ValidateCfg(const rtn_ocp_config& c) {
+  if (c.horizon < 1) throw Error(RTN_ECONFIG, "ocp config: horizon must be >= 1");
+  if (!(c.dt > 0.0)) throw Error(RTN_ECONFIG, "ocp config: dt must be positive");
+  for (double v : c.q_diag)
+    if (v < 0.0) throw Error(RTN_ECONFIG, "ocp config: weights must be nonnegative");
+  for (double v : c.r_diag)
+    if (v < 0.0) throw Error(RTN_ECONFIG, "ocp config: weights must be nonnegative");
+  for (int i = 0; i < kNu; ++i)
+    if (c.u_min[i] >= c.u_max[i]) throw Error(RTN_ECONFIG, "ocp config: u_min must be below u_max");
+  if (c.taylor_order != 1 && c.taylor_order != 2) throw Error(RTN_ECONFIG, "ocp config: taylor_order must be 1 or 2");
+}
+
+rtn::BlkParams MakeBlk(const rtn_quad_params& p, const rtn_ocp_config& c, long long n_inst) {
+  rtn::BlkParams b{};
+  b.n_inst = n_inst;
+  b.N = c.horizon;
+  b.order = c.taylor_order;
+  b.dt = c.dt;
+  b.mass = p.mass;
+  for (int i = 0; i < 3; ++i) b.inertia[i] = p.inertia[i];
+  // MixingMatrix (proj/src/dynamics.cpp:42-55), fp64 on the host
+  const double d = p.arm_length / std::sqrt(2.0);
+  const double rx[4] = {d, -d, d, -d}, ry[4] = {-d, d, d, -d};
+  for (int i = 0; i < 4; ++i) {
+    b.mix[0][i] = 0.0;
+    b.mix[1][i] = 0.0;
+    b.mix[2][i] = 1.0;
+    b.mix[3][i] = ry[i];
+    b.mix[4][i] = -rx[i];
+    b.mix[5][i] = p.rotor_sign[i] * p.torque_coeff;
+  }
+  for (int i = 0; i < kNx; ++i) {
+    b.qd[i] = c.q_diag[i];
+    b.qf[i] = c.has_q_terminal ? c.q_terminal[i] : c.q_diag[i];
+  }
+  for (int i = 0; i < kNu; ++i) {
+    b.rd[i] = c.r_diag[i];
+    b.umin[i] = c.u_min[i];
+    b.umax[i] = c.u_max[i];
+  }
+  return b;
+}
+
+// One host array <-> one slice of the contiguous device area.
+struct Slice {
+  const double* src;  // host input (nullptr for outputs)
+  double* dst;        // host output (nullptr for inputs)
+  size_t off, n;      // doubles
+};
+
+struct QpPlan {
+  std::vector<Slice> in, out;
+  size_t in_total = 0, out_total = 0;
+  size_t add_in(const double* h, size_t n) {
+    in.push_back({h, nullptr, in_total, n});
+    in_total += n;
+    return in.back().off;
+  }
+  size_t add_out(double* h, size_t n) {  // null host pointer: not wanted
+    if (!h) return SIZE_MAX;
+    out.push_back({nullptr, h, out_total, n});
+    out_total += n;
+    return out.back().off;
+  }
+};
+
+void Grow(double** d, size_t* cap, size_t need, bool pinned) {
+  if (need <= *cap) return;
+  if (pinned) {
+    cudaFreeHost(*d);
+    *d = nullptr;
+    *cap = 0;
+    CUDA_CHECK(cudaMallocHost(d, need * sizeof(double)));
+  } else {
+    cudaFree(*d);
+    *d = nullptr;
+    *cap = 0;
+    CUDA_CHECK(cudaMalloc(d, need * sizeof(double)));
+  }
+  *cap = need;
+}
+
+std::string QpErrorMessage(unsigned long long w, int N, long long n_inst) {
+  const long long node = static_cast<long long>(w >> 8);
+  const int code = static_cast<int>(w & 0xff);
+  const long long inst = node / N, k = node % N;
+  std::string what = code / 10 == 1 ? "quad dynamics: quaternion norm too far from unit"
+                                     : "rk4: non-finite derivative at stage " + std::to_string(code % 10);
+  std::string msg = "build qp: node " + std::to_string(k) + ": " + what;
+  if (n_inst > 1) msg = "instance " + std::to_string(inst) + ": " + msg;
+  return msg;
+}
+
+bool AllPinned(const QpPlan& plan) {
+  for (const Slice& s : plan.in)
+    if (!IsPinned(s.src)) return false;
+  for (const Slice& s : plan.out)
+    if (!IsPinned(s.dst)) return false;
+  return true;
+}
+
+// Shared driver of rtn_build_qp (approximations given) and rtn_cycle_qp
+// (approximations computed on the device from z_k = [x_k; u_k]).
+void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst, const rtn_iterate* it,
+           const rtn_approx* ap, rtn_qp_blocks* out, bool cycle, double* f, double* jac, double* hess) {
+  if (!p || !cfg) throw Error(RTN_ECONFIG, "null argument");
+  ValidateQuad(*p);  // configuration errors first, as BuildQp validates before any work
+  ValidateCfg(*cfg);
+  if (!c || !it || !out || (!cycle && !ap)) throw Error(RTN_ECONFIG, "null argument");
+  const int N = cfg->horizon, order = cfg->taylor_order;
+  if (n_inst < 0) throw Error(RTN_EDOMAIN, "n_inst must be >= 0");
+  const long long K = n_inst * N;
+  if (K > c->max_rows) throw Error(RTN_EDOMAIN, "n_inst * horizon exceeds the context's max_rows");
+  const rtn_model* m = c->model;
+  if (cycle) {
+    if (m->n_in != kNf || m->n_out != kNr)
+      throw Error(RTN_ECONFIG, "rtn controller: model is " + std::to_string(m->n_in) + " -> " +
+                                   std::to_string(m->n_out) + ", the quadrotor 'full' plant needs 17 -> 6");
+    if (order > c->max_order) throw Error(RTN_EUNSUPPORTED, "taylor_order exceeds the context's max_order");
+    if (order == 2 && m->act == RTN_ACT_RELU)
+      throw Error(RTN_EUNSUPPORTED, "mlp hessian: relu networks are not twice differentiable");
+  }
+  if (K > 0 && (!it->xs || !it->us || !it->ref_xs || !it->ref_us)) throw Error(RTN_ECONFIG, "null iterate buffer");
+  if (!cycle && K > 0 && (!ap->z0 || !ap->f_bar || !ap->jac || (order == 2 && !ap->hess)))
+    throw Error(RTN_ECONFIG, "null approximation buffer");
+  if (cycle) {
+    c->calls += 1;  // one batched model call per cycle (SPEC; test_sqp_rti.cpp:246-247)
+    c->points += static_cast<unsigned long long>(K);
+  }
+  if (K == 0) return;
+  CUDA_CHECK(cudaSetDevice(m->device));
+
+  const size_t X = static_cast<size_t>(n_inst) * (N + 1) * kNx, U = static_cast<size_t>(K) * kNu,
+               Kz = static_cast<size_t>(K);
+  QpPlan plan;
+  const size_t o_xs = plan.add_in(it->xs, X), o_us = plan.add_in(it->us, U), o_rxs = plan.add_in(it->ref_xs, X),
+               o_rus = plan.add_in(it->ref_us, U);
+  size_t o_z0 = 0, o_fb = 0, o_jac = 0, o_hess = 0;
+  if (!cycle) {
+    o_z0 = plan.add_in(ap->z0, Kz * kNf);
+    o_fb = plan.add_in(ap->f_bar, Kz * kNr);
+    o_jac = plan.add_in(ap->jac, Kz * kNr * kNf);
+    if (order == 2) o_hess = plan.add_in(ap->hess, Kz * kNr * kNf * kNf);
+  }
+  const size_t o_a = plan.add_out(out->a, Kz * kNx * kNx), o_b = plan.add_out(out->b, Kz * kNx * kNu),
+               o_phi = plan.add_out(out->phi_res, Kz * kNx), o_q = plan.add_out(out->q, X),
+               o_r = plan.add_out(out->r, U), o_hx = plan.add_out(out->hx_diag, X), o_hu = plan.add_out(out->hu_diag, U),
+               o_lb = plan.add_out(out->du_lb, U), o_ub = plan.add_out(out->du_ub, U);
+  // device-side approximations of the cycle are copied out like the blocks
+  Slice sf{nullptr, f, 0, Kz * kNr}, sj{nullptr, jac, 0, Kz * kNr * kNf}, sh{nullptr, hess, 0, Kz * kNr * kNf * kNf};
+
+  Grow(&c->d_qin, &c->qin_cap, plan.in_total, false);
+  Grow(&c->d_qout, &c->qout_cap, std::max<size_t>(plan.out_total, 1), false);
+  if (!c->d_bad) {
+    CUDA_CHECK(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
+    CUDA_CHECK(cudaMallocHost(&c->h_bad, sizeof(unsigned long long)));
+  }
+  double* din = c->d_qin;
+  double* dout = c->d_qout;
+  rtn::BlkParams b = MakeBlk(*p, *cfg, n_inst);
+  b.xs = din + o_xs;
+  b.us = din + o_us;
+  b.rxs = din + o_rxs;
+  b.rus = din + o_rus;
+  if (cycle) {
+    b.z0 = nullptr;  // z0 = [x_k; u_k], the point PrepareNodes was evaluated at
+    b.fbar = c->d_f;
+    b.jac = c->d_jac;
+    b.hess = order == 2 ? c->d_hess : nullptr;
+  } else {
+    b.z0 = din + o_z0;
+    b.fbar = din + o_fb;
+    b.jac = din + o_jac;
+    b.hess = order == 2 ? din + o_hess : nullptr;
+  }
+  auto outp = [dout](size_t off) { return off == SIZE_MAX ? nullptr : dout + off; };
+  b.a = outp(o_a);
+  b.b = outp(o_b);
+  b.phi = outp(o_phi);
+  b.q = outp(o_q);
+  b.r = outp(o_r);
+  b.hx = outp(o_hx);
+  b.hu = outp(o_hu);
+  b.lb = outp(o_lb);
+  b.ub = outp(o_ub);
+  b.first_bad = c->d_bad;
+
+  auto enqueue_compute = [&](cudaStream_t s) {
+    CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
+    if (cycle) {
+      CUDA_CHECK(rtn::LaunchFeaturesFull(b.xs, b.us, n_inst, N, c->d_z, s));
+      Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr);
+    }
+    CUDA_CHECK(rtn::LaunchQpBlocks(b, s));
+    c->launches += cycle ? 2 : 1;
+  };
+  const unsigned mask = (out->a ? 1u : 0) | (out->b ? 2u : 0) | (out->phi_res ? 4u : 0) | (out->q ? 8u : 0) |
+                        (out->r ? 16u : 0) | (out->hx_diag ? 32u : 0) | (out->hu_diag ? 64u : 0) |
+                        (out->du_lb ? 128u : 0) | (out->du_ub ? 256u : 0) | (f ? 512u : 0) | (jac ? 1024u : 0) |
+                        (hess ? 2048u : 0);
+  const bool staged = c->latency_mode || !AllPinned(plan) || (f && !IsPinned(f)) || (jac && !IsPinned(jac)) ||
+                      (hess && !IsPinned(hess));
+  cudaStream_t s = c->stream;
+  if (staged) {
+    // Pack everything through contiguous pinned staging: one H2D, one D2H.
+    size_t extra = 0;
+    if (cycle) extra = (f ? sf.n : 0) + (jac ? sj.n : 0) + (hess ? sh.n : 0);
+    Grow(&c->h_qin, &c->hqin_cap, plan.in_total, true);
+    Grow(&c->h_qout, &c->hqout_cap, plan.out_total + extra + 1, true);
+    for (const Slice& sl : plan.in) std::memcpy(c->h_qin + sl.off, sl.src, sl.n * sizeof(double));
+    size_t eo = plan.out_total;
+    const size_t o_f = f ? eo : 0;
+    eo += f ? sf.n : 0;
+    const size_t o_j = jac ? eo : 0;
+    eo += jac ? sj.n : 0;
+    const size_t o_h = hess ? eo : 0;
+    auto body = [&](cudaStream_t st) {
+      CUDA_CHECK(cudaMemcpyAsync(din, c->h_qin, plan.in_total * sizeof(double), cudaMemcpyHostToDevice, st));
+      enqueue_compute(st);
+      if (plan.out_total)
+        CUDA_CHECK(cudaMemcpyAsync(c->h_qout, dout, plan.out_total * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (cycle && f) CUDA_CHECK(cudaMemcpyAsync(c->h_qout + o_f, c->d_f, sf.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (cycle && jac)
+        CUDA_CHECK(cudaMemcpyAsync(c->h_qout + o_j, c->d_jac, sj.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (cycle && hess)
+        CUDA_CHECK(cudaMemcpyAsync(c->h_qout + o_h, c->d_hess, sh.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    };
+    if (c->latency_mode && K <= kGraphMaxRows) {
+      const unsigned key = mask | (cycle ? 1u << 31 : 0);
+      const rtn_ctx::QpGraph* g = nullptr;
+      for (const auto& e : c->qp_graphs)
+        if (e.n_inst == n_inst && e.N == N && e.order == order && e.mask == key) g = &e;
+      if (!g) {
+        body(s);  // first run outside capture (kernel attributes, lazy loading)
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        const unsigned long long l0 = c->launches;
+        CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        body(s);
+        CUDA_CHECK(cudaStreamEndCapture(s, &graph));
+        const unsigned long long per = c->launches - l0;
+        c->launches = l0;  // the capture pass launched nothing
+        CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+        CUDA_CHECK(cudaGraphDestroy(graph));
+        c->qp_graphs.push_back({n_inst, N, order, key, exec, per});
+      } else {
+        CUDA_CHECK(cudaGraphLaunch(g->exec, s));
+        c->launches += g->kernels;
+      }
+    } else {
+      body(s);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (*c->h_bad != rtn::kNoError) throw Error(RTN_ERUNTIME, QpErrorMessage(*c->h_bad, N, n_inst));
+    for (const Slice& sl : plan.out) std::memcpy(sl.dst, c->h_qout + sl.off, sl.n * sizeof(double));
+    if (cycle && f) std::memcpy(f, c->h_qout + o_f, sf.n * sizeof(double));
+    if (cycle && jac) std::memcpy(jac, c->h_qout + o_j, sj.n * sizeof(double));
+    if (cycle && hess) std::memcpy(hess, c->h_qout + o_h, sh.n * sizeof(double));
+    return;
+  }
+  // Caller buffers are page-locked: DMA each array directly.
+  for (const Slice& sl : plan.in)
+    CUDA_CHECK(cudaMemcpyAsync(din + sl.off, sl.src, sl.n * sizeof(double), cudaMemcpyHostToDevice, s));
+  enqueue_compute(s);
+  CUDA_CHECK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  for (const Slice& sl : plan.out)
+    CUDA_CHECK(cudaMemcpyAsync(sl.dst, dout + sl.off, sl.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (cycle && f) CUDA_CHECK(cudaMemcpyAsync(f, c->d_f, sf.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (cycle && jac) CUDA_CHECK(cudaMemcpyAsync(jac, c->d_jac, sj.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (cycle && hess) CUDA_CHECK(cudaMemcpyAsync(hess, c->d_hess, sh.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  if (*c->h_bad != rtn::kNoError) throw Error(RTN_ERUNTIME, QpErrorMessage(*c->h_bad, N, n_inst));
+}
+
+}  // namespace
+
+extern "C" {
+
+rtn_status rtn_build_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
+                        const rtn_iterate* it, const rtn_approx* ap, rtn_qp_blocks* out, unsigned long long* fevals) {
+  return Guard([&] {
+    RunQp(c, p, cfg, n_inst, it, ap, out, false, nullptr, nullptr, nullptr);
+    if (fevals) {  // FevalCounter: 4 values + 4 Jacobians per node (integrator.cpp:79-82)
+      fevals[0] = 4ull * static_cast<unsigned long long>(n_inst * cfg->horizon);
+      fevals[1] = fevals[0];
+    }
+  });
+}
+
+rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
+                               const rtn_iterate* it, const rtn_approx* ap, rtn_qp_blocks* out) {
+  return Guard([&] {
+    if (!c || !p || !cfg || !it || !ap || !out) throw Error(RTN_ECONFIG, "null argument");
+    ValidateQuad(*p);
+    ValidateCfg(*cfg);
+    if (n_inst < 0) throw Error(RTN_EDOMAIN, "n_inst must be >= 0");
+    const long long K = n_inst * cfg->horizon;
+    if (K == 0) return;
+    CUDA_CHECK(cudaSetDevice(c->model->device));
+    if (!c->d_bad) {
+      CUDA_CHECK(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
+      CUDA_CHECK(cudaMallocHost(&c->h_bad, sizeof(unsigned long long)));
+    }
+    rtn::BlkParams b = MakeBlk(*p, *cfg, n_inst);
+    b.xs = it->xs;
+    b.us = it->us;
+    b.rxs = it->ref_xs;
+    b.rus = it->ref_us;
+    b.z0 = ap->z0;
+    b.fbar = ap->f_bar;
+    b.jac = ap->jac;
+    b.hess = cfg->taylor_order == 2 ? ap->hess : nullptr;
+    if (!b.xs || !b.us || !b.rxs || !b.rus || !b.fbar || !b.jac || (cfg->taylor_order == 2 && !b.hess))
+      throw Error(RTN_ECONFIG, "null device buffer");
+    b.a = out->a;
+    b.b = out->b;
+    b.phi = out->phi_res;
+    b.q = out->q;
+    b.r = out->r;
+    b.hx = out->hx_diag;
+    b.hu = out->hu_diag;
+    b.lb = out->du_lb;
+    b.ub = out->du_ub;
+    b.first_bad = c->d_bad;
+    CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), c->stream));
+    CUDA_CHECK(rtn::LaunchQpBlocks(b, c->stream));
+    c->launches += 1;
+    CUDA_CHECK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    if (*c->h_bad != rtn::kNoError) throw Error(RTN_ERUNTIME, QpErrorMessage(*c->h_bad, cfg->horizon, n_inst));
+  });
+}
+
+rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
+                        const rtn_iterate* it, rtn_qp_blocks* out, double* f, double* jac, double* hess) {
+  return Guard([&] {
+    if (hess && cfg && cfg->taylor_order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless taylor_order == 2");
+    RunQp(c, p, cfg, n_inst, it, nullptr, out, true, f, jac, hess);
   });
 }
 

@@ -24,5 +24,6 @@ def raise_for_status(status: int) -> None:
         return
     from . import _lib
     msg = _lib.last_error()
-    cls = {1: ConfigError, 2: InputDomainError, 3: UnsupportedError}.get(status, DeviceError)
+    # 6: std::runtime_error of BuildQp ("build qp: node k: ...", sqp_rti.cpp:134-138)
+    cls = {1: ConfigError, 2: InputDomainError, 3: UnsupportedError, 6: RuntimeError}.get(status, DeviceError)
     raise cls(msg)
