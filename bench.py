@@ -247,6 +247,125 @@ def precision_modes(torch, z, k, sizes, steps=2):
     return out
 
 
+def _quad_iterate(np, n_inst, n, seed):
+    rng = np.random.default_rng(seed)
+    xs = np.empty((n_inst, n + 1, 13))
+    xs[..., 0:3] = rng.uniform(-2, 2, (n_inst, n + 1, 3))
+    q = rng.uniform(-1, 1, (n_inst, n + 1, 4))
+    xs[..., 3:7] = q / np.linalg.norm(q, axis=-1, keepdims=True)
+    xs[..., 7:10] = rng.uniform(-4, 4, (n_inst, n + 1, 3))
+    xs[..., 10:13] = rng.uniform(-3, 3, (n_inst, n + 1, 3))
+    us = rng.uniform(0.5, 5.0, (n_inst, n, 4))
+    return xs, us, xs + rng.normal(0, 0.1, xs.shape), us + rng.normal(0, 0.1, us.shape)
+
+
+def blocks_bench(torch, hbm_peak, steps=5):
+    """§8f rank 1: the continuity-block builder (csrc/rtn_blocks.cu) on the
+    cfg5 shape (65,536 instances x N=50), fp64. Device-resident throughput
+    with the HBM roofline, e2e through rtn_build_qp (pinned host buffers),
+    the fused PrepareNodes+BuildQp cycle latency at cfg3, and the oracle
+    BuildQp on the host as the CPU baseline."""
+    import numpy as np
+    import oracle
+    from paper_2203_07747_b200 import _lib, make_mlp, qp
+    from paper_2203_07747_b200.errors import raise_for_status
+    L = _lib.lib()
+    n_inst, n = INSTANCES, HORIZON
+    k = n_inst * n
+    xs, us, rx, ru = _quad_iterate(np, n_inst, n, 2203)
+    rng = np.random.default_rng(5)
+    z0 = np.concatenate([xs[:, :n], us], axis=-1).reshape(k, 17)
+    fb = rng.normal(0, 0.5, (k, 6))
+    jac = rng.normal(0, 0.1, (k, 6, 17))
+    p, cfg = qp.QuadParams(), qp.OcpConfig(horizon=n, dt=0.02, q_diag=np.ones(13), r_diag=np.full(4, 0.1))
+    model = make_mlp([17, 64, 6], "silu", "full", 1)  # context owner only; the builder does not touch it
+    eng = model.engine()
+    eng._ensure(k, 1)
+    st = torch.cuda.Stream()
+    raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d_in = [dev(a) for a in (xs, us, rx, ru, z0, fb, jac)]
+    shapes = {"a": (k, 13, 13), "b": (k, 13, 4), "phi_res": (k, 13), "q": (n_inst, n + 1, 13), "r": (k, 4),
+              "hx_diag": (n_inst, n + 1, 13), "hu_diag": (k, 4), "du_lb": (k, 4), "du_ub": (k, 4)}
+    d_out = {name: torch.empty(s, dtype=torch.float64, device="cuda") for name, s in shapes.items()}
+    it = _lib.IterateC(*[t.data_ptr() for t in d_in[:4]])
+    ap = _lib.ApproxC(d_in[4].data_ptr(), d_in[5].data_ptr(), d_in[6].data_ptr(), None)
+    oc = _lib.QpBlocksC(*[d_out[nm].data_ptr() for nm in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag",
+                                                             "du_lb", "du_ub")])
+    pc, cc = p.to_c(), cfg.to_c()
+    run = lambda: raise_for_status(L.rtn_build_qp_device(eng.ctx_ptr, C.byref(pc), C.byref(cc), n_inst, C.byref(it),
+                                                         C.byref(ap), C.byref(oc)))
+    with torch.cuda.stream(st):
+        run()
+        ms = []
+        for _ in range(steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            run()
+            e1.record(st)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    in_b = sum(a.numel() for a in d_in) * 8
+    out_b = sum(v.numel() for v in d_out.values()) * 8
+    gbs = (in_b + out_b) / (t * 1e-3) / 1e9
+    raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, None))
+    # e2e: the C-ABI call a user makes, pinned host buffers in and out
+    h_in = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (xs, us, rx, ru, z0, fb, jac)]
+    h_out = {name: torch.empty(s, dtype=torch.float64).pin_memory() for name, s in shapes.items()}
+    hit = _lib.IterateC(*[t_.data_ptr() for t_ in h_in[:4]])
+    hap = _lib.ApproxC(h_in[4].data_ptr(), h_in[5].data_ptr(), h_in[6].data_ptr(), None)
+    hoc = _lib.QpBlocksC(*[h_out[nm].data_ptr() for nm in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag",
+                                                              "du_lb", "du_ub")])
+    hrun = lambda: raise_for_status(L.rtn_build_qp(eng.ctx_ptr, C.byref(pc), C.byref(cc), n_inst, C.byref(hit),
+                                                   C.byref(hap), C.byref(hoc), None))
+    hrun()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        hrun()
+    e2e_s = (time.perf_counter() - t0) / 2
+    same = bool(torch.equal(h_out["a"], d_out["a"].cpu()))
+    del d_in, d_out, h_in, h_out
+    eng.close()
+    # fused phase 1+2 latency at cfg3 (12x512, N=20, one instance), host -> host
+    lat = {}
+    big = make_mlp(SIZES, "silu", "full", SEED)
+    for order in (1, 2):
+        b = qp.QpBuilder(big, latency_mode=1)
+        cfg3 = qp.OcpConfig(horizon=20, dt=0.02, q_diag=np.ones(13), r_diag=np.full(4, 0.1), taylor_order=order)
+        x3, u3, rx3, ru3 = _quad_iterate(np, 1, 20, 3)
+        for _ in range(30):
+            b.cycle_qp(p, cfg3, x3, u3, rx3, ru3)
+        ts = []
+        for _ in range(300 if order == 2 else 1000):
+            t0 = time.perf_counter()
+            b.cycle_qp(p, cfg3, x3, u3, rx3, ru3)
+            ts.append((time.perf_counter() - t0) * 1e6)
+        ts.sort()
+        lat[f"cfg3_cycle_order{order}"] = {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)],
+                                           "steps": len(ts),
+                                           "path": "rtn_cycle_qp: [x;u] features -> MLP (f,A,B" +
+                                                   (",H" if order == 2 else "") + ") -> RK4 blocks, one CUDA graph"}
+    # CPU baseline: the oracle's serial BuildQp (like the reference's per-instance loop)
+    ns = 64
+    t0 = time.perf_counter()
+    oracle.build_qp_quad(p.flat(), cfg.flat(), n, 0, 1, xs[:ns], us[:ns], rx[:ns], ru[:ns], z0[:ns * n], fb[:ns * n],
+                         jac[:ns * n])
+    cpu_s = time.perf_counter() - t0
+    return {"metric": "continuity blocks/s (A 13x13, B 13x4, phi_res + cost terms per node, fp64)",
+            "value": k / (t * 1e-3), "unit": "node-blocks/s", "ms_per_step": t, "nodes": k,
+            "kernel": "QpBlocksKernel (warp per node, fp64)", "gpu_launches_per_step": 1,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": gbs / hbm_peak if hbm_peak else None, "bytes_per_node": (in_b + out_b) / k,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "e2e": {"value": k / e2e_s, "unit": "node-blocks/s", "h2d_bytes_per_step": in_b, "d2h_bytes_per_step": out_b,
+                    "path": "rtn_build_qp (C-ABI), pinned host buffers", "matches_device_run": same},
+            "cpu_baseline": {"value": ns * n / cpu_s, "unit": "node-blocks/s", "cores": 1, "kind": "port",
+                             "sample": f"{ns} instances x {n} nodes in {cpu_s:.2f} s",
+                             "algorithm": "oracle/blocks_oracle.cpp BuildQp (sqp_rti.cpp:59-155), serial like the reference"},
+            "latency": lat}
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -392,6 +511,9 @@ def run_ours(args, rank, world, local_rank):
                    "cfg3_12x512_N20_bf16x3": latency(torch, SIZES, SEED, 20, steps=300, precision=2),
                    "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20),
                    "cfg1_2x64_N10": latency(torch, [17, 64, 64, 6], 2064, 10, steps=300)}
+        blocks = None
+        if world == 1 and not args.no_blocks:
+            blocks = blocks_bench(torch, peaks.get("hbm_gbs"))
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -420,6 +542,8 @@ def run_ours(args, rank, world, local_rank):
             result["precision_modes"] = modes
         if lat:
             result["latency"] = lat
+        if blocks:
+            result["blocks"] = blocks
     if world > 1:
         dist.barrier(device_ids=[local_rank])
         dist.destroy_process_group()
@@ -437,6 +561,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-modes", action="store_true")
+    ap.add_argument("--no-blocks", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = _env_int("RANK", 0)

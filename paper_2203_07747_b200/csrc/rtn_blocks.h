@@ -33,6 +33,7 @@ struct BlkParams {
   int N, order;
   double dt, mass;
   double inertia[3];
+  double inv_mass, inv_inertia[3];  // 1/m, 1/J_i in fp64 (multiplies replace the reference's divisions)
   double mix[6][4];  // MixingMatrix (dynamics.cpp:42-55), built on the host in fp64
   double qd[13], rd[4], qf[13], umin[4], umax[4];
 };

@@ -915,7 +915,11 @@ rtn::BlkParams MakeBlk(const rtn_quad_params& p, const rtn_ocp_config& c, long l
   b.order = c.taylor_order;
   b.dt = c.dt;
   b.mass = p.mass;
-  for (int i = 0; i < 3; ++i) b.inertia[i] = p.inertia[i];
+  b.inv_mass = 1.0 / p.mass;
+  for (int i = 0; i < 3; ++i) {
+    b.inertia[i] = p.inertia[i];
+    b.inv_inertia[i] = 1.0 / p.inertia[i];
+  }
   // MixingMatrix (proj/src/dynamics.cpp:42-55), fp64 on the host
   const double d = p.arm_length / std::sqrt(2.0);
   const double rx[4] = {d, -d, d, -d}, ry[4] = {-d, d, d, -d};
