@@ -25,12 +25,13 @@ constexpr int kWarps = 4;          // 8 nodes per CTA
 constexpr int kDkStride = 18;      // dk row stride (doubles): 16-byte aligned pairs
 constexpr int kDk = kQNx * kDkStride;
 
-// Per-node scratch. 600 doubles = 4800 B ≡ 64 (mod 128): the two nodes of a
-// warp sit in disjoint banks, so their broadcast loads do not conflict.
+// Per-node scratch. 712 doubles = 5696 B ≡ 64 (mod 128): the two
+// nodes of a warp sit in disjoint banks, so their broadcast loads do not conflict.
 struct NodeSmem {
   double dk[2][kDk];  // dk_{s-1} / dk_s rows, then the A|B staging area
   double x[kQNx], xs[kQNx], u[kQNu], z0[kQNf], dz[kQNf + 1], k[4][kQNx], phi[kQNx];
-  double pad[2];
+  double g[kQNr * kQNf];  // H_o·dz at the stage point (order 2)
+  double pad[12];
 };
 static_assert(sizeof(NodeSmem) % 128 == 64, "node stride must split the banks");
 
@@ -200,6 +201,17 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
     __syncwarp();
     for (int c = r; c < kQNf; c += 16) S.dz[c] = (c < kQNx ? S.xs[c] : S.u[c - kQNx]) - S.z0[c];
     __syncwarp();
+    if (ORDER == 2) {  // G[o][a] = Σ_b H_o(a,b)·dz_b, 102 rows spread over the half-warp
+      const double* hn = p.hess + node * (kQNr * kQNf * kQNf);
+      for (int e = r; e < kQNr * kQNf; e += 16) {
+        const double* h = hn + e * kQNf;
+        double g = 0.0;
+#pragma unroll
+        for (int b = 0; b < kQNf; ++b) g += __ldg(h + b) * S.dz[b];
+        S.g[e] = g;
+      }
+      __syncwarp();
+    }
     const double* X = S.xs;
     // stage Jacobian row: nominal + embed·EvalTaylorJacobian (taylor.cpp:66-74)
     double fx[kQNx], fu[kQNu], y = 0.0, fnom;
@@ -213,22 +225,15 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
 #pragma unroll
         for (int c = 0; c < kQNf; ++c) a1 += jr[c] * S.dz[c];
         y = fbo + a1;
-        if (ORDER == 2) {
-          const double* h = p.hess + (node * kQNr + o) * (kQNf * kQNf);
+        if (ORDER == 2) {  // + ½ dzᵀ H_o dz; jn row o += H_o·dz (taylor.cpp:60-73)
+          const double* G = S.g + o * kQNf;
           double qv = 0.0;
-#pragma unroll 1
-          for (int a = 0; a < kQNf; ++a) {
-            double g = 0.0;
 #pragma unroll
-            for (int b = 0; b < kQNf; ++b) g += __ldg(h + a * kQNf + b) * S.dz[b];
-            qv += S.dz[a] * g;
+          for (int a = 0; a < kQNf; ++a) qv += S.dz[a] * G[a];
 #pragma unroll
-            for (int c = 0; c < kQNx; ++c)
-              if (c == a) fx[c] += g;
+          for (int c = 0; c < kQNx; ++c) fx[c] += G[c];
 #pragma unroll
-            for (int c = 0; c < kQNu; ++c)
-              if (kQNx + c == a) fu[c] += g;
-          }
+          for (int c = 0; c < kQNu; ++c) fu[c] += G[kQNx + c];
           y += 0.5 * qv;
         }
       }
