@@ -324,18 +324,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
   }
 }
 
-__global__ void FeaturesFullKernel(const double* __restrict__ xs, const double* __restrict__ us, long long n_inst,
-                                   int N, double* __restrict__ z) {
-  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long K = n_inst * N;
-  if (e >= K * kQNf) return;
-  const long long node = e / kQNf;
-  const int c = static_cast<int>(e - node * kQNf);
-  const long long inst = node / N;
-  const long long xrow = inst * (N + 1) + (node - inst * N);
-  z[e] = c < kQNx ? xs[xrow * kQNx + c] : us[node * kQNu + (c - kQNx)];
-}
-
 }  // namespace
 
 cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s) {
@@ -347,14 +335,6 @@ cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s) {
     QpBlocksKernel<2><<<static_cast<unsigned>(grid), kWarps * 32, 0, s>>>(p);
   else
     QpBlocksKernel<1><<<static_cast<unsigned>(grid), kWarps * 32, 0, s>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t LaunchFeaturesFull(const double* xs, const double* us, long long n_inst, int N, double* z,
-                               cudaStream_t s) {
-  const long long total = n_inst * N * kQNf;
-  if (total <= 0) return cudaSuccess;
-  FeaturesFullKernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(xs, us, n_inst, N, z);
   return cudaGetLastError();
 }
 

@@ -39,8 +39,4 @@ struct BlkParams {
 };
 
 cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s);
-// z_k = [x_k; u_k] (ResidualInput 'full', dynamics.cpp:137-139), K x 17.
-cudaError_t LaunchFeaturesFull(const double* xs, const double* us, long long n_inst, int N, double* z,
-                               cudaStream_t s);
-
 }  // namespace rtn

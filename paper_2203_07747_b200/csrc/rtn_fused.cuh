@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) rtn_fused_kernel(const KParams pr
       if (etid < P * n_in) {
         const int p = etid / n_in, k = etid - p * n_in;
         const long long node = node0 + p;
-        zs[etid] = node < prm.K ? static_cast<float>(prm.z[node * n_in + k]) : 0.0f;
+        zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, k)) : 0.0f;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       // ---- layer 0 on CUDA cores: value rows + tangent rows σ'(pre)·W0'[:, k]

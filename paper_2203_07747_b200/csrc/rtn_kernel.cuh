@@ -68,7 +68,20 @@ struct KParams {
   const float* b0;   // WP
   const float* bh;   // (n_hidden-1) x WP
   const float* bl;   // kMaxOut     (out_scale ⊙ b_L + out_mean)
+  // Gather mode (rtn_cycle_qp): when zx != null, row k is the quadrotor feature
+  // vector [x_k; u_k] (ResidualInput 'full', dynamics.cpp:137-139) read straight
+  // from the iterate: zx = Iterate::xs (n_inst x (N+1) x 13), zu = us (K x 4).
+  const double* zx;
+  const double* zu;
+  int zN;
 };
+
+// Element k of node row `node` of the MLP input.
+__device__ __forceinline__ double load_z(const KParams& prm, long long node, int k) {
+  if (prm.zx == nullptr) return prm.z[node * prm.n_in + k];
+  const long long xrow = node + node / prm.zN;  // inst·(N+1) + n
+  return k < 13 ? prm.zx[xrow * 13 + k] : prm.zu[node * 4 + (k - 13)];
+}
 
 // ----------------------------------------------------------------------------
 // PTX wrappers

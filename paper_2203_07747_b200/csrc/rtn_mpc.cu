@@ -539,12 +539,17 @@ Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
   return Kern::kPair;
 }
 
+// d_zx/d_zu (optional): gather the quadrotor rows [x_k; u_k] from an iterate
+// (n_inst x (N+1) x 13 states, K x 4 inputs) instead of reading d_z.
 void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac,
-             double* d_hess = nullptr) {
+             double* d_hess = nullptr, const double* d_zx = nullptr, const double* d_zu = nullptr, int zN = 0) {
   const rtn_model* m = c->model;
   if (K == 0) return;
   rtn::KParams prm{};
   prm.z = d_z;
+  prm.zx = d_zx;
+  prm.zu = d_zu;
+  prm.zN = zN;
   prm.f = d_f;
   prm.jac = order >= 1 ? d_jac : nullptr;
   prm.K = K;
@@ -1089,12 +1094,10 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
 
   auto enqueue_compute = [&](cudaStream_t s) {
     CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
-    if (cycle) {
-      CUDA_CHECK(rtn::LaunchFeaturesFull(b.xs, b.us, n_inst, N, c->d_z, s));
-      Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr);
-    }
+    if (cycle)  // PrepareNodes at z_k = [x_k; u_k], gathered from the iterate inside layer 0
+      Enqueue(c, nullptr, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr, b.xs, b.us, N);
     CUDA_CHECK(rtn::LaunchQpBlocks(b, s));
-    c->launches += cycle ? 2 : 1;
+    c->launches += 1;
   };
   const unsigned mask = (out->a ? 1u : 0) | (out->b ? 2u : 0) | (out->phi_res ? 4u : 0) | (out->q ? 8u : 0) |
                         (out->r ? 16u : 0) | (out->hx_diag ? 32u : 0) | (out->hu_diag ? 64u : 0) |

@@ -328,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
         tc_fence_after();
       }
-      if (etid < kNin2) zs[etid] = node < prm.K ? static_cast<float>(prm.z[node * kNin2 + etid]) : 0.0f;
+      if (etid < kNin2) zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, etid)) : 0.0f;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       // ---- layer 0: v = σ(pre), t_a = σ'·W0'[:,a], h_ab = σ''·W0'[:,a]·W0'[:,b]
       for (int g = static_cast<int>(rank); g < NG; g += 2) {
@@ -520,7 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (etid < 2 * P * n_in) {
         const int p = etid / n_in, k = etid - p * n_in;
         const long long node = node0 + p;
-        zs[etid] = node < prm.K ? static_cast<float>(prm.z[node * n_in + k]) : 0.0f;
+        zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, k)) : 0.0f;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       // ---- layer 0 (CUDA cores): this CTA owns K-groups g ≡ rank (mod 2); half h writes side h
