@@ -280,7 +280,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
     __syncwarp();
   }
   if (failed) {
-    if (valid && r == 0) Report(p.first_bad, node, failed);
+    if (valid && r == 0) {
+      if (p.first_bad) Report(p.first_bad, node, failed);
+      if (p.status) p.status[node] = static_cast<unsigned char>(failed);
+    }
     return;  // per-lane exit: no warp-wide barrier follows
   }
 
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
   }
   __syncwarp(half_mask);
   if (!valid) return;
+  if (p.status && r == 0) p.status[node] = 0;
   if (p.a)
     for (int e = r; e < kQNx * kQNx; e += 16) p.a[node * (kQNx * kQNx) + e] = stage[e];
   if (p.b)

@@ -28,7 +28,8 @@ struct BlkParams {
   const double* hess;  // K x 6 x 17 x 17 (order 2) or null
   // outputs (device; any may be null): QpData rows
   double *a, *b, *phi, *q, *r, *hx, *hu, *lb, *ub;
-  unsigned long long* first_bad;
+  unsigned long long* first_bad;  // atomic error word (may be null), or
+  unsigned char* status;          // per-node status byte, 0 = ok (may be null; zero-copy latency mode)
   long long n_inst;
   int N, order;
   double dt, mass;

@@ -188,6 +188,8 @@ struct rtn_ctx {
   size_t qin_cap = 0, qout_cap = 0, hqin_cap = 0, hqout_cap = 0;  // doubles
   unsigned long long* d_bad = nullptr;
   unsigned long long* h_bad = nullptr;
+  unsigned char* h_status = nullptr;  // zero-copy latency mode: per-node status bytes
+  long long status_cap = 0;
   struct QpGraph {
     long long n_inst;
     int N, order;
@@ -221,6 +223,7 @@ struct rtn_ctx {
       cudaFreeHost(h_qout);
       cudaFree(d_bad);
       cudaFreeHost(h_bad);
+      cudaFreeHost(h_status);
       cudaSetDevice(prev);
     }
   }
@@ -232,6 +235,15 @@ unsigned long long* trace_buf = nullptr;  // RTN_TRACE device buffer
 constexpr int kMaxChunks = 8;                 // end-to-end pipeline depth
 constexpr long long kGraphMaxRows = 4096;     // latency mode: graph-captured steps up to this K
 constexpr long long kChunkMinRows = 1 << 17;  // chunk only batches this large
+
+// Latency mode: kernels access the pinned staging in place (RTN_ZEROCOPY=0 restores memcpy nodes).
+bool ZeroCopy() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTN_ZEROCOPY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int PaddedWidth(const std::vector<int>& sizes) {
   int w = 0;
@@ -797,11 +809,17 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
         CUDA_CHECK(cudaStreamSynchronize(c->stream));
         cudaGraph_t graph;
         CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        CUDA_CHECK(cudaMemcpyAsync(c->d_z, c->h_z, zr * K, cudaMemcpyHostToDevice, c->stream));
-        Enqueue(c, c->d_z, K, order, c->d_f, order >= 1 ? c->d_jac : nullptr, order == 2 ? c->d_hess : nullptr);
-        CUDA_CHECK(cudaMemcpyAsync(c->h_f, c->d_f, fr * K, cudaMemcpyDeviceToHost, c->stream));
-        if (order >= 1) CUDA_CHECK(cudaMemcpyAsync(c->h_jac, c->d_jac, jr * K, cudaMemcpyDeviceToHost, c->stream));
-        if (order == 2) CUDA_CHECK(cudaMemcpyAsync(c->h_hess, c->d_hess, hr * K, cudaMemcpyDeviceToHost, c->stream));
+        if (ZeroCopy()) {
+          // The kernel reads z from and writes f/J/H to the pinned staging
+          // directly (unified addressing): the graph is the kernel alone.
+          Enqueue(c, c->h_z, K, order, c->h_f, order >= 1 ? c->h_jac : nullptr, order == 2 ? c->h_hess : nullptr);
+        } else {
+          CUDA_CHECK(cudaMemcpyAsync(c->d_z, c->h_z, zr * K, cudaMemcpyHostToDevice, c->stream));
+          Enqueue(c, c->d_z, K, order, c->d_f, order >= 1 ? c->d_jac : nullptr, order == 2 ? c->d_hess : nullptr);
+          CUDA_CHECK(cudaMemcpyAsync(c->h_f, c->d_f, fr * K, cudaMemcpyDeviceToHost, c->stream));
+          if (order >= 1) CUDA_CHECK(cudaMemcpyAsync(c->h_jac, c->d_jac, jr * K, cudaMemcpyDeviceToHost, c->stream));
+          if (order == 2) CUDA_CHECK(cudaMemcpyAsync(c->h_hess, c->d_hess, hr * K, cudaMemcpyDeviceToHost, c->stream));
+        }
         CUDA_CHECK(cudaStreamEndCapture(c->stream, &graph));
         CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
         CUDA_CHECK(cudaGraphDestroy(graph));
@@ -1093,7 +1111,7 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
   b.first_bad = c->d_bad;
 
   auto enqueue_compute = [&](cudaStream_t s) {
-    CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
+    if (b.first_bad) CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
     if (cycle)  // PrepareNodes at z_k = [x_k; u_k], gathered from the iterate inside layer 0
       Enqueue(c, nullptr, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr, b.xs, b.us, N);
     CUDA_CHECK(rtn::LaunchQpBlocks(b, s));
@@ -1119,20 +1137,57 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
     const size_t o_j = jac ? eo : 0;
     eo += jac ? sj.n : 0;
     const size_t o_h = hess ? eo : 0;
+    const bool zc = c->latency_mode && K <= kGraphMaxRows && ZeroCopy();
+    if (zc) {
+      // Zero-copy: the kernels read the iterate from and write QpData to the
+      // pinned staging in place (unified addressing); errors come back as
+      // per-node status bytes, so the graph holds the two kernels only.
+      if (c->status_cap < K) {
+        cudaFreeHost(c->h_status);
+        c->h_status = nullptr;
+        c->status_cap = 0;
+        CUDA_CHECK(cudaMallocHost(&c->h_status, static_cast<size_t>(K)));
+        c->status_cap = K;
+      }
+      const double* hin = c->h_qin;
+      double* hout = c->h_qout;
+      b.xs = hin + o_xs;
+      b.us = hin + o_us;
+      b.rxs = hin + o_rxs;
+      b.rus = hin + o_rus;
+      if (!cycle) {
+        b.z0 = hin + o_z0;
+        b.fbar = hin + o_fb;
+        b.jac = hin + o_jac;
+        b.hess = order == 2 ? hin + o_hess : nullptr;
+      }
+      auto houtp = [hout](size_t off) { return off == SIZE_MAX ? nullptr : hout + off; };
+      b.a = houtp(o_a);
+      b.b = houtp(o_b);
+      b.phi = houtp(o_phi);
+      b.q = houtp(o_q);
+      b.r = houtp(o_r);
+      b.hx = houtp(o_hx);
+      b.hu = houtp(o_hu);
+      b.lb = houtp(o_lb);
+      b.ub = houtp(o_ub);
+      b.first_bad = nullptr;
+      b.status = c->h_status;
+    }
     auto body = [&](cudaStream_t st) {
-      CUDA_CHECK(cudaMemcpyAsync(din, c->h_qin, plan.in_total * sizeof(double), cudaMemcpyHostToDevice, st));
+      if (!zc) CUDA_CHECK(cudaMemcpyAsync(din, c->h_qin, plan.in_total * sizeof(double), cudaMemcpyHostToDevice, st));
       enqueue_compute(st);
-      if (plan.out_total)
+      if (plan.out_total && !zc)
         CUDA_CHECK(cudaMemcpyAsync(c->h_qout, dout, plan.out_total * sizeof(double), cudaMemcpyDeviceToHost, st));
       if (cycle && f) CUDA_CHECK(cudaMemcpyAsync(c->h_qout + o_f, c->d_f, sf.n * sizeof(double), cudaMemcpyDeviceToHost, st));
       if (cycle && jac)
         CUDA_CHECK(cudaMemcpyAsync(c->h_qout + o_j, c->d_jac, sj.n * sizeof(double), cudaMemcpyDeviceToHost, st));
       if (cycle && hess)
         CUDA_CHECK(cudaMemcpyAsync(c->h_qout + o_h, c->d_hess, sh.n * sizeof(double), cudaMemcpyDeviceToHost, st));
-      CUDA_CHECK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      if (!zc) CUDA_CHECK(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     };
     if (c->latency_mode && K <= kGraphMaxRows) {
-      const unsigned key = mask | (cycle ? 1u << 31 : 0);
+      const unsigned key = mask | (cycle ? 1u << 31 : 0) | (zc ? 1u << 30 : 0);
       const rtn_ctx::QpGraph* g = nullptr;
       for (const auto& e : c->qp_graphs)
         if (e.n_inst == n_inst && e.N == N && e.order == order && e.mask == key) g = &e;
@@ -1158,7 +1213,13 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
       body(s);
     }
     CUDA_CHECK(cudaStreamSynchronize(s));
-    if (*c->h_bad != rtn::kNoError) throw Error(RTN_ERUNTIME, QpErrorMessage(*c->h_bad, N, n_inst));
+    if (zc) {
+      for (long long i = 0; i < K; ++i)
+        if (c->h_status[i]) throw Error(RTN_ERUNTIME, QpErrorMessage((static_cast<unsigned long long>(i) << 8) |
+                                                                         c->h_status[i], N, n_inst));
+    } else if (*c->h_bad != rtn::kNoError) {
+      throw Error(RTN_ERUNTIME, QpErrorMessage(*c->h_bad, N, n_inst));
+    }
     for (const Slice& sl : plan.out) std::memcpy(sl.dst, c->h_qout + sl.off, sl.n * sizeof(double));
     if (cycle && f) std::memcpy(f, c->h_qout + o_f, sf.n * sizeof(double));
     if (cycle && jac) std::memcpy(jac, c->h_qout + o_j, sj.n * sizeof(double));

@@ -189,3 +189,29 @@ def test_empty_batch():
     got = qp.QpBuilder(_model(om)).build_qp(qp.QuadParams(), _cfg(3), xs[:0], us[:0], rx[:0], ru[:0],
                                              {"z0": z[:0], "f_bar": f[:0], "jac": j[:0]})
     assert got.a.shape == (0, 3, 13, 13)
+
+
+def test_latency_mode_errors_and_recovery():
+    """Latency mode (graph + zero-copy staging, per-node status bytes) reports
+    the reference's message for the lowest failing node and recovers."""
+    xs, us, rx, ru, z, f, j, h, om = _case(1, 20, seed=21)
+    p, cfg = qp.QuadParams(), _cfg(20)
+    b = qp.QpBuilder(_model(om), precision=_lib.RTN_BF16X3, latency_mode=1)
+    good = b.cycle_qp(p, cfg, xs, us, rx, ru)
+    bad = xs.copy()
+    bad[0, 11, 5] = 4.0
+    bad[0, 14, 3] = np.nan  # non-finite later; node 11's domain error is the one reported
+    for _ in range(2):  # first call runs outside the graph, the second replays it
+        with pytest.raises(RuntimeError, match=re.escape("build qp: node 11: quad dynamics: quaternion norm too far")):
+            b.cycle_qp(p, cfg, bad, us, rx, ru)
+    again = b.cycle_qp(p, cfg, xs, us, rx, ru)
+    for name in FIELDS:
+        assert np.array_equal(getattr(again, name), getattr(good, name)), name
+    ap = {"z0": z, "f_bar": f, "jac": j}
+    f2 = f.copy()
+    f2[3, 0] = np.nan
+    with pytest.raises(RuntimeError, match=re.escape("build qp: node 3: rk4: non-finite derivative at stage 1")):
+        b.build_qp(p, cfg, xs, us, rx, ru, {"z0": z, "f_bar": f2, "jac": j})
+    ref = _oracle_qp(p, cfg, xs, us, rx, ru, z, f, j, None)
+    got = b.build_qp(p, cfg, xs, us, rx, ru, ap)
+    assert _block_err(got.a, ref["a"]) < TOL
