@@ -26,6 +26,10 @@ cudaError_t LaunchPair3xTF32(const KParams& prm, const CUtensorMap& th, const CU
 cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
                              int grid, cudaStream_t st);
 
+// Latency kernel on 4-CTA clusters (rtn_quad.cuh): TF32, width 512, order <= 1,
+// one node per CTA side, grid = 4 x ceil(K / 2).
+cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
+
 // Order 2 (value + Jacobian + Hessian; n_in = 17): two pair-tiles per node.
 cudaError_t LaunchPairOrder2(int mode, const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp,
                              int grid, cudaStream_t st);

@@ -530,9 +530,17 @@ void LaunchP(const rtn::KParams& prm, int grid, cudaStream_t st) {
 //   latency   : pair kernel, P = 1 node per CTA (N = 48), one node per SM,
 //               deep weight pipeline — small batches (one MPC step, K = N);
 //   single    : one-CTA kernel (padded width 128, or forced).
-enum class Kern { kSingle, kPair, kLatency };
+enum class Kern { kSingle, kPair, kLatency, kQuad };
 Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
   const bool lat_ok = m->has_pair && m->n_in + 1 <= 24;
+  // quad: 4-CTA clusters, one tile of 2 nodes each (TF32, width 512; order-1 path only reaches here)
+  const bool quad_ok = lat_ok && m->pair_mode == rtn::kTF32 && m->pair_wp == 512 && K <= 2 * (num_sms / 4);
+  if (const char* e = std::getenv("RTN_KERNEL"))
+    if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
+  if (quad_ok && !std::getenv("RTN_KERNEL")) {
+    const char* q = std::getenv("RTN_QUAD");
+    if (!(q && q[0] == '0')) return Kern::kQuad;
+  }
   if (m->pair_mode != rtn::kTF32) {  // split precisions exist only on the pair kernel
     if (const char* e = std::getenv("RTN_KERNEL"))
       if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
@@ -601,6 +609,16 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     return;
   }
   const Kern kern = Choose(m, K, prm.P, c->num_sms);
+  if (kern == Kern::kQuad) {
+    prm.bh = m->d_bh_pair;
+    prm.P = 1;
+    prm.nt = ((1 + m->n_in + 7) / 8) * 8;
+    prm.num_tiles = (K + 1) / 2;
+    const cudaError_t e = rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, static_cast<int>(4 * prm.num_tiles), c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
+    c->launches += 1;
+    return;
+  }
   if (kern != Kern::kSingle) {
     prm.bh = m->d_bh_pair;
     const bool lat = kern == Kern::kLatency;

@@ -1,0 +1,302 @@
+// rtn_quad.cuh — latency kernel on 4-CTA clusters (two CTA pairs), TF32, order 1.
+//
+// Why: at one MPC step (K = N nodes) the pair kernel gives each 2-node
+// cluster the WHOLE weight stream; every SM pushes ~5.8 MB of 12x512 weights
+// through its shared-memory port twice (TMA write + MMA read), which sets the
+// per-step latency. Here a cluster of four CTAs holds the same two nodes:
+//   pair p = ranks {2p, 2p+1} computes 256-neuron block p of every hidden
+//   layer (M = 256 pair MMA, N = 2 x 24 rows), so each SM streams half the
+//   weights and runs one epilogue block per layer instead of two.
+// Activations: CTA c produces next-layer K-group c (neurons 128c..128c+127)
+// and its epilogue half h writes node h's rows into BOTH CTAs holding node h
+// (ranks h and h+2; one of them may be itself), i.e. an all-to-all over DSMEM.
+// Synchronisation (all mbarriers):
+//   full/empty[s]  per pair: TMA bytes on the pair leader, empty multicast to the pair
+//   act_ready[g]   at both leaders (ranks 0, 2): 8 warp arrivals from CTA g per layer
+//   in_free[g]     at all four CTAs: one commit from EACH pair's leader (count 2)
+//   tmem_full      the pair's own block accumulated (multicast to the pair)
+//   tmem_last      pair 0's output layer accumulated
+// Pair p walks the K-groups starting at its own (2p, 2p+1), so its first
+// act_ready wait also proves its TMEM block was drained by its epilogue.
+// One tile (2 nodes) per cluster: used for K <= 2 * (#SMs / 4).
+#pragma once
+
+#include <cuda.h>
+
+#include "rtn_kernel.cuh"
+#include "rtn_pair.cuh"
+
+namespace rtn {
+
+// 4 tf32 K-steps + multicast commit of `bar` to `mask` (+ `bar2` to `mask2` if non-zero).
+__device__ __forceinline__ void mma4_tf32_pair_commit_m(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                        uint32_t accumulate, uint32_t bar, uint32_t mask,
+                                                        uint32_t bar2, uint32_t mask2) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b16 m, m2;\n\t"
+      "cvt.u16.u32 m, %7;\n\tcvt.u16.u32 m2, %8;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a3, b3, %3, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], m;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], m2;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2), "r"(mask), "r"(mask2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mask(uint64_t* bar, uint32_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\t"
+      "cvt.u16.u32 m, %1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "r"(mask)
+      : "memory");
+}
+
+template <int NSTAGE, int NTC>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
+    rtn_quad_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
+                    const __grid_constant__ CUtensorMap tmap_l) {
+  constexpr int WP = 512, P = 1;
+  using C = PairCfg<WP, NSTAGE, P, NTC, kTF32, false>;
+  constexpr int NKC = C::kNKC, CPG = C::kCPG, NG = C::kNG;  // 16 chunks, 4 per group, 4 groups
+  static_assert(NG == 4 && NKC % NSTAGE == 0, "quad kernel: width 512, whole stage rings per layer");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* act_s = smem;
+  uint8_t* stage_s = smem + C::kStageOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NSTAGE;
+  uint64_t* act_ready = bars + 2 * NSTAGE;
+  uint64_t* in_free = act_ready + 4;
+  uint64_t* tmem_full = in_free + 4;
+  uint64_t* tmem_last = tmem_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kMiscOff);
+  float* zs = reinterpret_cast<float*>(smem + C::kZsOff);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pr = static_cast<int>(rank) >> 1;    // pair index = 256-neuron block
+  const int sub = static_cast<int>(rank) & 1;    // half of the pair's M
+  const bool leader = sub == 0;
+  const uint32_t pair_mask = 3u << (2 * pr);
+  const int n_in = prm.n_in, ntc = prm.nt;
+  const int n_mma_layers = prm.n_hidden - 1;
+  const long long node0 = static_cast<long long>(blockIdx.x >> 2) * 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int g = 0; g < 4; ++g) {
+      mbar_init(&act_ready[g], 8);  // one elected arrive per epilogue warp of CTA g
+      mbar_init(&in_free[g], 2);    // one commit from each pair
+      mbar_init(&tmem_full[g], 1);
+    }
+    mbar_init(tmem_last, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    prefetch_tmap(&tmap_h);
+    prefetch_tmap(&tmap_l);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 256);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== weight producer: this CTA's 128 rows of block pr ====
+    const uint64_t pol = l2_evict_last_policy();
+    uint32_t ph = 0;
+    for (int l = 0; l < n_mma_layers; ++l) {
+      const int y = l * WP + pr * 256 + sub * 128;
+#pragma unroll
+      for (int i = 0; i < NKC; ++i) {
+        const int c = (i + 2 * pr * CPG) % NKC, st = i % NSTAGE;  // rotated K order
+        mbar_wait(&empty[st], ph ^ 1);
+        if (leader) mbar_expect_tx_elect(&full[st], 2 * kStageBytes);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * C::kCK, y, &full[st], pol);
+        if (st == NSTAGE - 1) ph ^= 1;
+      }
+    }
+    if (pr == 0) {
+#pragma unroll
+      for (int i = 0; i < NKC; ++i) {
+        const int st = i % NSTAGE;
+        mbar_wait(&empty[st], ph ^ 1);
+        if (leader) mbar_expect_tx_elect(&full[st], 2 * kLastHalfBytes);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, i * C::kCK, sub * 8, &full[st], pol);
+        if (st == NSTAGE - 1) ph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== pair MMA issuer (pair leaders: ranks 0 and 2) ======
+    if (leader) {
+      const uint32_t idesc_h = idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_o = idesc_tf32(256, kMaxOut);
+      const uint64_t a0 = sw128_desc(smem_u32(stage_s));
+      const uint64_t b0 = sw128_desc(smem_u32(act_s));
+      constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4;
+      uint32_t ph = 0, ar = 0;
+      for (int l = 0; l < n_mma_layers; ++l) {
+#pragma unroll
+        for (int i = 0; i < NKC; ++i) {
+          const int c = (i + 2 * pr * CPG) % NKC, st = i % NSTAGE, g = c / CPG;
+          if (i == 0) {  // own groups first: inputs ready AND this pair's TMEM block drained
+            mbar_wait_cluster(&act_ready[2 * pr], ar & 1);
+            mbar_wait_cluster(&act_ready[2 * pr + 1], ar & 1);
+            tc_fence_after();
+          } else if ((i % CPG) == 0 && g != 2 * pr + 1) {
+            mbar_wait_cluster(&act_ready[g], ar & 1);
+            tc_fence_after();
+          }
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const bool last_of_group = (c % CPG) == CPG - 1;
+          mma4_tf32_pair_commit_m(tmem_base, a0 + st * kStageD, b0 + c * kChunkD, idesc_h, i != 0,
+                                  smem_u32(&empty[st]), pair_mask, last_of_group ? smem_u32(&in_free[g]) : 0u, 0xFu);
+          if (st == NSTAGE - 1) ph ^= 1;
+        }
+        mma_commit_mask(&tmem_full[0], pair_mask);
+        ++ar;
+      }
+      if (pr == 0) {  // output layer: D[row, o] = Σ_k X[row, k]·W_L'[o, k]; M = 2 x 128 rows, N = 16
+#pragma unroll
+        for (int i = 0; i < NKC; ++i) {
+          const int st = i % NSTAGE;
+          if ((i % CPG) == 0) {
+            mbar_wait_cluster(&act_ready[i / CPG], ar & 1);
+            tc_fence_after();
+          }
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          mma4_tf32_pair_commit_m(tmem_base, b0 + i * kChunkD, a0 + st * kStageD, idesc_o, i != 0,
+                                  smem_u32(&empty[st]), pair_mask, 0u, 0u);
+          if (st == NSTAGE - 1) ph ^= 1;
+        }
+        mma_commit_mask(tmem_last, pair_mask);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: 8 warps, half h = node h's rows ==========
+    const int half = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int tid_h = q * 32 + lane;
+    const int etid = threadIdx.x - 128;
+    const int act = prm.act;
+    const int rows_used = P * (1 + n_in);
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const int u = ((tid_h * 4) >> 4) & 7;
+    int swz[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) swz[i] = ((u ^ i) - u) * 16 + i * 128;
+    // node h lives in ranks h and h + 2
+    const uint32_t act_local = smem_u32(act_s);
+    const uint32_t dst0 = mapa(act_local, static_cast<uint32_t>(half));
+    const uint32_t dst1 = mapa(act_local, static_cast<uint32_t>(half + 2));
+    const uint32_t ready0 = mapa(smem_u32(&act_ready[rank]), 0), ready2 = mapa(smem_u32(&act_ready[rank]), 2);
+    const int grp = static_cast<int>(rank);  // K-group this CTA produces
+
+    auto store_side = [&](const float* v, int j) {
+      const uint32_t off = (j / C::kCK) * C::kChunkStride + (((j % C::kCK) * 4) >> 4 << 4) + ((j * 4) & 15);
+#pragma unroll
+      for (int i = 0; i < NTC; ++i) {
+        if ((i & ~7) >= ntc) continue;
+        const uint32_t a = off + (i >> 3) * 1024 + swz[i & 7];
+        const float h = to_tf32(v[i]);
+        st_cluster_f32(dst0 + a, h);
+        st_cluster_f32(dst1 + a, h);
+      }
+    };
+    auto publish = [&]() {
+      fence_proxy_async_cluster();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster(ready0);
+        mbar_arrive_cluster(ready2);
+      }
+    };
+    const long long node = node0 + half;
+    if (etid < 2 * n_in) {
+      const int p = etid / n_in, k = etid - p * n_in;
+      zs[etid] = node0 + p < prm.K ? static_cast<float>(load_z(prm, node0 + p, k)) : 0.0f;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // ---- layer 0 (CUDA cores): this CTA produces K-group `rank` for both nodes
+    {
+      const int j = grp * 128 + tid_h;
+      const float* w0r = prm.w0 + j * n_in;
+      float pre = __ldg(prm.b0 + j);
+      for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[half * n_in + k], pre);
+      float val, sp;
+      act_fwd(act, pre, val, sp);
+      float v[NTC];
+#pragma unroll
+      for (int i = 0; i < NTC; ++i) v[i] = i == 0 ? val : (i < rows_used ? sp * __ldg(w0r + (i - 1)) : 0.0f);
+      store_side(v, j);
+      publish();
+    }
+    // ---- hidden layers: one block per CTA per layer
+    for (int l = 0; l < n_mma_layers; ++l) {
+      const int j = pr * 256 + sub * 128 + tid_h;  // == grp * 128 + tid_h
+      const float bj = __ldg(prm.bh + l * WP + j);
+      mbar_wait_sleep(&tmem_full[0], l & 1);
+      tc_fence_after();
+      float v[NTC];
+#pragma unroll
+      for (int c0 = 0; c0 < NTC; c0 += 8)
+        if (c0 < ntc) tmem_ld8(tmem_base + lane_base + half * ntc + c0, v + c0);
+      tmem_ld_wait();
+      tc_fence_before();
+      float val, sp;
+      act_fwd(act, v[0] + bj, val, sp);
+      v[0] = val;
+#pragma unroll
+      for (int i = 1; i < NTC; ++i) v[i] = i < rows_used ? v[i] * sp : 0.0f;
+      mbar_wait_sleep(&in_free[grp], l & 1);  // both pairs consumed group grp of this layer's input
+      store_side(v, j);
+      publish();
+    }
+    // ---- output layer (pair 0): row r of this CTA's side in TMEM lane r, outputs in columns 0..15
+    if (pr == 0 && half == 0) {
+      mbar_wait_sleep(tmem_last, 0);
+      tc_fence_after();
+      float o[16];
+      tmem_ld16(tmem_base + lane_base, o);
+      tmem_ld_wait();
+      const int r = tid_h, n_out = prm.n_out;
+      const long long nd = node0 + sub;
+      if (nd < prm.K) {
+        if (r == 0) {
+          for (int oo = 0; oo < n_out; ++oo) prm.f[nd * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+        } else if (r < rows_used && prm.jac != nullptr) {
+          for (int oo = 0; oo < n_out; ++oo) prm.jac[(nd * n_out + oo) * n_in + (r - 1)] = static_cast<double>(o[oo]);
+        }
+      }
+      tc_fence_before();
+    }
+    (void)node;
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 256);
+  }
+}
+
+}  // namespace rtn

@@ -15,9 +15,10 @@ TF32_TOL = 1e-3
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["single", "pair", "latency"])
+@pytest.fixture(params=["single", "pair", "latency", "quad"])
 def kernel(request, monkeypatch):
-    """Every device kernel: single-CTA, CTA-pair throughput (P=4) and CTA-pair latency (P=1)."""
+    """Every device kernel: single-CTA, CTA-pair throughput (P=4), CTA-pair latency (P=1) and the
+    4-CTA-cluster latency kernel (width-512 TF32 models, K <= 2·(#SMs/4); others fall back)."""
     monkeypatch.setenv("RTN_KERNEL", request.param)
     return request.param
 
@@ -88,3 +89,20 @@ def test_batch_rows_equal_single_calls(kernel):
 
 def test_throughput_shape_cfg4_subset(kernel):
     _check([17] + [256] * 5 + [6], "silu", 4096)
+
+
+def test_quad_latency_kernel_ragged_and_bitwise(monkeypatch):
+    """4-CTA-cluster latency kernel (csrc/rtn_quad.cuh): odd K (a half-empty
+    cluster), the K limit (74 on 148 SMs), and rows of a batch bit-identical to
+    single-node calls."""
+    from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
+    monkeypatch.setenv("RTN_KERNEL", "quad")
+    for k in (1, 2, 3, 5, 73, 74):
+        _check([17, 512, 512, 512, 6], "silu", k)
+    om = OracleModel.random_net([17] + [512] * 4 + [6], "tanh", 29)
+    pm = to_product_model(om)
+    z = quad_nodes(8, 9)
+    full = mlp_batched_eval(pm, z, EvalOrder.JACOBIAN)
+    for i in (0, 4, 8):
+        one = mlp_batched_eval(pm, z[i:i + 1], EvalOrder.JACOBIAN)
+        assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
