@@ -243,3 +243,72 @@ def quad_dynamics(params_flat, x, u):
     if st != 0:
         raise OracleError(st, lib().oracle_blocks_last_error().decode())
     return dx, fx, fu
+
+
+# ---------------------------------------------------------------------------
+# Closed-loop trajectory check (closedloop_oracle.h): one rollout of the
+# quadrotor RTI loop; phase 1 (PrepareNodes) and optionally phases 1+2
+# (BuildQp blocks) come from Python callables, e.g. the device path.
+PREP_CB = C.CFUNCTYPE(C.c_int, _dp, C.c_int, C.c_int, _dp, _dp, _dp, C.c_void_p)
+BLOCKS_CB = C.CFUNCTYPE(C.c_int, _dp, _dp, _dp, _dp, C.c_int, *([_dp] * 9), C.c_void_p)
+
+
+def closed_loop(om, params_flat, cfg_flat, horizon, order, traj=(0, 5.0, 2.0, 20.0, 1.5, 3.0),
+                sim=(0.3, 0.3, 0.15, 0.005, 0.02, 1e-3, 100.0), duration=0.5, seed=7, per_step_noise=False,
+                prepare=None, blocks=None, has_qf=False):
+    """prepare(z K x 17, order) -> (f K x 6, jac K x 6 x 17, hess or None);
+    blocks(xs, us, rxs, rus) -> dict of QpData arrays (a, b, phi_res, q, r, hx_diag, hu_diag, du_lb, du_ub).
+    Returns dict(states steps x 13, commands steps x 4, ok steps, failed)."""
+    L = lib()
+    if not hasattr(L, "_cl_bound"):
+        L.oracle_closed_loop_last_error.restype = C.c_char_p
+        L.oracle_closed_loop.argtypes = [C.c_void_p, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_double,
+                                         C.c_ulonglong, PREP_CB, BLOCKS_CB, C.c_void_p, _dp, _dp,
+                                         C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L._cl_bound = True
+    errors = []
+
+    def _prep(zp, k, ordr, fp, jp, hp, _u):
+        try:
+            z = np.ctypeslib.as_array(zp, shape=(k, 17)).copy()
+            f, j, h = prepare(z, ordr)
+            np.ctypeslib.as_array(fp, shape=(k, 6))[:] = f
+            np.ctypeslib.as_array(jp, shape=(k, 6, 17))[:] = j
+            if ordr == 2:
+                np.ctypeslib.as_array(hp, shape=(k, 6, 17, 17))[:] = h
+            return 0
+        except Exception as e:  # noqa: BLE001 - reported after the rollout
+            errors.append(e)
+            return 1
+
+    def _blocks(xp, up, rxp, rup, n, *outs_u):
+        try:
+            outs = outs_u[:9]
+            arr = lambda p, s: np.ctypeslib.as_array(p, shape=s)
+            res = blocks(arr(xp, (n + 1, 13)).copy(), arr(up, (n, 4)).copy(), arr(rxp, (n + 1, 13)).copy(),
+                         arr(rup, (n, 4)).copy())
+            shapes = [(n, 13, 13), (n, 13, 4), (n, 13), (n + 1, 13), (n, 4), (n + 1, 13), (n, 4), (n, 4), (n, 4)]
+            names = ["a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag", "du_lb", "du_ub"]
+            for p, s, nm in zip(outs, shapes, names):
+                arr(p, s)[:] = np.reshape(res[nm], s)
+            return 0
+        except Exception as e:  # noqa: BLE001 - a BuildQp failure: the cycle reuses the last command
+            errors.append(e)
+            return 1
+
+    pcb = PREP_CB(_prep) if prepare is not None else C.cast(None, PREP_CB)
+    bcb = BLOCKS_CB(_blocks) if blocks is not None else C.cast(None, BLOCKS_CB)
+    max_steps = int(round(duration * sim[6])) + 2
+    states, commands = np.zeros((max_steps, 13)), np.zeros((max_steps, 4))
+    ok = np.zeros(max_steps, dtype=np.int32)
+    n_steps, failed = C.c_int(), C.c_int()
+    arrd = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    st = L.oracle_closed_loop(om.h if om is not None else None, _p(arrd(params_flat)), _p(arrd(cfg_flat)), horizon,
+                              int(has_qf), order, _p(arrd(traj)), _p(arrd(sim)), int(per_step_noise), duration, seed,
+                              pcb, bcb, None, _p(states), _p(commands), ok.ctypes.data_as(C.POINTER(C.c_int)),
+                              max_steps, C.byref(n_steps), C.byref(failed))
+    if st != 0:
+        raise OracleError(st, L.oracle_closed_loop_last_error().decode())
+    n = n_steps.value
+    return {"states": states[:n], "commands": commands[:n], "ok": ok[:n], "failed": bool(failed.value),
+            "callback_errors": errors}
