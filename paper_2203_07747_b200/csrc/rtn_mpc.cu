@@ -177,6 +177,7 @@ struct rtn_ctx {
     long long K;
     int order;
     cudaGraphExec_t exec;
+    const void* io[4];  // caller buffers of a direct (zero-copy) graph; null = staged
   };
   std::vector<Graph> graphs;
   // continuity-block builder: contiguous device in/out areas and pinned
@@ -814,14 +815,47 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
     if (K == 0) return;
     CUDA_CHECK(cudaSetDevice(m->device));
     const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in, hr = jr * m->n_in;
+    if (c->latency_mode && K <= kGraphMaxRows && ZeroCopy() && IsPinned(z) && IsPinned(f) &&
+        (order < 1 || IsPinned(jac)) && (order < 2 || IsPinned(hess))) {
+      // One MPC step on page-locked caller buffers: the kernel reads z and
+      // writes f/J/H in place (unified addressing); one graph per buffer set.
+      double* jj = order >= 1 ? jac : nullptr;
+      double* hh = order == 2 ? hess : nullptr;
+      cudaGraphExec_t exec = nullptr;
+      for (auto& g : c->graphs)
+        if (g.K == K && g.order == order && g.io[0] == z && g.io[1] == f && g.io[2] == jj && g.io[3] == hh)
+          exec = g.exec;
+      if (!exec) {
+        Enqueue(c, z, K, order, f, jj, hh);  // first launch outside capture
+        CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        cudaGraph_t graph;
+        CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        Enqueue(c, z, K, order, f, jj, hh);
+        CUDA_CHECK(cudaStreamEndCapture(c->stream, &graph));
+        CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+        CUDA_CHECK(cudaGraphDestroy(graph));
+        c->launches -= 1;  // the capture pass launched nothing
+        if (c->graphs.size() >= 64) {  // bounded cache of buffer sets
+          cudaGraphExecDestroy(c->graphs.front().exec);
+          c->graphs.erase(c->graphs.begin());
+        }
+        c->graphs.push_back({K, order, exec, {z, f, jj, hh}});
+        return;
+      }
+      c->launches += 1;
+      CUDA_CHECK(cudaGraphLaunch(exec, c->stream));
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      return;
+    }
     if (c->latency_mode && K <= kGraphMaxRows) {
-      // One MPC step: pinned staging + a CUDA graph of H2D → kernel → D2H,
-      // so the call costs one graph launch and one synchronisation.
+      // One MPC step: pinned staging + a CUDA graph of H2D → kernel → D2H
+      // (or the kernel alone on the staging, zero-copy), so the call costs
+      // one graph launch and one synchronisation.
       EnsureStaging(c);
       std::memcpy(c->h_z, z, zr * K);
       cudaGraphExec_t exec = nullptr;
       for (auto& g : c->graphs)
-        if (g.K == K && g.order == order) exec = g.exec;
+        if (g.K == K && g.order == order && g.io[0] == nullptr) exec = g.exec;
       if (!exec) {
         Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac, c->d_hess);  // first launch outside capture (attributes, checks)
         CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -841,7 +875,7 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
         CUDA_CHECK(cudaStreamEndCapture(c->stream, &graph));
         CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
         CUDA_CHECK(cudaGraphDestroy(graph));
-        c->graphs.push_back({K, order, exec});
+        c->graphs.push_back({K, order, exec, {nullptr, nullptr, nullptr, nullptr}});
       } else {
         c->launches += 1;  // the graph's kernel node
       }
