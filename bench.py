@@ -247,6 +247,44 @@ def precision_modes(torch, z, k, sizes, steps=2):
     return out
 
 
+def cfg4_bench(torch, tf32_peak, steps=5):
+    """BASELINE configs[3]: 4096 instances x N=20 x MLP 5x256 SiLU, throughput mode on
+    1 B200, TF32 and 3xTF32 (device-resident, CUDA events on the launching stream)."""
+    from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp, synth_quad_nodes
+    from paper_2203_07747_b200.errors import raise_for_status
+    L = _lib.lib()
+    sizes, k = [17] + [256] * 5 + [6], 4096 * 20
+    fl = flops_per_node(sizes, 1)
+    z = torch.from_numpy(synth_quad_nodes(2203, k)).cuda()
+    f = torch.empty((k, 6), dtype=torch.float64, device="cuda")
+    j = torch.empty((k, 6, 17), dtype=torch.float64, device="cuda")
+    out = {"workload": "cfg4: 4096 instances x N=20 nodes, MLP 5x256 SiLU (17->6), order 1", "nodes": k}
+    for name in ("tf32", "3xtf32"):
+        m = make_mlp(sizes, "silu", "full", 5256)
+        eng = m.engine(precision=_lib.PRECISIONS[name])
+        eng._ensure(k, 1)
+        st = torch.cuda.Stream()
+        raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
+        run = lambda: raise_for_status(L.rtn_prepare_device(eng.ctx_ptr, z.data_ptr(), k, 1, f.data_ptr(),
+                                                            j.data_ptr(), None))
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                run()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(steps):
+                run()
+            e1.record(st)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        ach = k * fl / (ms * 1e-3) / 1e12
+        out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": ach,
+                     "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
+                     "hardware_frac": (3 if name == "3xtf32" else 1) * ach / tf32_peak if tf32_peak else None}
+        eng.close()
+    return out
+
+
 def _quad_iterate(np, n_inst, n, seed):
     rng = np.random.default_rng(seed)
     xs = np.empty((n_inst, n + 1, 13))
@@ -523,6 +561,7 @@ def run_ours(args, rank, world, local_rank):
                    "cfg3_12x512_N20_bf16x3": latency(torch, SIZES, SEED, 20, steps=300, precision=2),
                    "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20),
                    "cfg1_2x64_N10": latency(torch, [17, 64, 64, 6], 2064, 10, steps=300)}
+        cfg4 = cfg4_bench(torch, tf32_peak) if world == 1 and not args.no_modes else None
         blocks = None
         if world == 1 and not args.no_blocks:
             blocks = blocks_bench(torch, peaks.get("hbm_gbs"))
@@ -554,6 +593,8 @@ def run_ours(args, rank, world, local_rank):
             result["precision_modes"] = modes
         if lat:
             result["latency"] = lat
+        if cfg4:
+            result["cfg4"] = cfg4
         if blocks:
             result["blocks"] = blocks
     if world > 1:

@@ -30,6 +30,11 @@ cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CU
 // one node per CTA side, grid = 4 x ceil(K / 2).
 cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 
+// Width-256 throughput kernel with two tiles in flight per CTA pair
+// (rtn_pingpong.cuh): TF32, order <= 1, P = 4 nodes per CTA side.
+cudaError_t LaunchPingPongTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
+                               cudaStream_t st);
+
 // Order 2 (value + Jacobian + Hessian; n_in = 17): two pair-tiles per node.
 cudaError_t LaunchPairOrder2(int mode, const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp,
                              int grid, cudaStream_t st);

@@ -631,7 +631,14 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
     cudaError_t e;
-    if (m->pair_mode == rtn::kTF32) e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+    const char* pp = std::getenv("RTN_PINGPONG");
+    if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && prm.P == 4 && !(pp && pp[0] == '0')) {
+      // width 256: two tiles in flight per CTA pair (rtn_pingpong.cuh)
+      const long long tile_pairs = (prm.num_tiles + 1) / 2;
+      const int g2 = 2 * static_cast<int>(std::min<long long>(tile_pairs, c->num_sms / 2));
+      e = rtn::LaunchPingPongTF32(prm, m->tmap_h, m->tmap_l, g2, c->stream);
+    } else if (m->pair_mode == rtn::kTF32)
+      e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
     else if (m->pair_mode == rtn::k3xTF32) e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
     else e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));

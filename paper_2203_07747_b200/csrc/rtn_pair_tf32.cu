@@ -1,5 +1,6 @@
 // Pair-kernel instantiations, TF32 mode (one kind::tf32 pass).
 #include "rtn_pair_launch.cuh"
+#include "rtn_pingpong.cuh"
 #include "rtn_quad.cuh"
 
 namespace rtn {
@@ -31,6 +32,20 @@ cudaError_t LaunchPairTF32(const KParams& prm, const CUtensorMap& th, const CUte
 cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
   using Cfg = PairCfg<512, 8, 1, 24, kTF32, false>;
   auto kern = rtn_quad_kernel<8, 24>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
+  return cudaGetLastError();
+}
+
+cudaError_t LaunchPingPongTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
+                               cudaStream_t st) {
+  using Cfg = PingCfg<4, 4, 80>;
+  auto kern = rtn_pingpong_kernel<4, 4, 80>;
   static bool attr_set = false;
   if (!attr_set) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
