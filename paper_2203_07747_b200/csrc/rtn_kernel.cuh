@@ -76,6 +76,21 @@ struct KParams {
   int zN;
 };
 
+// Layer-0 weight row of neuron j in registers (n_in <= kMaxIn0 for every tile shape).
+constexpr int kMaxIn0 = 24;
+__device__ __forceinline__ void load_w0_row(const float* w0r, int n_in, float (&w)[kMaxIn0]) {
+#pragma unroll
+  for (int k = 0; k < kMaxIn0; ++k) w[k] = k < n_in ? __ldg(w0r + k) : 0.0f;
+}
+// pre = b + Σ_k W0'[j,k]·z[k], ascending k (same rounding as the loop it replaces).
+__device__ __forceinline__ float layer0_pre(float b, const float (&w)[kMaxIn0], const float* z, int n_in) {
+  float pre = b;
+#pragma unroll
+  for (int k = 0; k < kMaxIn0; ++k)
+    if (k < n_in) pre = fmaf(w[k], z[k], pre);
+  return pre;
+}
+
 // Element k of node row `node` of the MLP input.
 __device__ __forceinline__ double load_z(const KParams& prm, long long node, int k) {
   if (prm.zx == nullptr) return prm.z[node * prm.n_in + k];

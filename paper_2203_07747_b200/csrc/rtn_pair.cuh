@@ -526,20 +526,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---- layer 0 (CUDA cores): this CTA owns K-groups g ≡ rank (mod 2); half h writes side h
       for (int g = static_cast<int>(rank); g < NG; g += 2) {
         const int j = g * 128 + tid_h;
-        const float* w0r = prm.w0 + j * n_in;
+        float w0[kMaxIn0];
+        load_w0_row(prm.w0 + j * n_in, n_in, w0);
         const float bj = __ldg(prm.b0 + j);
         float val[P], sp[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          float pre = bj;
-          for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[(half * P + p) * n_in + k], pre);
-          act_fwd(act, pre, val[p], sp[p]);
-        }
+        for (int p = 0; p < P; ++p) act_fwd(act, layer0_pre(bj, w0, zs + (half * P + p) * n_in, n_in), val[p], sp[p]);
         float v[NTC];
 #pragma unroll
         for (int i = 0; i < NTC; ++i) {
           if (i < P) v[i] = val[i];
-          else v[i] = i < rows_used ? sp[i % P] * __ldg(w0r + (i - P) / P) : 0.0f;
+          else v[i] = i < rows_used ? sp[i % P] * w0[((i - P) / P) % kMaxIn0] : 0.0f;
         }
         store_side(v, j);
         publish(g);

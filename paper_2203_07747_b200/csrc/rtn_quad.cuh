@@ -239,14 +239,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     // ---- layer 0 (CUDA cores): this CTA produces K-group `rank` for both nodes
     {
       const int j = grp * 128 + tid_h;
-      const float* w0r = prm.w0 + j * n_in;
-      float pre = __ldg(prm.b0 + j);
-      for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[half * n_in + k], pre);
+      float w0[kMaxIn0];
+      load_w0_row(prm.w0 + j * n_in, n_in, w0);
       float val, sp;
-      act_fwd(act, pre, val, sp);
+      act_fwd(act, layer0_pre(__ldg(prm.b0 + j), w0, zs + half * n_in, n_in), val, sp);
       float v[NTC];
 #pragma unroll
-      for (int i = 0; i < NTC; ++i) v[i] = i == 0 ? val : (i < rows_used ? sp * __ldg(w0r + (i - 1)) : 0.0f);
+      for (int i = 0; i < NTC; ++i) v[i] = i == 0 ? val : (i < rows_used ? sp * w0[(i - 1) % kMaxIn0] : 0.0f);
       store_side(v, j);
       publish();
     }
