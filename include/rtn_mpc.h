@@ -115,7 +115,8 @@ const char* rtn_last_error(void);
  *       -- /root/reference/proj/include/resmpc/sqp_rti.hpp:56-59
  *          /root/reference/proj/src/sqp_rti.cpp:59-155
  * for the quadrotor plant (MakeQuadrotorPlant, proj/src/plant.cpp:34-85) with
- * the 'full' residual variant (z = [x; u], 17 -> 6), in rtn mode, batched over
+ * any residual variant (rtn_variant; the features and their Jacobian are
+ * re-evaluated at every RK4 stage), in rtn mode, batched over
  * n_inst independent MPC instances of horizon N. All arithmetic is fp64.
  * Per node: RK4 sensitivities of f_F + embed·EvalTaylor (integrator.cpp:41-89).
  * Errors: ConfigError -> RTN_ECONFIG (same messages as QuadParams::Validate,
@@ -132,6 +133,14 @@ typedef struct { /* resmpc::QuadParams, proj/include/resmpc/dynamics.hpp:50-62 *
   double rotor_sign[4];
 } rtn_quad_params;
 
+/* Residual variant of the quadrotor plant (ResidualVariant, dynamics.hpp:95-131;
+ * MakeQuadrotorPlant, plant.cpp:34-85): the network's features z and outputs.
+ *   FULL   z = [x; u]                    17 -> 6 (v̇, ω̇ rows)
+ *   A      z = v_B = R(q)ᵀ v_W            3 -> 3 (v̇ rows)
+ *   AU     z = [v_B; u]                   7 -> 3
+ *   GROUND z = [x; u; z_WB·1 − patch]    26 -> 3 (patch: per-node 3x3 height map aux) */
+typedef enum { RTN_VARIANT_FULL = 0, RTN_VARIANT_A = 1, RTN_VARIANT_AU = 2, RTN_VARIANT_GROUND = 3 } rtn_variant;
+
 typedef struct { /* resmpc::OcpConfig at quadrotor dims, sqp_rti.hpp:22-34 */
   int horizon; /* N */
   double dt;
@@ -142,6 +151,7 @@ typedef struct { /* resmpc::OcpConfig at quadrotor dims, sqp_rti.hpp:22-34 */
   double u_min[4];
   double u_max[4];
   int taylor_order; /* 1 or 2 */
+  int variant;      /* rtn_variant (0 = FULL) */
 } rtn_ocp_config;
 
 typedef struct { /* Iterate + ReferenceWindow, row-major, instance-major */
@@ -149,13 +159,14 @@ typedef struct { /* Iterate + ReferenceWindow, row-major, instance-major */
   const double* us;     /* n_inst x N x 4 */
   const double* ref_xs; /* n_inst x (N+1) x 13 */
   const double* ref_us; /* n_inst x N x 4 */
+  const double* aux;    /* n_inst x N x 9 height patches (Plant::NodeAux, row-major), GROUND only */
 } rtn_iterate;
 
-typedef struct { /* one TaylorApprox per node, K = n_inst*N rows (taylor.hpp:13-24) */
-  const double* z0;    /* K x 17 */
-  const double* f_bar; /* K x 6 */
-  const double* jac;   /* K x 6 x 17 */
-  const double* hess;  /* K x 6 x 17 x 17, taylor_order 2 only (else NULL) */
+typedef struct { /* one TaylorApprox per node, K = n_inst*N rows (taylor.hpp:13-24); n_f/n_r per variant */
+  const double* z0;    /* K x n_f */
+  const double* f_bar; /* K x n_r */
+  const double* jac;   /* K x n_r x n_f */
+  const double* hess;  /* K x n_r x n_f x n_f, taylor_order 2 only (else NULL) */
 } rtn_approx;
 
 typedef struct { /* QpData (proj/include/resmpc/qp.hpp:13-28); any pointer may be NULL = not wanted */
@@ -183,8 +194,9 @@ rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_o
                                rtn_qp_blocks* d_out);
 
 /* Phases 1+2 of RtiController::Cycle fused on the device (sqp_rti.cpp:219-231):
- * features z_k = [x_k; u_k] -> PrepareNodes(order = cfg->taylor_order) -> BuildQp.
- * The context's model must be 17 -> 6. The approximations are returned too
+ * features z_k = features(x_k, u_k, aux_k) (the MLP's layer 0 gathers them from
+ * the iterate) -> PrepareNodes(order = cfg->taylor_order) -> BuildQp. The
+ * context's model must be n_f -> n_r of cfg->variant. The approximations are returned too
  * if f/jac/hess are non-NULL. Counts one batched call of K points. */
 rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
                         const rtn_iterate* it, rtn_qp_blocks* out, double* f, double* jac, double* hess);

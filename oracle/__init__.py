@@ -55,7 +55,7 @@ def lib() -> C.CDLL:
         L.oracle_random_vector.restype = None
         L.oracle_blocks_last_error.restype = C.c_char_p
         L.oracle_build_qp_quad.argtypes = ([_dp, _dp, C.c_int, C.c_int, C.c_int, C.c_longlong] + [_dp] * 8 +
-                                           [_dp] * 9 + [C.POINTER(C.c_ulonglong)])
+                                           [_dp] * 9 + [C.POINTER(C.c_ulonglong), C.c_int, _dp])
         L.oracle_quad_dynamics.argtypes = [_dp] * 6
         _lib = L
     return _lib
@@ -208,18 +208,25 @@ def to_product_model(om: OracleModel):
 # ---------------------------------------------------------------------------
 # Continuity-block builder oracle (blocks_oracle.h): BuildQp for the quadrotor
 # 'full' plant, batched over instances (instance-major rows).
-def build_qp_quad(params_flat, cfg_flat, horizon, has_qf, order, xs, us, ref_xs, ref_us, z0, f_bar, jac, hess=None):
+VARIANTS = {"a": (0, 3, 3), "a_u": (1, 7, 3), "full": (2, 17, 6), "ground": (3, 26, 3)}  # code, n_f, n_r
+
+
+def build_qp_quad(params_flat, cfg_flat, horizon, has_qf, order, xs, us, ref_xs, ref_us, z0, f_bar, jac, hess=None,
+                  variant="full", aux=None):
     """Returns dict of QpData arrays + 'f_evals'. Raises OracleError with the
-    reference's message ("build qp: node k: ...") on failure."""
+    reference's message ("build qp: node k: ...") on failure. variant: a, a_u,
+    full, ground (aux: n_inst x N x 9 height patches)."""
     n = int(horizon)
+    code, nf, nr = VARIANTS[variant]
     xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, n + 1, 13)
     n_inst = xs.shape[0]
     k = n_inst * n
     cast = lambda a, s: np.ascontiguousarray(a, dtype=np.float64).reshape(s)
     ins = [cast(params_flat, (11,)), cast(cfg_flat, (39,))]
     arrs = [xs, cast(us, (n_inst, n, 4)), cast(ref_xs, (n_inst, n + 1, 13)), cast(ref_us, (n_inst, n, 4)),
-            cast(z0, (k, 17)), cast(f_bar, (k, 6)), cast(jac, (k, 6, 17)),
-            cast(hess, (k, 6, 17, 17)) if order == 2 else None]
+            cast(z0, (k, nf)), cast(f_bar, (k, nr)), cast(jac, (k, nr, nf)),
+            cast(hess, (k, nr, nf, nf)) if order == 2 else None]
+    aux_a = cast(aux, (k, 9)) if variant == "ground" else None
     out = {"a": np.empty((n_inst, n, 13, 13)), "b": np.empty((n_inst, n, 13, 4)), "phi_res": np.empty((n_inst, n, 13)),
            "q": np.empty((n_inst, n + 1, 13)), "r": np.empty((n_inst, n, 4)), "hx_diag": np.empty((n_inst, n + 1, 13)),
            "hu_diag": np.empty((n_inst, n, 4)), "du_lb": np.empty((n_inst, n, 4)), "du_ub": np.empty((n_inst, n, 4))}
@@ -227,7 +234,7 @@ def build_qp_quad(params_flat, cfg_flat, horizon, has_qf, order, xs, us, ref_xs,
     st = lib().oracle_build_qp_quad(_p(ins[0]), _p(ins[1]), n, int(has_qf), int(order), n_inst,
                                     *[_p(a) for a in arrs], *[_p(out[k_]) for k_ in
                                                               ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag",
-                                                               "du_lb", "du_ub")], fe)
+                                                               "du_lb", "du_ub")], fe, code, _p(aux_a))
     if st != 0:
         raise OracleError(st, lib().oracle_blocks_last_error().decode())
     out["f_evals"] = (fe[0], fe[1])

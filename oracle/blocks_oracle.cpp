@@ -307,7 +307,7 @@ Plant MakeDoubleIntegratorPlant() {
   };
   p.feature_dim = 3;
   p.residual_dim = 2;
-  p.features = [](const Vec& x, const Vec& u) { return Vec{x[0], x[1], u[0]}; };
+  p.features = [](const Vec& x, const Vec& u, const Vec&) { return Vec{x[0], x[1], u[0]}; };
   p.features_jac = [](const Vec&, const Vec&) { return Identity(3); };
   p.embed = Identity(2);
   return p;
@@ -315,8 +315,8 @@ Plant MakeDoubleIntegratorPlant() {
 
 Plant MakeQuadrotorPlant(const QuadParams& params, const std::string& variant) {
   params.Validate();
-  if (variant != "a" && variant != "a_u" && variant != "full")
-    throw ConfigError("quadrotor plant: oracle supports variants a, a_u, full");
+  if (variant != "a" && variant != "a_u" && variant != "full" && variant != "ground")
+    throw ConfigError("unknown residual variant '" + variant + "' (expected a, a_u, full, ground)");
   Plant p;
   p.name = "quadrotor";
   p.nx = kQuadNx;
@@ -325,14 +325,18 @@ Plant MakeQuadrotorPlant(const QuadParams& params, const std::string& variant) {
   p.f = [params](const Vec& x, const Vec& u) { return QuadNominalDynamics(x, u, params); };
   p.df = [params](const Vec& x, const Vec& u, Mat& fx, Mat& fu) { QuadNominalJacobians(x, u, params, fx, fu); };
   p.variant_tag = variant;
-  const bool full = variant == "full", au = variant == "a_u";
-  p.feature_dim = full ? 17 : (au ? 7 : 3);
+  const bool full = variant == "full", au = variant == "a_u", ground = variant == "ground";
+  p.feature_dim = full ? 17 : (au ? 7 : (ground ? 26 : 3));  // dynamics.cpp:110-118
   p.residual_dim = full ? 6 : 3;
-  // dynamics.cpp:125-152 (ResidualInput) and :154-180 (ResidualInputJacobian)
-  p.features = [full, au](const Vec& x, const Vec& u) {
-    if (full) {
+  // dynamics.cpp:125-152 (ResidualInput), plant.cpp:60-73 (ground: x, u, z_WB·1 − patch)
+  p.features = [full, au, ground](const Vec& x, const Vec& u, const Vec& aux) {
+    if (full || ground) {
       Vec z(x);
       z.insert(z.end(), u.begin(), u.end());
+      if (ground) {
+        if (aux.size() != 9) throw InputDomainError("quadrotor plant: ground features need a 9-entry patch aux");
+        for (int i = 0; i < 9; ++i) z.push_back(x[2] - aux[i]);
+      }
       return z;
     }
     Vec z(3);
@@ -341,9 +345,15 @@ Plant MakeQuadrotorPlant(const QuadParams& params, const std::string& variant) {
     return z;
   };
   const int nf = p.feature_dim;
-  p.features_jac = [full, au, nf](const Vec& x, const Vec&) {
+  // dynamics.cpp:154-180 (ResidualInputJacobian)
+  p.features_jac = [full, au, ground, nf](const Vec& x, const Vec&) {
     Mat jz(nf, kQuadNx + kQuadNu);
     if (full) return Identity(17);
+    if (ground) {
+      for (int i = 0; i < 17; ++i) jz(i, i) = 1.0;
+      for (int i = 17; i < 26; ++i) jz(i, 2) = 1.0;
+      return jz;
+    }
     const double* q = &x[kQuatRow];
     const double* v = &x[kVelRow];
     double dr[4][9], r[9];
@@ -386,7 +396,8 @@ void OcpConfig::Validate(int nx, int nu) const {
 
 QpData BuildQp(const Plant& plant, const OcpConfig& cfg, const std::vector<Vec>& xs, const std::vector<Vec>& us,
                const std::vector<Vec>& ref_xs, const std::vector<Vec>& ref_us,
-               const std::vector<TaylorApprox>* approxes, const NaiveNet* naive, FevalCounter* f_counters) {
+               const std::vector<TaylorApprox>* approxes, const NaiveNet* naive, FevalCounter* f_counters,
+               const std::vector<Vec>* node_aux) {
   cfg.Validate(plant.nx, plant.nu);
   const int n = cfg.horizon;
   if (static_cast<int>(xs.size()) != n + 1 || static_cast<int>(us.size()) != n)
@@ -404,6 +415,7 @@ QpData BuildQp(const Plant& plant, const OcpConfig& cfg, const std::vector<Vec>&
   for (int k = 0; k < n; ++k) {
     DynFn fk = plant.f;
     DynJacFn dfk = plant.df;
+    const Vec aux = node_aux != nullptr ? (*node_aux)[k] : Vec();  // plant.NodeAux(xs[k]) (sqp_rti.cpp:91)
     if (approxes != nullptr || naive != nullptr) {
       const TaylorApprox* ap = approxes ? &(*approxes)[k] : nullptr;
       // residual value r(z) and Jacobian jn(z) (nr x nf) at feature vector z
@@ -421,9 +433,9 @@ QpData BuildQp(const Plant& plant, const OcpConfig& cfg, const std::vector<Vec>&
                            ap->hess.empty() ? nullptr : ap->hess.data(), z.data(), j.data());
         return j;
       };
-      fk = [&plant, rval, nx, nr](const Vec& x, const Vec& u) {
+      fk = [&plant, rval, nx, nr, aux](const Vec& x, const Vec& u) {
         Vec f = plant.f(x, u);
-        const Vec r = rval(plant.features(x, u));
+        const Vec r = rval(plant.features(x, u, aux));
         for (int i = 0; i < nx; ++i) {
           double s = 0.0;
           for (int c = 0; c < nr; ++c) s += plant.embed(i, c) * r[c];
@@ -431,9 +443,9 @@ QpData BuildQp(const Plant& plant, const OcpConfig& cfg, const std::vector<Vec>&
         }
         return f;
       };
-      dfk = [&plant, rjac, nx, nu, nf, nr](const Vec& x, const Vec& u, Mat& fx, Mat& fu) {
+      dfk = [&plant, rjac, nx, nu, nf, nr, aux](const Vec& x, const Vec& u, Mat& fx, Mat& fu) {
         plant.df(x, u, fx, fu);
-        const Vec jn = rjac(plant.features(x, u));
+        const Vec jn = rjac(plant.features(x, u, aux));
         const Mat jz = plant.features_jac(x, u);
         Mat chain(nx, nf);  // embed * jn
         for (int i = 0; i < nx; ++i)
@@ -521,15 +533,19 @@ static oracle::QuadParams ParamsFrom(const double* p) {
   return q;
 }
 
+// variant: 0 a, 1 a_u, 2 full, 3 ground (aux: n_inst x N x 9 height patches, ground only)
 int oracle_build_qp_quad(const double* params, const double* cfgv, int horizon, int has_qf, int order,
                          long long n_inst, const double* xs, const double* us, const double* rxs,
                          const double* rus, const double* z0, const double* fbar, const double* jac,
                          const double* hess, double* a, double* b, double* phi, double* q, double* r,
-                         double* hx, double* hu, double* lb, double* ub, unsigned long long* fevals) {
+                         double* hx, double* hu, double* lb, double* ub, unsigned long long* fevals, int variant,
+                         const double* aux) {
   using namespace oracle;
   try {
     const QuadParams qp = ParamsFrom(params);
-    const Plant plant = MakeQuadrotorPlant(qp, "full");
+    static const char* kVariants[4] = {"a", "a_u", "full", "ground"};
+    if (variant < 0 || variant > 3) throw ConfigError("unknown residual variant");
+    const Plant plant = MakeQuadrotorPlant(qp, kVariants[variant]);
     OcpConfig cfg;
     cfg.horizon = horizon;
     cfg.dt = cfgv[0];
@@ -539,7 +555,7 @@ int oracle_build_qp_quad(const double* params, const double* cfgv, int horizon, 
     cfg.u_min.assign(cfgv + 31, cfgv + 35);
     cfg.u_max.assign(cfgv + 35, cfgv + 39);
     cfg.taylor_order = order;
-    const int n = horizon, nx = kQuadNx, nu = kQuadNu, nf = 17, nr = 6;
+    const int n = horizon, nx = kQuadNx, nu = kQuadNu, nf = plant.feature_dim, nr = plant.residual_dim;
     FevalCounter fc;
     for (long long i = 0; i < n_inst; ++i) {
       std::vector<Vec> vx, vu, vrx, vru;
@@ -561,9 +577,12 @@ int oracle_build_qp_quad(const double* params, const double* cfgv, int horizon, 
         ap[k].jac.assign(jac + row * nr * nf, jac + (row + 1) * nr * nf);
         if (order == 2) ap[k].hess.assign(hess + row * nr * nf * nf, hess + (row + 1) * nr * nf * nf);
       }
+      std::vector<Vec> vaux;
+      if (variant == 3)
+        for (int k = 0; k < n; ++k) vaux.emplace_back(aux + (i * n + k) * 9, aux + (i * n + k + 1) * 9);
       QpData d;
       try {
-        d = BuildQp(plant, cfg, vx, vu, vrx, vru, &ap, nullptr, &fc);
+        d = BuildQp(plant, cfg, vx, vu, vrx, vru, &ap, nullptr, &fc, variant == 3 ? &vaux : nullptr);
       } catch (const ConfigError&) {
         throw;
       } catch (const std::exception& e) {

@@ -73,7 +73,7 @@ SensitivityResult Rk4Sensitivities(const DynFn& f, const DynJacFn& df, const Vec
                                    FevalCounter* counter = nullptr);  // integrator.cpp:41-89
 
 // ---- plant ------------------------------------------------------------------
-struct Plant {  // plant.hpp:19-39 (no height map: the ground variant is out of scope)
+struct Plant {  // plant.hpp:19-39 (the ground variant's height-map patch arrives as per-node aux)
   std::string name;
   int nx = 0, nu = 0;
   DynFn f;
@@ -81,11 +81,12 @@ struct Plant {  // plant.hpp:19-39 (no height map: the ground variant is out of 
   int quat_row = -1;
   std::string variant_tag = "full";
   int feature_dim = 0, residual_dim = 0;
-  std::function<Vec(const Vec&, const Vec&)> features;      // (x, u) -> z
+  std::function<Vec(const Vec&, const Vec&, const Vec&)> features;  // (x, u, aux) -> z (plant.hpp:33-36)
   std::function<Mat(const Vec&, const Vec&)> features_jac;  // feature_dim x (nx+nu)
   Mat embed;                                                // nx x residual_dim
 };
 Plant MakeDoubleIntegratorPlant();                                            // plant.cpp:7-32
+// variants a, a_u, full, ground (ground: aux = the node's 3x3 height patch, row-major)
 Plant MakeQuadrotorPlant(const QuadParams& p, const std::string& variant);    // plant.cpp:34-85
 
 // ---- sqp_rti ----------------------------------------------------------------
@@ -108,10 +109,12 @@ struct NaiveNet {
   std::function<Vec(const Vec&)> jacobian;  // out x in, row-major
 };
 // sqp_rti.cpp:59-150. approxes: one TaylorApprox per node (rtn mode), or
-// naive != nullptr, or neither (nominal model only).
+// naive != nullptr, or neither (nominal model only). node_aux: per-node
+// residual aux (Plant::NodeAux, frozen at the expansion point; ground patch).
 QpData BuildQp(const Plant& plant, const OcpConfig& cfg, const std::vector<Vec>& xs,
                const std::vector<Vec>& us, const std::vector<Vec>& ref_xs,
                const std::vector<Vec>& ref_us, const std::vector<TaylorApprox>* approxes,
-               const NaiveNet* naive, FevalCounter* f_counters = nullptr);
+               const NaiveNet* naive, FevalCounter* f_counters = nullptr,
+               const std::vector<Vec>* node_aux = nullptr);
 
 }  // namespace oracle

@@ -380,7 +380,7 @@ Vec RtiController::Cycle(const Vec& x_measured, const std::vector<Vec>& rxs, con
   } else {
     Vec z;
     for (int k = 0; k < n; ++k) {
-      const Vec f = plant_.features(xs_[k], us_[k]);
+      const Vec f = plant_.features(xs_[k], us_[k], Vec());
       z.insert(z.end(), f.begin(), f.end());
     }
     const std::vector<TaylorApprox> approxes = prepare_(z, n, cfg_.taylor_order);  // phase 1 propagates

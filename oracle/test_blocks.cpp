@@ -430,7 +430,7 @@ std::vector<TaylorApprox> Prepare(const Plant& plant, const MlpModel& m, const s
   const int n = static_cast<int>(us.size());
   Vec z;
   for (int k = 0; k < n; ++k) {
-    const Vec f = plant.features(xs[k], us[k]);
+    const Vec f = plant.features(xs[k], us[k], Vec());
     z.insert(z.end(), f.begin(), f.end());
   }
   return PrepareNodes(m, z.data(), n, plant.feature_dim, order);
@@ -528,6 +528,58 @@ void BuildQpTests() {
       CHECK(worst < 1e-6);
     }
   }
+  // Every residual variant (dynamics.cpp:95-211, plant.cpp:60-85): rtn == naive for a
+  // linear residual (the Taylor model of a linear map is exact in feature space), and
+  // FD of the assembled blocks for a nonlinear one (orders 1 and 2).
+  for (const char* var : {"a", "a_u", "full", "ground"}) {
+    const Plant plant = MakeQuadrotorPlant(kParams, var);
+    const int nf = plant.feature_dim, nr = plant.residual_dim;
+    std::vector<Vec> aux;
+    for (int k = 0; k < qc.horizon; ++k) aux.push_back(RandomVector(rng, 9, -0.2, 0.3));
+    const std::vector<Vec>* auxp = std::string(var) == "ground" ? &aux : nullptr;
+    auto prepare = [&](const MlpModel& m, int order) {
+      Vec z;
+      for (int k = 0; k < qc.horizon; ++k) {
+        const Vec f = plant.features(xs[k], us[k], auxp ? aux[k] : Vec());
+        z.insert(z.end(), f.begin(), f.end());
+      }
+      return PrepareNodes(m, z.data(), qc.horizon, nf, order);
+    };
+    {
+      MlpModel lin = RandomNet(rng, {nf, nr});
+      const auto ap = prepare(lin, 1);
+      const NaiveNet nv = Naive(lin);
+      qc.taylor_order = 1;
+      const QpData a = BuildQp(plant, qc, xs, us, rx, ru, &ap, nullptr, nullptr, auxp);
+      const QpData b = BuildQp(plant, qc, xs, us, rx, ru, nullptr, &nv, nullptr, auxp);
+      CHECK(MaxQpDiff(a, b) < 1e-10);
+    }
+    MlpModel net = RandomNet(rng, {nf, 24, 24, nr}, Activation::kSilu);
+    for (int order = 1; order <= 2; ++order) {
+      const auto ap = prepare(net, order);
+      qc.taylor_order = order;
+      const QpData a = BuildQp(plant, qc, xs, us, rx, ru, &ap, nullptr, nullptr, auxp);
+      double worst = 0.0;
+      for (int k = 0; k < qc.horizon; ++k) {
+        const TaylorApprox* p = &ap[k];
+        const Vec ax = auxp ? aux[k] : Vec();
+        const DynFn fk = [&](const Vec& x, const Vec& u) {
+          Vec f = QuadNominalDynamics(x, u, kParams);
+          const Vec z = plant.features(x, u, ax);
+          Vec y(nr);
+          EvalTaylor(nf, nr, p->order, p->z0.data(), p->f_bar.data(), p->jac.data(),
+                     p->hess.empty() ? nullptr : p->hess.data(), z.data(), y.data());
+          for (int i = 0; i < nr; ++i) f[7 + i] += y[i];
+          return f;
+        };
+        const Vec fda = FdJacobian([&](const Vec& x) { return Rk4Step(fk, x, us[k], qc.dt, -1); }, xs[k]);
+        const Vec fdb = FdJacobian([&](const Vec& u) { return Rk4Step(fk, xs[k], u, qc.dt, -1); }, us[k]);
+        worst = std::max({worst, RelError(a.a[k].v, fda), RelError(a.b[k].v, fdb)});
+      }
+      CHECK(worst < 1e-6);
+    }
+  }
+  qc.taylor_order = 1;
   {  // errors: quaternion far from unit at node 3 -> "build qp: node 3: quad dynamics: ..."
     std::vector<Vec> bad = xs;
     bad[3][kQuatRow] = 3.0;

@@ -16,6 +16,8 @@ RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL, RTN_ER
 RTN_TF32, RTN_3XTF32, RTN_BF16X3 = range(3)
 RTN_BF16 = RTN_BF16X3
 PRECISIONS = {"tf32": RTN_TF32, "3xtf32": RTN_3XTF32, "bf16x3": RTN_BF16X3}
+# rtn_variant codes and (n_f, n_r) per residual variant (dynamics.hpp:95-131)
+VARIANTS = {"full": (0, 17, 6), "a": (1, 3, 3), "a_u": (2, 7, 3), "ground": (3, 26, 3)}
 
 # Every symbol include/rtn_mpc.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -36,11 +38,12 @@ class QuadParamsC(C.Structure):
 class OcpConfigC(C.Structure):
     _fields_ = [("horizon", C.c_int), ("dt", C.c_double), ("q_diag", C.c_double * 13), ("r_diag", C.c_double * 4),
                 ("has_q_terminal", C.c_int), ("q_terminal", C.c_double * 13), ("u_min", C.c_double * 4),
-                ("u_max", C.c_double * 4), ("taylor_order", C.c_int)]
+                ("u_max", C.c_double * 4), ("taylor_order", C.c_int), ("variant", C.c_int)]
 
 
 class IterateC(C.Structure):
-    _fields_ = [("xs", C.c_void_p), ("us", C.c_void_p), ("ref_xs", C.c_void_p), ("ref_us", C.c_void_p)]
+    _fields_ = [("xs", C.c_void_p), ("us", C.c_void_p), ("ref_xs", C.c_void_p), ("ref_us", C.c_void_p),
+                ("aux", C.c_void_p)]
 
 
 class ApproxC(C.Structure):

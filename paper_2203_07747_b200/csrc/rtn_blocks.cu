@@ -25,18 +25,88 @@ constexpr int kWarps = 4;          // 8 nodes per CTA
 constexpr int kDkStride = 18;      // dk row stride (doubles): 16-byte aligned pairs
 constexpr int kDk = kQNx * kDkStride;
 
-// Per-node scratch. 712 doubles = 5696 B ≡ 64 (mod 128): the two
-// nodes of a warp sit in disjoint banks, so their broadcast loads do not conflict.
+constexpr int kMaxNf = 26;
+
+// Per-node scratch, ≡ 64 (mod 128) bytes: the two nodes of a warp sit in
+// disjoint banks, so their broadcast loads do not conflict.
 struct NodeSmem {
   double dk[2][kDk];  // dk_{s-1} / dk_s rows, then the A|B staging area
-  double x[kQNx], xs[kQNx], u[kQNu], z0[kQNf], dz[kQNf + 1], k[4][kQNx], phi[kQNx];
-  double g[kQNr * kQNf];  // H_o·dz at the stage point (order 2)
-  double pad[12];
+  double x[kQNx], xs[kQNx], u[kQNu], z0[kMaxNf], dz[kMaxNf], k[4][kQNx], phi[kQNx], aux[9];
+  double g[kQNr * kQNf];  // H_o·dz at the stage point (order 2); n_r·n_f <= 102 for every variant
+  double pad[2];
 };
 static_assert(sizeof(NodeSmem) % 128 == 64, "node stride must split the banks");
 
 __device__ __forceinline__ void Report(unsigned long long* w, long long node, int code) {
   atomicMin(w, (static_cast<unsigned long long>(node) << 8) | static_cast<unsigned long long>(code));
+}
+
+// Column c of R(q) (QuatToRot, quat.hpp:36-44).
+__device__ __forceinline__ void RotCol(int c, double qw, double qx, double qy, double qz, double& r0, double& r1,
+                                       double& r2) {
+  if (c == 0) {
+    r0 = 1.0 - 2.0 * (qy * qy + qz * qz); r1 = 2.0 * (qx * qy + qw * qz); r2 = 2.0 * (qx * qz - qw * qy);
+  } else if (c == 1) {
+    r0 = 2.0 * (qx * qy - qw * qz); r1 = 1.0 - 2.0 * (qx * qx + qz * qz); r2 = 2.0 * (qy * qz + qw * qx);
+  } else {
+    r0 = 2.0 * (qx * qz + qw * qy); r1 = 2.0 * (qy * qz - qw * qx); r2 = 1.0 - 2.0 * (qx * qx + qy * qy);
+  }
+}
+
+// Feature c of the residual input at (x, u, aux): ResidualInput (dynamics.cpp:125-152)
+// and the ground layout of plant.cpp:60-73.
+template <int VAR>
+__device__ __forceinline__ double Feature(int c, const double* X, const double* U, const double* aux) {
+  if (VAR == kVarFull) return c < kQNx ? X[c] : U[c - kQNx];
+  if (VAR == kVarGround) return c < kQNx ? X[c] : (c < kQNf ? U[c - kQNx] : X[2] - aux[c - kQNf]);
+  if (c >= 3) return U[c - 3];  // a_u: [v_B; u]
+  double r0, r1, r2;            // v_B = R(q)ᵀ v_W (QuatRotateInv)
+  RotCol(c, X[3], X[4], X[5], X[6], r0, r1, r2);
+  return r0 * X[7] + r1 * X[8] + r2 * X[9];
+}
+
+// Row o of embed·jn·jz (sqp_rti.cpp:104-111) with jz = ResidualInputJacobian at the
+// stage state (dynamics.cpp:154-180): the residual row's derivative wrt (x, u).
+template <int VAR>
+__device__ __forceinline__ void ChainRow(const double (&jn)[VarNf(VAR)], const double* X, double (&jc)[kQNf]) {
+  if (VAR == kVarFull) {
+#pragma unroll
+    for (int c = 0; c < kQNf; ++c) jc[c] = jn[c];
+  } else if (VAR == kVarGround) {
+#pragma unroll
+    for (int c = 0; c < kQNf; ++c) jc[c] = jn[c];
+    double s = 0.0;  // ∂(z_WB·1 − patch)/∂p_z = 1
+#pragma unroll
+    for (int m = kQNf; m < 26; ++m) s += jn[m];
+    jc[2] += s;
+  } else {
+#pragma unroll
+    for (int c = 0; c < kQNf; ++c) jc[c] = 0.0;
+    const double qw = X[3], qx = X[4], qy = X[5], qz = X[6], v0 = X[7], v1 = X[8], v2 = X[9];
+    // ∂v_B/∂q_c = dR_cᵀ v (QuatRotateInvJacQ, quat.hpp:88-96; dR_c rows from quat.hpp:57-74)
+    const double d[4][3][3] = {{{0, -2 * qz, 2 * qy}, {2 * qz, 0, -2 * qx}, {-2 * qy, 2 * qx, 0}},
+                               {{0, 2 * qy, 2 * qz}, {2 * qy, -4 * qx, -2 * qw}, {2 * qz, 2 * qw, -4 * qx}},
+                               {{-4 * qy, 2 * qx, 2 * qw}, {2 * qx, 0, 2 * qz}, {-2 * qw, 2 * qz, -4 * qy}},
+                               {{-4 * qz, -2 * qw, 2 * qx}, {2 * qw, -4 * qz, 2 * qy}, {2 * qx, 2 * qy, 0}}};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) s += jn[m] * (d[c][0][m] * v0 + d[c][1][m] * v1 + d[c][2][m] * v2);
+      jc[3 + c] = s;
+    }
+    double rc[3][3];  // rc[i][j] = R(i, j)
+    RotCol(0, qw, qx, qy, qz, rc[0][0], rc[1][0], rc[2][0]);
+    RotCol(1, qw, qx, qy, qz, rc[0][1], rc[1][1], rc[2][1]);
+    RotCol(2, qw, qx, qy, qz, rc[0][2], rc[1][2], rc[2][2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)  // ∂v_B/∂v_W = Rᵀ: entry (m, c) = R(c, m)
+      jc[7 + c] = jn[0] * rc[c][0] + jn[1] * rc[c][1] + jn[2] * rc[c][2];
+    if (VAR == kVarAU) {
+#pragma unroll
+      for (int i = 0; i < kQNu; ++i) jc[kQNx + i] = jn[3 + i];
+    }
+  }
 }
 
 // Row i of QuadNominalDynamics (dynamics.cpp:64-86) AND of QuadNominalJacobians
@@ -153,8 +223,9 @@ __device__ __forceinline__ double NominalRowAndJacobian(int i, const double* X, 
   return f;
 }
 
-template <int ORDER>
+template <int ORDER, int VAR>
 __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams p) {
+  constexpr int NF = VarNf(VAR), NR = VarNr(VAR);
   __shared__ __align__(128) NodeSmem smem[kWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, r = lane & 15;
@@ -170,17 +241,17 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
   const long long xrow = inst * (p.N + 1) + n;
   const double dt = p.dt;
   const bool row = r < kQNx;
-  const bool res_row = r >= 7 && r < kQNx;  // rows carrying the residual (embed: v̇, ω̇)
+  const bool res_row = r >= 7 && r < 7 + NR;  // rows carrying the residual (embed: v̇ [, ω̇])
 
   if (row) S.x[r] = p.xs[xrow * kQNx + r];
   if (r < kQNu) S.u[r] = p.us[node * kQNu + r];
+  if (VAR == kVarGround && r < 9) S.aux[r] = p.aux[node * 9 + r];
   __syncwarp();
-  for (int c = r; c < kQNf; c += 16)
-    S.z0[c] = p.z0 ? p.z0[node * kQNf + c] : (c < kQNx ? S.x[c] : S.u[c - kQNx]);
+  for (int c = r; c < NF; c += 16) S.z0[c] = p.z0 ? p.z0[node * NF + c] : Feature<VAR>(c, S.x, S.u, S.aux);
   // Taylor rows: lane 7+o evaluates residual row o (TaylorApprox, taylor.hpp:13-24)
   const int o = res_row ? r - 7 : 0;
-  const double* jrow_g = p.jac + (node * kQNr + o) * kQNf;
-  const double fbo = res_row ? p.fbar[node * kQNr + o] : 0.0;
+  const double* jrow_g = p.jac + (node * NR + o) * NF;
+  const double fbo = res_row ? p.fbar[node * NR + o] : 0.0;
   // body wrench = mix · u (MixThrustTorque, dynamics.cpp:57-62)
   double tb[3], tau[3];
 #pragma unroll
@@ -199,15 +270,16 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
     // stage state x_s = x + c_s·k_{s-1} (integrator.cpp:57, 65, 73)
     if (row) S.xs[r] = s == 0 ? S.x[r] : S.x[r] + cs * S.k[s - 1][r];
     __syncwarp();
-    for (int c = r; c < kQNf; c += 16) S.dz[c] = (c < kQNx ? S.xs[c] : S.u[c - kQNx]) - S.z0[c];
+    // dz = features(x_s, u, aux) − z0 (the EvalTaylor argument, sqp_rti.cpp:96-99)
+    for (int c = r; c < NF; c += 16) S.dz[c] = Feature<VAR>(c, S.xs, S.u, S.aux) - S.z0[c];
     __syncwarp();
-    if (ORDER == 2) {  // G[o][a] = Σ_b H_o(a,b)·dz_b, 102 rows spread over the half-warp
-      const double* hn = p.hess + node * (kQNr * kQNf * kQNf);
-      for (int e = r; e < kQNr * kQNf; e += 16) {
-        const double* h = hn + e * kQNf;
+    if (ORDER == 2) {  // G[o][a] = Σ_b H_o(a,b)·dz_b, n_r·n_f rows spread over the half-warp
+      const double* hn = p.hess + node * (NR * NF * NF);
+      for (int e = r; e < NR * NF; e += 16) {
+        const double* h = hn + e * NF;
         double g = 0.0;
 #pragma unroll
-        for (int b = 0; b < kQNf; ++b) g += __ldg(h + b) * S.dz[b];
+        for (int b = 0; b < NF; ++b) g += __ldg(h + b) * S.dz[b];
         S.g[e] = g;
       }
       __syncwarp();
@@ -216,27 +288,26 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
     // stage Jacobian row: nominal + embed·EvalTaylorJacobian (taylor.cpp:66-74)
     double fx[kQNx], fu[kQNu], y = 0.0, fnom;
     {
-      double jr[kQNf];
+      double jn[NF], jc[kQNf];
 #pragma unroll
-      for (int c = 0; c < kQNf; ++c) jr[c] = res_row ? __ldg(jrow_g + c) : 0.0;
-      fnom = NominalRowAndJacobian(row ? r : 0, X, tb, tau, p, jr, fx, fu);
+      for (int c = 0; c < NF; ++c) jn[c] = res_row ? __ldg(jrow_g + c) : 0.0;
       if (res_row) {  // EvalTaylor row o: f_bar + jac·dz (+ ½ dzᵀ H_o dz) (taylor.cpp:57-64)
         double a1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < kQNf; ++c) a1 += jr[c] * S.dz[c];
+        for (int c = 0; c < NF; ++c) a1 += jn[c] * S.dz[c];
         y = fbo + a1;
-        if (ORDER == 2) {  // + ½ dzᵀ H_o dz; jn row o += H_o·dz (taylor.cpp:60-73)
-          const double* G = S.g + o * kQNf;
+        if (ORDER == 2) {  // jn row o += H_o·dz (EvalTaylorJacobian, taylor.cpp:66-74)
+          const double* G = S.g + o * NF;
           double qv = 0.0;
 #pragma unroll
-          for (int a = 0; a < kQNf; ++a) qv += S.dz[a] * G[a];
+          for (int a = 0; a < NF; ++a) qv += S.dz[a] * G[a];
 #pragma unroll
-          for (int c = 0; c < kQNx; ++c) fx[c] += G[c];
-#pragma unroll
-          for (int c = 0; c < kQNu; ++c) fu[c] += G[kQNx + c];
+          for (int c = 0; c < NF; ++c) jn[c] += G[c];
           y += 0.5 * qv;
         }
       }
+      ChainRow<VAR>(jn, X, jc);  // zero unless res_row (jn is zero there)
+      fnom = NominalRowAndJacobian(row ? r : 0, X, tb, tau, p, jc, fx, fu);
     }
     const double qn = sqrt(X[3] * X[3] + X[4] * X[4] + X[5] * X[5] + X[6] * X[6]);
     if (!failed && fabs(qn - 1.0) > 0.25) failed = 10 + s + 1;  // InputDomainError in f (dynamics.cpp:70-73)
@@ -328,17 +399,53 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
   }
 }
 
+template <int VAR>
+__global__ void FeaturesKernel(const double* __restrict__ xs, const double* __restrict__ us,
+                               const double* __restrict__ aux, long long n_inst, int N, double* __restrict__ z) {
+  constexpr int NF = VarNf(VAR);
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long K = n_inst * N;
+  if (e >= K * NF) return;
+  const long long node = e / NF;
+  const int c = static_cast<int>(e - node * NF);
+  const double* x = xs + (node + node / N) * kQNx;  // inst·(N+1) + n
+  z[e] = Feature<VAR>(c, x, us + node * kQNu, aux ? aux + node * 9 : nullptr);
+}
+
 }  // namespace
+
+cudaError_t LaunchFeatures(int variant, const double* xs, const double* us, const double* aux, long long n_inst,
+                           int N, double* z, cudaStream_t s) {
+  const long long total = n_inst * N * VarNf(variant);
+  if (total <= 0) return cudaSuccess;
+  const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+  switch (variant) {
+    case kVarA: FeaturesKernel<kVarA><<<grid, 256, 0, s>>>(xs, us, aux, n_inst, N, z); break;
+    case kVarAU: FeaturesKernel<kVarAU><<<grid, 256, 0, s>>>(xs, us, aux, n_inst, N, z); break;
+    case kVarGround: FeaturesKernel<kVarGround><<<grid, 256, 0, s>>>(xs, us, aux, n_inst, N, z); break;
+    default: FeaturesKernel<kVarFull><<<grid, 256, 0, s>>>(xs, us, aux, n_inst, N, z); break;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s) {
   const long long K = p.n_inst * p.N;
   if (K <= 0) return cudaSuccess;
   const long long per_cta = 2 * kWarps;
   const long long grid = (K + per_cta - 1) / per_cta;
-  if (p.order == 2)
-    QpBlocksKernel<2><<<static_cast<unsigned>(grid), kWarps * 32, 0, s>>>(p);
-  else
-    QpBlocksKernel<1><<<static_cast<unsigned>(grid), kWarps * 32, 0, s>>>(p);
+  const unsigned g = static_cast<unsigned>(grid);
+#define RTN_BLK_LAUNCH(O, V) QpBlocksKernel<O, V><<<g, kWarps * 32, 0, s>>>(p)
+  switch (p.variant * 2 + (p.order == 2 ? 1 : 0)) {
+    case kVarFull * 2: RTN_BLK_LAUNCH(1, kVarFull); break;
+    case kVarFull * 2 + 1: RTN_BLK_LAUNCH(2, kVarFull); break;
+    case kVarA * 2: RTN_BLK_LAUNCH(1, kVarA); break;
+    case kVarA * 2 + 1: RTN_BLK_LAUNCH(2, kVarA); break;
+    case kVarAU * 2: RTN_BLK_LAUNCH(1, kVarAU); break;
+    case kVarAU * 2 + 1: RTN_BLK_LAUNCH(2, kVarAU); break;
+    case kVarGround * 2: RTN_BLK_LAUNCH(1, kVarGround); break;
+    default: RTN_BLK_LAUNCH(2, kVarGround); break;
+  }
+#undef RTN_BLK_LAUNCH
   return cudaGetLastError();
 }
 

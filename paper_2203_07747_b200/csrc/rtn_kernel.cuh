@@ -68,9 +68,10 @@ struct KParams {
   const float* b0;   // WP
   const float* bh;   // (n_hidden-1) x WP
   const float* bl;   // kMaxOut     (out_scale ⊙ b_L + out_mean)
-  // Gather mode (rtn_cycle_qp): when zx != null, row k is the quadrotor feature
-  // vector [x_k; u_k] (ResidualInput 'full', dynamics.cpp:137-139) read straight
-  // from the iterate: zx = Iterate::xs (n_inst x (N+1) x 13), zu = us (K x 4).
+  // Gather mode (rtn_cycle_qp, 'full' variant): when zx != null, row k is the
+  // quadrotor feature vector [x_k; u_k] (ResidualInput 'full', dynamics.cpp:137-139)
+  // read straight from the iterate: zx = Iterate::xs (n_inst x (N+1) x 13),
+  // zu = us (K x 4). Other variants stage their features with FeaturesKernel.
   const double* zx;
   const double* zu;
   int zN;

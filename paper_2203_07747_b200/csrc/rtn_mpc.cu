@@ -535,7 +535,8 @@ enum class Kern { kSingle, kPair, kLatency, kQuad };
 Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
   const bool lat_ok = m->has_pair && m->n_in + 1 <= 24;
   // quad: 4-CTA clusters, one tile of 2 nodes each (TF32, width 512; order-1 path only reaches here)
-  const bool quad_ok = lat_ok && m->pair_mode == rtn::kTF32 && m->pair_wp == 512 && K <= 2 * (num_sms / 4);
+  const bool quad_ok = lat_ok && m->pair_mode == rtn::kTF32 && m->pair_wp == 512 && m->n_in <= rtn::kMaxIn0 &&
+                       K <= 2 * (num_sms / 4);
   if (const char* e = std::getenv("RTN_KERNEL"))
     if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
   if (quad_ok && !std::getenv("RTN_KERNEL")) {
@@ -632,7 +633,8 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
     cudaError_t e;
     const char* pp = std::getenv("RTN_PINGPONG");
-    if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && prm.P == 4 && !(pp && pp[0] == '0')) {
+    if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && prm.P == 4 && m->n_in <= rtn::kMaxIn0 &&
+        !(pp && pp[0] == '0')) {
       // width 256: two tiles in flight per CTA pair (rtn_pingpong.cuh)
       const long long tile_pairs = (prm.num_tiles + 1) / 2;
       const int g2 = 2 * static_cast<int>(std::min<long long>(tile_pairs, c->num_sms / 2));
@@ -960,7 +962,7 @@ rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int or
 // Continuity-block builder host side (resmpc::BuildQp, sqp_rti.cpp:59-155).
 namespace {
 
-constexpr int kNx = 13, kNu = 4, kNf = 17, kNr = 6;
+constexpr int kNx = 13, kNu = 4;
 
 // QuadParams::Validate (proj/src/dynamics.cpp:29-40), same messages.
 void ValidateQuad(const rtn_quad_params& p) {
@@ -988,6 +990,9 @@ void ValidateCfg(const rtn_ocp_config& c) {
   for (int i = 0; i < kNu; ++i)
     if (c.u_min[i] >= c.u_max[i]) throw Error(RTN_ECONFIG, "ocp config: u_min must be below u_max");
   if (c.taylor_order != 1 && c.taylor_order != 2) throw Error(RTN_ECONFIG, "ocp config: taylor_order must be 1 or 2");
+  if (c.variant < 0 || c.variant > 3)
+    throw Error(RTN_ECONFIG, "unknown residual variant code " + std::to_string(c.variant) +
+                                 " (expected full, a, a_u, ground)");
 }
 
 rtn::BlkParams MakeBlk(const rtn_quad_params& p, const rtn_ocp_config& c, long long n_inst) {
@@ -995,6 +1000,7 @@ rtn::BlkParams MakeBlk(const rtn_quad_params& p, const rtn_ocp_config& c, long l
   b.n_inst = n_inst;
   b.N = c.horizon;
   b.order = c.taylor_order;
+  b.variant = c.variant;
   b.dt = c.dt;
   b.mass = p.mass;
   b.inv_mass = 1.0 / p.mass;
@@ -1091,20 +1097,24 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
   ValidateQuad(*p);  // configuration errors first, as BuildQp validates before any work
   ValidateCfg(*cfg);
   if (!c || !it || !out || (!cycle && !ap)) throw Error(RTN_ECONFIG, "null argument");
-  const int N = cfg->horizon, order = cfg->taylor_order;
+  const int N = cfg->horizon, order = cfg->taylor_order, var = cfg->variant;
+  const int nf = rtn::VarNf(var), nr = rtn::VarNr(var);
   if (n_inst < 0) throw Error(RTN_EDOMAIN, "n_inst must be >= 0");
   const long long K = n_inst * N;
   if (K > c->max_rows) throw Error(RTN_EDOMAIN, "n_inst * horizon exceeds the context's max_rows");
   const rtn_model* m = c->model;
   if (cycle) {
-    if (m->n_in != kNf || m->n_out != kNr)
-      throw Error(RTN_ECONFIG, "rtn controller: model is " + std::to_string(m->n_in) + " -> " +
-                                   std::to_string(m->n_out) + ", the quadrotor 'full' plant needs 17 -> 6");
+    if (m->n_in != nf || m->n_out != nr)  // sqp_rti.cpp:196-197
+      throw Error(RTN_ECONFIG, "controller: model dimensions do not match the plant's residual wiring (model " +
+                                   std::to_string(m->n_in) + " -> " + std::to_string(m->n_out) + ", variant needs " +
+                                   std::to_string(nf) + " -> " + std::to_string(nr) + ")");
     if (order > c->max_order) throw Error(RTN_EUNSUPPORTED, "taylor_order exceeds the context's max_order");
     if (order == 2 && m->act == RTN_ACT_RELU)
       throw Error(RTN_EUNSUPPORTED, "mlp hessian: relu networks are not twice differentiable");
   }
   if (K > 0 && (!it->xs || !it->us || !it->ref_xs || !it->ref_us)) throw Error(RTN_ECONFIG, "null iterate buffer");
+  if (K > 0 && var == rtn::kVarGround && !it->aux)
+    throw Error(RTN_EDOMAIN, "quadrotor plant: ground features need a 9-entry patch aux per node");
   if (!cycle && K > 0 && (!ap->z0 || !ap->f_bar || !ap->jac || (order == 2 && !ap->hess)))
     throw Error(RTN_ECONFIG, "null approximation buffer");
   if (cycle) {
@@ -1119,19 +1129,20 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
   QpPlan plan;
   const size_t o_xs = plan.add_in(it->xs, X), o_us = plan.add_in(it->us, U), o_rxs = plan.add_in(it->ref_xs, X),
                o_rus = plan.add_in(it->ref_us, U);
+  const size_t o_aux = var == rtn::kVarGround ? plan.add_in(it->aux, Kz * 9) : 0;
   size_t o_z0 = 0, o_fb = 0, o_jac = 0, o_hess = 0;
   if (!cycle) {
-    o_z0 = plan.add_in(ap->z0, Kz * kNf);
-    o_fb = plan.add_in(ap->f_bar, Kz * kNr);
-    o_jac = plan.add_in(ap->jac, Kz * kNr * kNf);
-    if (order == 2) o_hess = plan.add_in(ap->hess, Kz * kNr * kNf * kNf);
+    o_z0 = plan.add_in(ap->z0, Kz * nf);
+    o_fb = plan.add_in(ap->f_bar, Kz * nr);
+    o_jac = plan.add_in(ap->jac, Kz * nr * nf);
+    if (order == 2) o_hess = plan.add_in(ap->hess, Kz * nr * nf * nf);
   }
   const size_t o_a = plan.add_out(out->a, Kz * kNx * kNx), o_b = plan.add_out(out->b, Kz * kNx * kNu),
                o_phi = plan.add_out(out->phi_res, Kz * kNx), o_q = plan.add_out(out->q, X),
                o_r = plan.add_out(out->r, U), o_hx = plan.add_out(out->hx_diag, X), o_hu = plan.add_out(out->hu_diag, U),
                o_lb = plan.add_out(out->du_lb, U), o_ub = plan.add_out(out->du_ub, U);
   // device-side approximations of the cycle are copied out like the blocks
-  Slice sf{nullptr, f, 0, Kz * kNr}, sj{nullptr, jac, 0, Kz * kNr * kNf}, sh{nullptr, hess, 0, Kz * kNr * kNf * kNf};
+  Slice sf{nullptr, f, 0, Kz * nr}, sj{nullptr, jac, 0, Kz * nr * nf}, sh{nullptr, hess, 0, Kz * nr * nf * nf};
 
   Grow(&c->d_qin, &c->qin_cap, plan.in_total, false);
   Grow(&c->d_qout, &c->qout_cap, std::max<size_t>(plan.out_total, 1), false);
@@ -1146,6 +1157,7 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
   b.us = din + o_us;
   b.rxs = din + o_rxs;
   b.rus = din + o_rus;
+  b.aux = var == rtn::kVarGround ? din + o_aux : nullptr;
   if (cycle) {
     b.z0 = nullptr;  // z0 = [x_k; u_k], the point PrepareNodes was evaluated at
     b.fbar = c->d_f;
@@ -1171,8 +1183,13 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
 
   auto enqueue_compute = [&](cudaStream_t s) {
     if (b.first_bad) CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), s));
-    if (cycle)  // PrepareNodes at z_k = [x_k; u_k], gathered from the iterate inside layer 0
+    if (cycle && var == rtn::kVarFull) {  // PrepareNodes at z_k = [x_k; u_k], gathered inside layer 0
       Enqueue(c, nullptr, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr, b.xs, b.us, N);
+    } else if (cycle) {  // other variants: stage z_k = features(x_k, u_k, aux_k) first
+      CUDA_CHECK(rtn::LaunchFeatures(var, b.xs, b.us, b.aux, n_inst, N, c->d_z, s));
+      c->launches += 1;
+      Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr);
+    }
     CUDA_CHECK(rtn::LaunchQpBlocks(b, s));
     c->launches += 1;
   };
@@ -1214,6 +1231,7 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
       b.us = hin + o_us;
       b.rxs = hin + o_rxs;
       b.rus = hin + o_rus;
+      b.aux = var == rtn::kVarGround ? hin + o_aux : nullptr;
       if (!cycle) {
         b.z0 = hin + o_z0;
         b.fbar = hin + o_fb;
@@ -1337,7 +1355,9 @@ rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_o
     b.fbar = ap->f_bar;
     b.jac = ap->jac;
     b.hess = cfg->taylor_order == 2 ? ap->hess : nullptr;
-    if (!b.xs || !b.us || !b.rxs || !b.rus || !b.fbar || !b.jac || (cfg->taylor_order == 2 && !b.hess))
+    b.aux = cfg->variant == rtn::kVarGround ? it->aux : nullptr;
+    if (!b.xs || !b.us || !b.rxs || !b.rus || !b.fbar || !b.jac || (cfg->taylor_order == 2 && !b.hess) ||
+        (cfg->variant == rtn::kVarGround && !b.aux))
       throw Error(RTN_ECONFIG, "null device buffer");
     b.a = out->a;
     b.b = out->b;

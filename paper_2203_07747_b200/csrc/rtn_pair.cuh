@@ -526,17 +526,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---- layer 0 (CUDA cores): this CTA owns K-groups g ≡ rank (mod 2); half h writes side h
       for (int g = static_cast<int>(rank); g < NG; g += 2) {
         const int j = g * 128 + tid_h;
-        float w0[kMaxIn0];
-        load_w0_row(prm.w0 + j * n_in, n_in, w0);
         const float bj = __ldg(prm.b0 + j);
         float val[P], sp[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) act_fwd(act, layer0_pre(bj, w0, zs + (half * P + p) * n_in, n_in), val[p], sp[p]);
         float v[NTC];
+        // P·(1+n_in) <= NTC bounds n_in: tiles of P >= 4 (or 24 rows) never see more than
+        // kMaxIn0 inputs, so only the small-P tiles carry the streaming fallback.
+        constexpr bool kMayBeWide = P < 4 && NTC / P - 1 > kMaxIn0;
+        if (!kMayBeWide || n_in <= kMaxIn0) {  // weight row in registers
+          float w0[kMaxIn0];
+          load_w0_row(prm.w0 + j * n_in, n_in, w0);
 #pragma unroll
-        for (int i = 0; i < NTC; ++i) {
-          if (i < P) v[i] = val[i];
-          else v[i] = i < rows_used ? sp[i % P] * w0[((i - P) / P) % kMaxIn0] : 0.0f;
+          for (int p = 0; p < P; ++p)
+            act_fwd(act, layer0_pre(bj, w0, zs + (half * P + p) * n_in, n_in), val[p], sp[p]);
+#pragma unroll
+          for (int i = 0; i < NTC; ++i) {
+            if (i < P) v[i] = val[i];
+            else v[i] = i < rows_used ? sp[i % P] * w0[((i - P) / P) % kMaxIn0] : 0.0f;
+          }
+        } else if constexpr (kMayBeWide) {  // wide inputs (e.g. the 26-feature ground variant)
+          const float* w0r = prm.w0 + j * n_in;
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            float pre = bj;
+            for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[(half * P + p) * n_in + k], pre);
+            act_fwd(act, pre, val[p], sp[p]);
+          }
+#pragma unroll
+          for (int i = 0; i < NTC; ++i) {
+            if (i < P) v[i] = val[i];
+            else v[i] = i < rows_used ? sp[i % P] * __ldg(w0r + (i - P) / P) : 0.0f;
+          }
         }
         store_side(v, j);
         publish(g);

@@ -1,5 +1,5 @@
 """Host mirror of the reference's QP-block construction for the quadrotor
-'full' plant — the step after PrepareNodes.
+plant — the step after PrepareNodes.
 
     QpData resmpc::BuildQp(plant, cfg, iterate, refs, &approxes, nullptr, ...)
         -- /root/reference/proj/include/resmpc/sqp_rti.hpp:56-59
@@ -7,9 +7,12 @@
 
 `build_qp` takes prepared approximations (one TaylorApprox per node, or the
 flat arrays `prepare_nodes` produces) and runs the RK4 sensitivities of
-f_F + embed·Taylor on the device (csrc/rtn_blocks.cu). `cycle_qp` fuses
-phases 1 and 2 of `RtiController::Cycle` (sqp_rti.cpp:219-231): features
-z_k = [x_k; u_k] → PrepareNodes → BuildQp in one device pass. Both batch
+f_F + embed·Taylor on the device (csrc/rtn_blocks.cu), for every residual
+variant (OcpConfig.variant: full, a, a_u, ground — the feature map and its
+Jacobian are re-evaluated at each RK4 stage, dynamics.cpp:125-180). `cycle_qp`
+fuses phases 1 and 2 of `RtiController::Cycle` (sqp_rti.cpp:219-231): the
+MLP's layer 0 gathers z_k = features(x_k, u_k, aux_k) from the iterate →
+PrepareNodes → BuildQp in one device pass. Both batch
 over independent MPC instances (leading axis). Errors follow the reference:
 ConfigError for bad parameters/config (same messages), RuntimeError
 "build qp: node k: ..." for a non-finite stage derivative or a quaternion
@@ -66,6 +69,13 @@ class OcpConfig:
     u_min: np.ndarray = field(default_factory=lambda: np.zeros(NU))
     u_max: np.ndarray = field(default_factory=lambda: np.full(NU, 6.0))
     taylor_order: int = 1
+    variant: str = "full"  # residual variant: full, a, a_u, ground (dynamics.hpp:95-131)
+
+    def dims(self) -> tuple[int, int]:
+        """(n_f, n_r) of the variant's network."""
+        if self.variant not in _lib.VARIANTS:
+            raise ConfigError(f"unknown residual variant '{self.variant}' (expected a, a_u, full, ground)")
+        return _lib.VARIANTS[self.variant][1:]
 
     def terminal_weight(self) -> np.ndarray:
         return self.q_diag if self.q_terminal is None else self.q_terminal
@@ -78,6 +88,8 @@ class OcpConfig:
             return [float(x) for x in v]
         c = _lib.OcpConfigC()
         c.horizon, c.dt, c.taylor_order = int(self.horizon), float(self.dt), int(self.taylor_order)
+        self.dims()
+        c.variant = _lib.VARIANTS[self.variant][0]
         c.q_diag[:] = vec(self.q_diag, NX, "weight dimensions do not match the plant")
         c.r_diag[:] = vec(self.r_diag, NU, "weight dimensions do not match the plant")
         c.has_q_terminal = 0 if self.q_terminal is None else 1
@@ -131,7 +143,7 @@ def _batched(a, tail: tuple, what: str) -> np.ndarray:
     return np.ascontiguousarray(a)
 
 
-def _approx_arrays(approxes, n_inst: int, n: int, order: int):
+def _approx_arrays(approxes, n_inst: int, n: int, order: int, nf: int = NF, nr: int = NR):
     """TaylorApprox list (per node, instance-major) or dict/tuple of flat arrays."""
     k = n_inst * n
     if isinstance(approxes, dict):
@@ -149,10 +161,10 @@ def _approx_arrays(approxes, n_inst: int, n: int, order: int):
                 raise ConfigError("build qp: approximation order does not match taylor_order")
     else:
         raise ConfigError("build qp: approxes must be TaylorApprox objects or a dict of arrays")
-    out = [np.ascontiguousarray(np.reshape(z0, (k, NF)), dtype=np.float64),
-           np.ascontiguousarray(np.reshape(fb, (k, NR)), dtype=np.float64),
-           np.ascontiguousarray(np.reshape(jac, (k, NR, NF)), dtype=np.float64)]
-    out.append(np.ascontiguousarray(np.reshape(hess, (k, NR, NF, NF)), dtype=np.float64) if order == 2 else None)
+    out = [np.ascontiguousarray(np.reshape(z0, (k, nf)), dtype=np.float64),
+           np.ascontiguousarray(np.reshape(fb, (k, nr)), dtype=np.float64),
+           np.ascontiguousarray(np.reshape(jac, (k, nr, nf)), dtype=np.float64)]
+    out.append(np.ascontiguousarray(np.reshape(hess, (k, nr, nf, nf)), dtype=np.float64) if order == 2 else None)
     if order == 2 and hess is None:
         raise ConfigError("build qp: taylor_order 2 needs Hessians")
     return out
@@ -173,7 +185,7 @@ class QpBuilder:
         c = _lib.QpBlocksC(*[_ptr(arrs[k]) for k in _QP_FIELDS])
         return arrs, c
 
-    def _iterate(self, cfg: OcpConfig, xs, us, ref_xs, ref_us):
+    def _iterate(self, cfg: OcpConfig, xs, us, ref_xs, ref_us, aux=None):
         n = int(cfg.horizon)
         xs = _batched(xs, (n + 1, NX), "iterate xs")
         us = _batched(us, (n, NU), "iterate us")
@@ -181,15 +193,23 @@ class QpBuilder:
         ru = _batched(ref_us, (n, NU), "reference us")
         if not (xs.shape[0] == us.shape[0] == rx.shape[0] == ru.shape[0]):
             raise ConfigError("build qp: iterate and reference window instance counts differ")
-        return xs, us, rx, ru, _lib.IterateC(_ptr(xs), _ptr(us), _ptr(rx), _ptr(ru))
+        ax = None
+        if cfg.variant == "ground":
+            if aux is None:
+                raise ConfigError("quadrotor plant: ground features need a 9-entry patch aux per node")
+            ax = _batched(aux, (n, 9), "ground patches")
+        self._keep = (xs, us, rx, ru, ax)
+        return xs, us, rx, ru, _lib.IterateC(_ptr(xs), _ptr(us), _ptr(rx), _ptr(ru), _ptr(ax))
 
-    def build_qp(self, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, approxes) -> QpData:
-        """BuildQp in rtn mode from prepared approximations (sqp_rti.cpp:59-155)."""
+    def build_qp(self, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, approxes, aux=None) -> QpData:
+        """BuildQp in rtn mode from prepared approximations (sqp_rti.cpp:59-155).
+        aux: per-node 3x3 height patches (row-major, n_inst x N x 9), ground variant only."""
         if cfg.horizon < 1:
             raise ConfigError("ocp config: horizon must be >= 1")
-        xs, us, rx, ru, it = self._iterate(cfg, xs, us, ref_xs, ref_us)
+        nf, nr = cfg.dims()
+        xs, us, rx, ru, it = self._iterate(cfg, xs, us, ref_xs, ref_us, aux)
         n_inst, n = xs.shape[0], int(cfg.horizon)
-        z0, fb, jac, hess = _approx_arrays(approxes, n_inst, n, int(cfg.taylor_order))
+        z0, fb, jac, hess = _approx_arrays(approxes, n_inst, n, int(cfg.taylor_order), nf, nr)
         ap = _lib.ApproxC(_ptr(z0), _ptr(fb), _ptr(jac), _ptr(hess))
         arrs, oc = self._outputs(n_inst, n)
         self.engine._ensure(max(n_inst * n, 1), 1)
@@ -199,20 +219,22 @@ class QpBuilder:
                                                  C.byref(ap), C.byref(oc), fe))
         return QpData(NX, NU, n, *(arrs[k] for k in _QP_FIELDS), f_evals=(fe[0], fe[1]))
 
-    def cycle_qp(self, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, return_approx: bool = False):
+    def cycle_qp(self, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, return_approx: bool = False,
+                 aux=None):
         """Phases 1+2 of RtiController::Cycle on the device: PrepareNodes at
-        z_k = [x_k; u_k] (taylor.cpp:37-55) then BuildQp (sqp_rti.cpp:59-155)."""
+        z_k = features(x_k, u_k, aux_k) (taylor.cpp:37-55) then BuildQp (sqp_rti.cpp:59-155)."""
         if cfg.horizon < 1:
             raise ConfigError("ocp config: horizon must be >= 1")
-        xs, us, rx, ru, it = self._iterate(cfg, xs, us, ref_xs, ref_us)
+        nf, nr = cfg.dims()
+        xs, us, rx, ru, it = self._iterate(cfg, xs, us, ref_xs, ref_us, aux)
         n_inst, n = xs.shape[0], int(cfg.horizon)
         k = n_inst * n
         order = int(cfg.taylor_order)
         arrs, oc = self._outputs(n_inst, n)
         f = jac = hess = None
         if return_approx:
-            f, jac = np.empty((k, NR)), np.empty((k, NR, NF))
-            hess = np.empty((k, NR, NF, NF)) if order == 2 else None
+            f, jac = np.empty((k, nr)), np.empty((k, nr, nf))
+            hess = np.empty((k, nr, nf, nf)) if order == 2 else None
         self.engine._ensure(max(k, 1), max(1, min(order, 2)))
         pc, cc = params.to_c(), cfg.to_c()
         raise_for_status(_lib.lib().rtn_cycle_qp(self.engine.ctx_ptr, C.byref(pc), C.byref(cc), n_inst, C.byref(it),
@@ -224,10 +246,10 @@ class QpBuilder:
 
 
 def build_qp(model: MlpModel, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, approxes,
-             **kw) -> QpData:
-    return QpBuilder(model, **kw).build_qp(params, cfg, xs, us, ref_xs, ref_us, approxes)
+             aux=None, **kw) -> QpData:
+    return QpBuilder(model, **kw).build_qp(params, cfg, xs, us, ref_xs, ref_us, approxes, aux=aux)
 
 
-def cycle_qp(model: MlpModel, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, **kw):
+def cycle_qp(model: MlpModel, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, aux=None, **kw):
     ret = kw.pop("return_approx", False)
-    return QpBuilder(model, **kw).cycle_qp(params, cfg, xs, us, ref_xs, ref_us, return_approx=ret)
+    return QpBuilder(model, **kw).cycle_qp(params, cfg, xs, us, ref_xs, ref_us, return_approx=ret, aux=aux)

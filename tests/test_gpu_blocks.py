@@ -215,3 +215,80 @@ def test_latency_mode_errors_and_recovery():
     ref = _oracle_qp(p, cfg, xs, us, rx, ru, z, f, j, None)
     got = b.build_qp(p, cfg, xs, us, rx, ru, ap)
     assert _block_err(got.a, ref["a"]) < TOL
+
+
+# --- residual variants: features + chain rule on the device ---
+VARS = {"a": (3, 3), "a_u": (7, 3), "full": (17, 6), "ground": (26, 3)}
+
+
+def _variant_case(var, n_inst, n, order, seed=17, hidden=(32, 32)):
+    xs, us, rx, ru, *_ = _case(n_inst, n, seed=seed)
+    nf, nr = VARS[var]
+    rng = np.random.default_rng(seed + 1)
+    aux = rng.uniform(-0.3, 0.4, (n_inst, n, 9)) if var == "ground" else None
+    x, u = xs[:, :n, :], us
+    if var == "full":
+        z = np.concatenate([x, u], axis=-1)
+    elif var == "ground":
+        z = np.concatenate([x, u, x[..., 2:3] - aux], axis=-1)
+    else:
+        q, v = x[..., 3:7], x[..., 7:10]
+        w_, x_, y_, z_ = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+        R = np.stack([np.stack([1 - 2 * (y_ * y_ + z_ * z_), 2 * (x_ * y_ - w_ * z_), 2 * (x_ * z_ + w_ * y_)], -1),
+                      np.stack([2 * (x_ * y_ + w_ * z_), 1 - 2 * (x_ * x_ + z_ * z_), 2 * (y_ * z_ - w_ * x_)], -1),
+                      np.stack([2 * (x_ * z_ - w_ * y_), 2 * (y_ * z_ + w_ * x_), 1 - 2 * (x_ * x_ + y_ * y_)], -1)], -2)
+        vb = np.einsum("...ij,...i->...j", R, v)  # Rᵀ v
+        z = vb if var == "a" else np.concatenate([vb, u], axis=-1)
+    z = z.reshape(-1, nf)
+    om = oracle.OracleModel.random_net([nf, *hidden, nr], "silu", seed, True)
+    f, j, h = om.batched_eval(z, order)
+    return xs, us, rx, ru, z, f, j, h, om, aux
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("var", ["a", "a_u", "full", "ground"])
+def test_build_qp_variants_match_oracle(var, order):
+    """BuildQp for every residual variant: stage features + jz chain rule
+    (dynamics.cpp:125-180, sqp_rti.cpp:96-111) at fp64 parity."""
+    n_inst, n = 5, 12
+    xs, us, rx, ru, z, f, j, h, om, aux = _variant_case(var, n_inst, n, order)
+    p, cfg = qp.QuadParams(), _cfg(n, order)
+    cfg.variant = var
+    ref = oracle.build_qp_quad(p.flat(), cfg.flat(), n, 0, order, xs, us, rx, ru, z, f, j, h if order == 2 else None,
+                               variant=var, aux=aux)
+    b = qp.QpBuilder(_model(oracle.OracleModel.random_net([17, 8, 6], "tanh", 1, True)))  # context owner only
+    got = b.build_qp(p, cfg, xs, us, rx, ru, {"z0": z, "f_bar": f, "jac": j, "hess": h if order == 2 else None}, aux=aux)
+    for name in FIELDS:
+        assert _block_err(getattr(got, name), ref[name]) < TOL, (var, order, name)
+
+
+@pytest.mark.parametrize("var", ["a", "a_u", "ground"])
+def test_cycle_qp_variants_fused(var):
+    """The fused cycle for every variant: the MLP's layer 0 gathers the variant's
+    features from the iterate; blocks match the oracle on the device's own
+    approximations (fp64), and those match the oracle PrepareNodes (3xTF32)."""
+    n_inst, n = 3, 20
+    xs, us, rx, ru, z, f, j, h, om, aux = _variant_case(var, n_inst, n, 1, hidden=(64, 64))
+    p, cfg = qp.QuadParams(), _cfg(n, 1)
+    cfg.variant = var
+    for latency in (0, 1):
+        b = qp.QpBuilder(_model(om), precision=_lib.RTN_3XTF32, latency_mode=latency)
+        got, ap = b.cycle_qp(p, cfg, xs, us, rx, ru, return_approx=True, aux=aux)
+        assert oracle.max_node_rel_error(ap["f_bar"], f) < 1e-5 and oracle.max_node_rel_error(ap["jac"], j) < 1e-5
+        ref = oracle.build_qp_quad(p.flat(), cfg.flat(), n, 0, 1, xs, us, rx, ru, z, ap["f_bar"], ap["jac"],
+                                   variant=var, aux=aux)
+        for name in FIELDS:
+            assert _block_err(getattr(got, name), ref[name]) < TOL, (var, latency, name)
+
+
+def test_variant_model_mismatch_rejected():
+    om = oracle.OracleModel.random_net([17, 16, 6], "tanh", 1, True)
+    xs, us, rx, ru, *_ = _case(1, 4)
+    cfg = _cfg(4)
+    cfg.variant = "a"
+    with pytest.raises(ConfigError, match="residual wiring"):
+        qp.cycle_qp(_model(om), qp.QuadParams(), cfg, xs, us, rx, ru)
+    cfg.variant = "ground"
+    om3 = oracle.OracleModel.random_net([26, 16, 3], "tanh", 1, True)
+    with pytest.raises(ConfigError, match="patch aux"):
+        qp.cycle_qp(_model(om3), qp.QuadParams(), cfg, xs, us, rx, ru)
