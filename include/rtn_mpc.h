@@ -201,6 +201,32 @@ rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_o
 rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
                         const rtn_iterate* it, rtn_qp_blocks* out, double* f, double* jac, double* hess);
 
+/* ---------------------------------------------------------------------------
+ * Batched feedback solve: resmpc::SolveFeedback
+ * (/root/reference/proj/src/sqp_rti.cpp:157-180) per MPC instance — condensing
+ * (proj/src/qp.cpp:33-73), the primal active-set box QP with the reference's
+ * pivot rules and regularisation (qp.cpp:77-208), and the state recovery
+ * dx_k = M_k·du + c_k. Quadrotor dims (nx 13, nu 4), N <= 64. Per-instance
+ * status instead of exceptions (RtiController::Cycle turns a throw into
+ * ok = false, sqp_rti.cpp:247-252):
+ *   0 optimal, 1 iteration cap (QpStatus::kMaxIter), 2 SolveFeedback threw
+ *   (non-finite measured state or solution, crossed bounds), 3 Hessian not
+ *   positive definite after regularisation.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  double* dxs;         /* n_inst x (N+1) x 13  FeedbackResult::dxs */
+  double* dus;         /* n_inst x N x 4       FeedbackResult::dus */
+  double* u_command;   /* n_inst x 4           iterate head input + its step */
+  int* status;         /* n_inst */
+  int* iterations;     /* n_inst, may be NULL */
+  signed char* active; /* n_inst x 4N working set: warm-start hint in, final set out; may be NULL */
+} rtn_feedback;
+
+/* qp: QpData as rtn_build_qp returns it; it->xs / it->us: the iterate (dx0 =
+ * x_measured − xs[0]); x_measured: n_inst x 13. Host buffers, blocking. */
+rtn_status rtn_solve_feedback(rtn_ctx* c, const rtn_ocp_config* cfg, long long n_inst, const rtn_qp_blocks* qp,
+                              const double* x_measured, const rtn_iterate* it, rtn_feedback* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -319,3 +319,31 @@ def closed_loop(om, params_flat, cfg_flat, horizon, order, traj=(0, 5.0, 2.0, 20
     n = n_steps.value
     return {"states": states[:n], "commands": commands[:n], "ok": ok[:n], "failed": bool(failed.value),
             "callback_errors": errors}
+
+
+def solve_feedback(horizon, qpd, x_meas, xs, us, active=None):
+    """oracle SolveFeedback per instance (closedloop_oracle.cpp); qpd: dict/obj of QpData arrays."""
+    n = int(horizon)
+    get = (lambda k: qpd[k]) if isinstance(qpd, dict) else (lambda k: getattr(qpd, k))
+    arr = [np.ascontiguousarray(get(k), dtype=np.float64) for k in
+           ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag", "du_lb", "du_ub")]
+    xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1, n + 1, 13)
+    n_inst = xs.shape[0]
+    us = np.ascontiguousarray(us, dtype=np.float64).reshape(n_inst, n, 4)
+    xm = np.ascontiguousarray(x_meas, dtype=np.float64).reshape(n_inst, 13)
+    act = (np.zeros((n_inst, 4 * n), dtype=np.int8) if active is None
+           else np.ascontiguousarray(active, dtype=np.int8).reshape(n_inst, 4 * n).copy())
+    dxs, dus, u = np.empty((n_inst, n + 1, 13)), np.empty((n_inst, n, 4)), np.empty((n_inst, 4))
+    st, it = np.empty(n_inst, dtype=np.int32), np.empty(n_inst, dtype=np.int32)
+    L = lib()
+    if not hasattr(L, "_fb_bound"):
+        ip = C.POINTER(C.c_int)
+        L.oracle_solve_feedback.argtypes = [C.c_int, C.c_longlong] + [_dp] * 12 + [C.POINTER(C.c_byte), _dp, _dp, _dp,
+                                                                                   ip, ip]
+        L._fb_bound = True
+    rc = L.oracle_solve_feedback(n, n_inst, *[_p(a) for a in arr], _p(xm), _p(xs), _p(us),
+                                 act.ctypes.data_as(C.POINTER(C.c_byte)), _p(dxs), _p(dus), _p(u),
+                                 st.ctypes.data_as(C.POINTER(C.c_int)), it.ctypes.data_as(C.POINTER(C.c_int)))
+    if rc != 0:
+        raise OracleError(rc, L.oracle_closed_loop_last_error().decode())
+    return {"dxs": dxs, "dus": dus, "u_command": u, "status": st, "iterations": it, "active": act}

@@ -767,3 +767,76 @@ int oracle_closed_loop(const void* model, const double* params, const double* cf
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// SolveFeedback (sqp_rti.cpp:157-180) for a batch of instances (QpData arrays
+// in the C-ABI layout of rtn_qp_blocks), the checker of rtn_solve_feedback.
+extern "C" {
+
+int oracle_solve_feedback(int horizon, long long n_inst, const double* a, const double* b, const double* phi,
+                          const double* q, const double* r, const double* hx, const double* hu, const double* lb,
+                          const double* ub, const double* x_meas, const double* xs, const double* us,
+                          signed char* warm /* n_inst x N*4, in/out, may be null */, double* dxs, double* dus,
+                          double* u_cmd, int* status, int* iterations) {
+  using namespace oracle;
+  try {
+    const int n = horizon, nx = 13, nu = 4, nv = n * nu;
+    for (long long i = 0; i < n_inst; ++i) {
+      QpData d;
+      d.nx = nx;
+      d.nu = nu;
+      d.horizon = n;
+      for (int k = 0; k < n; ++k) {
+        const long long row = i * n + k;
+        Mat ak(nx, nx), bk(nx, nu);
+        std::copy(a + row * 169, a + (row + 1) * 169, ak.v.begin());
+        std::copy(b + row * 52, b + (row + 1) * 52, bk.v.begin());
+        d.a.push_back(ak);
+        d.b.push_back(bk);
+        d.phi_res.emplace_back(phi + row * nx, phi + (row + 1) * nx);
+        d.r.emplace_back(r + row * nu, r + (row + 1) * nu);
+        d.hu_diag.emplace_back(hu + row * nu, hu + (row + 1) * nu);
+        d.du_lb.emplace_back(lb + row * nu, lb + (row + 1) * nu);
+        d.du_ub.emplace_back(ub + row * nu, ub + (row + 1) * nu);
+      }
+      for (int k = 0; k <= n; ++k) {
+        const long long row = i * (n + 1) + k;
+        d.q.emplace_back(q + row * nx, q + (row + 1) * nx);
+        d.hx_diag.emplace_back(hx + row * nx, hx + (row + 1) * nx);
+      }
+      std::vector<Vec> vx, vu;
+      for (int k = 0; k <= n; ++k) vx.emplace_back(xs + (i * (n + 1) + k) * nx, xs + (i * (n + 1) + k + 1) * nx);
+      for (int k = 0; k < n; ++k) vu.emplace_back(us + (i * n + k) * nu, us + (i * n + k + 1) * nu);
+      std::vector<std::int8_t> w;
+      if (warm) w.assign(warm + i * nv, warm + (i + 1) * nv);
+      bool all_free = true;
+      for (auto v : w) all_free = all_free && v == 0;
+      if (all_free) w.clear();  // an all-zero hint is "no warm start" on both sides
+      FeedbackResult fb;
+      int st = 0;
+      try {
+        fb = SolveFeedback(d, Vec(x_meas + i * nx, x_meas + (i + 1) * nx), vx, vu, &w);
+        st = fb.status == QpStatus::kOptimal ? 0 : 1;
+      } catch (const std::exception&) {
+        st = 2;
+      }
+      status[i] = st;
+      iterations[i] = st == 2 ? 0 : fb.qp_iterations;
+      if (st == 2) continue;
+      if (warm)
+        for (int j = 0; j < nv; ++j) warm[i * nv + j] = static_cast<signed char>(w.empty() ? 0 : w[j]);
+      for (int k = 0; k <= n; ++k) std::copy(fb.dxs[k].begin(), fb.dxs[k].end(), dxs + (i * (n + 1) + k) * nx);
+      for (int k = 0; k < n; ++k) std::copy(fb.dus[k].begin(), fb.dus[k].end(), dus + (i * n + k) * nu);
+      std::copy(fb.u_command.begin(), fb.u_command.end(), u_cmd + i * nu);
+    }
+    return 0;
+  } catch (const oracle::ConfigError& e) {
+    g_cl_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_cl_err = e.what();
+    return 6;
+  }
+}
+
+}  // extern "C"

@@ -24,7 +24,7 @@ EXPORTS = (
     "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info",
     "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
     "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_last_error",
-    "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp",
+    "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp", "rtn_solve_feedback",
 )
 
 
@@ -52,6 +52,11 @@ class ApproxC(C.Structure):
 
 class QpBlocksC(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag", "du_lb", "du_ub")]
+
+
+class FeedbackC(C.Structure):
+    _fields_ = [("dxs", C.c_void_p), ("dus", C.c_void_p), ("u_command", C.c_void_p), ("status", C.c_void_p),
+                ("iterations", C.c_void_p), ("active", C.c_void_p)]
 
 _lib = None
 
@@ -94,6 +99,8 @@ def lib() -> C.CDLL:
                                       C.POINTER(IterateC), C.POINTER(ApproxC), C.POINTER(QpBlocksC)]
     L.rtn_cycle_qp.argtypes = [_vp, C.POINTER(QuadParamsC), C.POINTER(OcpConfigC), C.c_longlong,
                                C.POINTER(IterateC), C.POINTER(QpBlocksC), _vp, _vp, _vp]
+    L.rtn_solve_feedback.argtypes = [_vp, C.POINTER(OcpConfigC), C.c_longlong, C.POINTER(QpBlocksC), _vp,
+                                     C.POINTER(IterateC), C.POINTER(FeedbackC)]
     L.rtn_make_mlp.argtypes = [_ip, C.c_int, C.c_ulonglong, C.POINTER(_dp), C.POINTER(_dp)]
     L.rtn_synth_quad_nodes.argtypes = [C.c_ulonglong, C.c_longlong, _dp]
     L.rtn_synth_quad_nodes.restype = None

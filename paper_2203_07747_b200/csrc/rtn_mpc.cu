@@ -19,6 +19,7 @@
 
 #include "../../include/rtn_mpc.h"
 #include "rtn_blocks.h"
+#include "rtn_qpsolve.h"
 #include "rtn_fused.cuh"
 #include "rtn_launch.h"
 
@@ -189,6 +190,11 @@ struct rtn_ctx {
   size_t qin_cap = 0, qout_cap = 0, hqin_cap = 0, hqout_cap = 0;  // doubles
   unsigned long long* d_bad = nullptr;
   unsigned long long* h_bad = nullptr;
+  // feedback solve workspace (grown on demand)
+  double* d_fb = nullptr;
+  size_t fb_cap = 0;  // doubles
+  char* d_fb_small = nullptr;
+  size_t fb_small_cap = 0;  // bytes (status, iterations, active)
   unsigned char* h_status = nullptr;  // zero-copy latency mode: per-node status bytes
   long long status_cap = 0;
   struct QpGraph {
@@ -224,6 +230,8 @@ struct rtn_ctx {
       cudaFreeHost(h_qout);
       cudaFree(d_bad);
       cudaFreeHost(h_bad);
+      cudaFree(d_fb);
+      cudaFree(d_fb_small);
       cudaFreeHost(h_status);
       cudaSetDevice(prev);
     }
@@ -1387,3 +1395,89 @@ rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_conf
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Batched feedback solve (resmpc::SolveFeedback, sqp_rti.cpp:157-180).
+extern "C" rtn_status rtn_solve_feedback(rtn_ctx* c, const rtn_ocp_config* cfg, long long n_inst,
+                                         const rtn_qp_blocks* qp, const double* x_measured, const rtn_iterate* it,
+                                         rtn_feedback* out) {
+  return Guard([&] {
+    if (!cfg) throw Error(RTN_ECONFIG, "null argument");
+    if (cfg->horizon < 1) throw Error(RTN_ECONFIG, "qp data: bad dimensions");
+    if (cfg->horizon > 64) throw Error(RTN_EUNSUPPORTED, "feedback solve: horizon above 64 (N·nu > 256)");
+    if (!c || !qp || !x_measured || !it || !out) throw Error(RTN_ECONFIG, "null argument");
+    if (n_inst < 0) throw Error(RTN_EDOMAIN, "n_inst must be >= 0");
+    const int N = cfg->horizon, nv = 4 * N;
+    if (n_inst == 0) return;
+    if (!qp->a || !qp->b || !qp->phi_res || !qp->q || !qp->r || !qp->hx_diag || !qp->hu_diag || !qp->du_lb ||
+        !qp->du_ub || !it->xs || !it->us || !out->dxs || !out->dus || !out->u_command || !out->status)
+      throw Error(RTN_ECONFIG, "null buffer");
+    CUDA_CHECK(cudaSetDevice(c->model->device));
+    const size_t K = static_cast<size_t>(n_inst) * N, X = static_cast<size_t>(n_inst) * (N + 1) * 13;
+    QpPlan plan;  // doubles in, doubles out; ints/chars travel separately
+    const size_t o_a = plan.add_in(qp->a, K * 169), o_b = plan.add_in(qp->b, K * 52),
+                 o_phi = plan.add_in(qp->phi_res, K * 13), o_q = plan.add_in(qp->q, X), o_r = plan.add_in(qp->r, K * 4),
+                 o_hx = plan.add_in(qp->hx_diag, X), o_hu = plan.add_in(qp->hu_diag, K * 4),
+                 o_lb = plan.add_in(qp->du_lb, K * 4), o_ub = plan.add_in(qp->du_ub, K * 4),
+                 o_xm = plan.add_in(x_measured, static_cast<size_t>(n_inst) * 13), o_xs = plan.add_in(it->xs, X),
+                 o_us = plan.add_in(it->us, K * 4);
+    const size_t o_dxs = plan.add_out(out->dxs, X), o_dus = plan.add_out(out->dus, K * 4),
+                 o_u = plan.add_out(out->u_command, static_cast<size_t>(n_inst) * 4);
+    const int grid = static_cast<int>(std::min<long long>(n_inst, 2LL * c->num_sms));
+    const size_t work = static_cast<size_t>(grid) * static_cast<size_t>(rtn::FeedbackWorkPerCta(N));
+    Grow(&c->d_fb, &c->fb_cap, plan.in_total + plan.out_total + work, false);
+    const size_t small = static_cast<size_t>(n_inst) * (2 * sizeof(int) + nv);
+    if (small > c->fb_small_cap) {
+      cudaFree(c->d_fb_small);
+      c->d_fb_small = nullptr;
+      c->fb_small_cap = 0;
+      CUDA_CHECK(cudaMalloc(&c->d_fb_small, small));
+      c->fb_small_cap = small;
+    }
+    Grow(&c->h_qin, &c->hqin_cap, plan.in_total, true);
+    Grow(&c->h_qout, &c->hqout_cap, plan.out_total + 1, true);
+    for (const Slice& sl : plan.in) std::memcpy(c->h_qin + sl.off, sl.src, sl.n * sizeof(double));
+    double* din = c->d_fb;
+    double* dout = din + plan.in_total;
+    int* d_status = reinterpret_cast<int*>(c->d_fb_small);
+    int* d_iters = d_status + n_inst;
+    signed char* d_act = reinterpret_cast<signed char*>(d_iters + n_inst);
+    cudaStream_t s = c->stream;
+    CUDA_CHECK(cudaMemcpyAsync(din, c->h_qin, plan.in_total * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (out->active)
+      CUDA_CHECK(cudaMemcpyAsync(d_act, out->active, static_cast<size_t>(n_inst) * nv, cudaMemcpyHostToDevice, s));
+    rtn::FbParams p{};
+    p.a = din + o_a;
+    p.b = din + o_b;
+    p.phi = din + o_phi;
+    p.q = din + o_q;
+    p.r = din + o_r;
+    p.hx = din + o_hx;
+    p.hu = din + o_hu;
+    p.lb = din + o_lb;
+    p.ub = din + o_ub;
+    p.x_meas = din + o_xm;
+    p.xs = din + o_xs;
+    p.us = din + o_us;
+    p.active = out->active ? d_act : nullptr;
+    p.dxs = dout + o_dxs;
+    p.dus = dout + o_dus;
+    p.u_cmd = dout + o_u;
+    p.status = d_status;
+    p.iterations = d_iters;
+    p.work = dout + plan.out_total;
+    p.n_inst = n_inst;
+    p.N = N;
+    CUDA_CHECK(rtn::LaunchFeedback(p, grid, s));
+    c->launches += 1;
+    CUDA_CHECK(cudaMemcpyAsync(c->h_qout, dout, plan.out_total * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(out->status, d_status, static_cast<size_t>(n_inst) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (out->iterations)
+      CUDA_CHECK(cudaMemcpyAsync(out->iterations, d_iters, static_cast<size_t>(n_inst) * sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    if (out->active)
+      CUDA_CHECK(cudaMemcpyAsync(out->active, d_act, static_cast<size_t>(n_inst) * nv, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (const Slice& sl : plan.out) std::memcpy(sl.dst, c->h_qout + sl.off, sl.n * sizeof(double));
+  });
+}

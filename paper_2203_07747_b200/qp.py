@@ -201,6 +201,11 @@ class QpBuilder:
         self._keep = (xs, us, rx, ru, ax)
         return xs, us, rx, ru, _lib.IterateC(_ptr(xs), _ptr(us), _ptr(rx), _ptr(ru), _ptr(ax))
 
+    def solve_feedback(self, cfg: OcpConfig, qpd: QpData, x_measured, xs, us, active=None) -> FeedbackResult:
+        """SolveFeedback (sqp_rti.cpp:157-180) for every instance on the device:
+        condensing + box QP + recovery. `active` (n_inst x 4N) seeds the working set."""
+        return _solve_feedback(self.engine, cfg, qpd, x_measured, xs, us, active)
+
     def build_qp(self, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, approxes, aux=None) -> QpData:
         """BuildQp in rtn mode from prepared approximations (sqp_rti.cpp:59-155).
         aux: per-node 3x3 height patches (row-major, n_inst x N x 9), ground variant only."""
@@ -243,6 +248,41 @@ class QpBuilder:
         if return_approx:
             return qp, {"f_bar": f, "jac": jac, "hess": hess}
         return qp
+
+
+@dataclass
+class FeedbackResult:
+    """resmpc::FeedbackResult (sqp_rti.hpp:61-68), batched: status 0 optimal,
+    1 iteration cap, 2 SolveFeedback threw, 3 not positive definite."""
+    dxs: np.ndarray        # n_inst x (N+1) x 13
+    dus: np.ndarray        # n_inst x N x 4
+    u_command: np.ndarray  # n_inst x 4
+    status: np.ndarray     # n_inst
+    iterations: np.ndarray
+    active: np.ndarray     # n_inst x 4N working set (the next call's warm start)
+
+
+def _solve_feedback(engine, cfg: OcpConfig, qpd: QpData, x_measured, xs, us, active=None) -> FeedbackResult:
+    n = int(cfg.horizon)
+    xs = _batched(xs, (n + 1, NX), "iterate xs")
+    us = _batched(us, (n, NU), "iterate us")
+    xm = np.ascontiguousarray(np.reshape(x_measured, (-1, NX)), dtype=np.float64)
+    n_inst = xs.shape[0]
+    if xm.shape[0] != n_inst:
+        raise ConfigError("feedback: one measured state per instance")
+    arrs = [np.ascontiguousarray(np.reshape(getattr(qpd, nm), (n_inst, -1)), dtype=np.float64) for nm in _QP_FIELDS]
+    qc = _lib.QpBlocksC(*[_ptr(a) for a in arrs])
+    dxs, dus, u = np.empty((n_inst, n + 1, NX)), np.empty((n_inst, n, NU)), np.empty((n_inst, NU))
+    st, it = np.empty(n_inst, dtype=np.int32), np.empty(n_inst, dtype=np.int32)
+    act = (np.zeros((n_inst, n * NU), dtype=np.int8) if active is None
+           else np.ascontiguousarray(np.reshape(active, (n_inst, n * NU)), dtype=np.int8).copy())
+    out = _lib.FeedbackC(_ptr(dxs), _ptr(dus), _ptr(u), st.ctypes.data, it.ctypes.data, act.ctypes.data)
+    itc = _lib.IterateC(_ptr(xs), _ptr(us), None, None, None)
+    engine._ensure(1, 1)
+    cc = cfg.to_c()
+    raise_for_status(_lib.lib().rtn_solve_feedback(engine.ctx_ptr, C.byref(cc), n_inst, C.byref(qc), _ptr(xm),
+                                                   C.byref(itc), C.byref(out)))
+    return FeedbackResult(dxs, dus, u, st, it, act)
 
 
 def build_qp(model: MlpModel, params: QuadParams, cfg: OcpConfig, xs, us, ref_xs, ref_us, approxes,
