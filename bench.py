@@ -285,6 +285,36 @@ def cfg4_bench(torch, tf32_peak, steps=5):
     return out
 
 
+def feedback_bench():
+    """§8f rank 4: the batched feedback solve (csrc/rtn_qpsolve.cu: condensing + primal
+    active-set box QP + recovery, fp64) through rtn_solve_feedback (host buffers in and out),
+    on QpData from the oracle's BuildQp of quadrotor iterates; the oracle's SolveFeedback on
+    one host core beside it."""
+    import sys as _sys
+    _sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import oracle
+    import test_gpu_feedback as T
+    out = {}
+    for n_inst, n in ((4096, 20), (1024, 50)):
+        cfg, qpd, qd, xm, xs, us, om = T._setup(n_inst, n, seed=1)
+        b = T._builder(om)
+        b.solve_feedback(cfg, qpd, xm, xs, us)
+        t0 = time.perf_counter()
+        r = b.solve_feedback(cfg, qpd, xm, xs, us)
+        t = time.perf_counter() - t0
+        ns = 32
+        t1 = time.perf_counter()
+        oracle.solve_feedback(n, {k: v[:ns] for k, v in qd.items() if k != "f_evals"}, xm[:ns], xs[:ns], us[:ns])
+        tc = time.perf_counter() - t1
+        out[f"N{n}"] = {"value": n_inst / t, "unit": "instances/s", "instances": n_inst, "ms": t * 1e3,
+                        "mean_active_set_passes": float(r.iterations.mean()),
+                        "path": "rtn_solve_feedback (C-ABI), host QpData in, steps/commands out",
+                        "cpu_baseline": {"value": ns / tc, "unit": "instances/s", "cores": 1, "kind": "port",
+                                         "sample": f"{ns} instances in {tc:.2f} s"}}
+    return out
+
+
 def _quad_iterate(np, n_inst, n, seed):
     rng = np.random.default_rng(seed)
     xs = np.empty((n_inst, n + 1, 13))
@@ -597,6 +627,7 @@ def run_ours(args, rank, world, local_rank):
             result["cfg4"] = cfg4
         if blocks:
             result["blocks"] = blocks
+            result["feedback"] = feedback_bench()
     if world > 1:
         dist.barrier(device_ids=[local_rank])
         dist.destroy_process_group()
