@@ -287,31 +287,41 @@ def cfg4_bench(torch, tf32_peak, steps=5):
 
 def feedback_bench():
     """§8f rank 4: the batched feedback solve (csrc/rtn_qpsolve.cu: condensing + primal
-    active-set box QP + recovery, fp64) through rtn_solve_feedback (host buffers in and out),
-    on QpData from the oracle's BuildQp of quadrotor iterates; the oracle's SolveFeedback on
-    one host core beside it."""
-    import sys as _sys
-    _sys.path.insert(0, os.path.join(ROOT, "tests"))
+    active-set box QP + recovery, fp64) through rtn_solve_feedback (host buffers in and
+    out). QpData come from the product's own BuildQp (rtn_build_qp) on synthetic
+    quadrotor iterates and approximations; the oracle's SolveFeedback on one host core
+    is timed beside it (cpu_baseline)."""
     import numpy as np
     import oracle
-    import test_gpu_feedback as T
+    from paper_2203_07747_b200 import make_mlp, qp
     out = {}
     for n_inst, n in ((4096, 20), (1024, 50)):
-        cfg, qpd, qd, xm, xs, us, om = T._setup(n_inst, n, seed=1)
-        b = T._builder(om)
+        xs, us, rx, ru = _quad_iterate(np, n_inst, n, 1)
+        rng = np.random.default_rng(2)
+        k = n_inst * n
+        z0 = np.concatenate([xs[:, :n], us], axis=-1).reshape(k, 17)
+        fb, jac = rng.normal(0, 0.5, (k, 6)), rng.normal(0, 0.1, (k, 6, 17))
+        xm = xs[:, 0, :] + rng.normal(0, 0.1, (n_inst, 13))
+        cfg = qp.OcpConfig(horizon=n, dt=0.05, q_diag=np.array([10, 10, 10, 1, 1, 1, 1, 1, 1, 1, .1, .1, .1]),
+                           r_diag=np.full(4, 0.1), u_min=np.zeros(4), u_max=np.full(4, 6.0))
+        b = qp.QpBuilder(make_mlp([17, 64, 6], "silu", "full", 1))
+        qpd = b.build_qp(qp.QuadParams(), cfg, xs, us, rx, ru, {"z0": z0, "f_bar": fb, "jac": jac})
         b.solve_feedback(cfg, qpd, xm, xs, us)
         t0 = time.perf_counter()
         r = b.solve_feedback(cfg, qpd, xm, xs, us)
         t = time.perf_counter() - t0
         ns = 32
+        sub = {f: getattr(qpd, f)[:ns] for f in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag", "du_lb", "du_ub")}
         t1 = time.perf_counter()
-        oracle.solve_feedback(n, {k: v[:ns] for k, v in qd.items() if k != "f_evals"}, xm[:ns], xs[:ns], us[:ns])
+        oracle.solve_feedback(n, sub, xm[:ns], xs[:ns], us[:ns])
         tc = time.perf_counter() - t1
         out[f"N{n}"] = {"value": n_inst / t, "unit": "instances/s", "instances": n_inst, "ms": t * 1e3,
+                        "optimal": int((r.status == 0).sum()),
                         "mean_active_set_passes": float(r.iterations.mean()),
                         "path": "rtn_solve_feedback (C-ABI), host QpData in, steps/commands out",
                         "cpu_baseline": {"value": ns / tc, "unit": "instances/s", "cores": 1, "kind": "port",
                                          "sample": f"{ns} instances in {tc:.2f} s"}}
+        b.engine.close()
     return out
 
 

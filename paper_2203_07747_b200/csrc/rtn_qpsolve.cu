@@ -97,6 +97,9 @@ __device__ void CholSolve(const double* L, int nf, int ld, double* y) {
   }
 }
 
+// SMEM_L: the Cholesky factor of the free subproblem lives in shared memory
+// (N <= 32), which removes its O(nf³) inner-product traffic from L2.
+template <bool SMEM_L>
 __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
   extern __shared__ double dyn[];
   const int N = p.N, nv = N * kNu;
@@ -104,13 +107,14 @@ __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
   double* Mn = M + kNx * nv;    // 13 x nv
   double* c = Mn + kNx * nv;    // 13
   double* cn = c + 16;          // 13
-  int* fidx = reinterpret_cast<int*>(cn + 16);            // nv
-  signed char* act = reinterpret_cast<signed char*>(fidx + nv);  // nv
+  double* Ls = cn + 16;         // nv x nv (SMEM_L)
+  int* fidx = reinterpret_cast<int*>(Ls + (SMEM_L ? nv * nv : 0));  // nv
+  signed char* act = reinterpret_cast<signed char*>(fidx + nv);      // nv
   __shared__ Shared sh;
   double* W = p.work + static_cast<long long>(blockIdx.x) * FeedbackWorkPerCta(N);
   double* H = W;               // nv x nv
-  double* L = H + nv * nv;     // nv x nv (free subproblem, row stride nv)
-  double* g = L + nv * nv;
+  double* L = SMEM_L ? Ls : H + nv * nv;  // nv x nv (free subproblem, row stride nv)
+  double* g = H + 2 * nv * nv;             // vectors follow both matrices in the global workspace
   double* x = g + nv;
   double* y = x + nv;          // free-subproblem solution / rhs
   double* lb = y + nv;
@@ -352,15 +356,24 @@ size_t FeedbackSmemBytes(int N) {
 
 cudaError_t LaunchFeedback(const FbParams& p, int grid, cudaStream_t s) {
   if (p.n_inst <= 0) return cudaSuccess;
-  const size_t smem = FeedbackSmemBytes(p.N);
-  static size_t attr = 0;
-  if (smem > attr) {
-    const cudaError_t e = cudaFuncSetAttribute(FeedbackKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem));
+  const size_t nv = static_cast<size_t>(p.N) * kNu;
+  const size_t base = FeedbackSmemBytes(p.N), with_l = base + sizeof(double) * nv * nv;
+  const bool smem_l = with_l <= 200 * 1024;
+  const size_t smem = smem_l ? with_l : base;
+  static size_t attr[2] = {0, 0};
+  if (smem > attr[smem_l]) {
+    const cudaError_t e =
+        smem_l ? cudaFuncSetAttribute(FeedbackKernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem))
+               : cudaFuncSetAttribute(FeedbackKernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[smem_l] = smem;
   }
-  FeedbackKernel<<<grid, kT, smem, s>>>(p);
+  if (smem_l)
+    FeedbackKernel<true><<<grid, kT, smem, s>>>(p);
+  else
+    FeedbackKernel<false><<<grid, kT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
