@@ -470,41 +470,48 @@ __device__ __forceinline__ void mma4_tf32_pair_commit(uint32_t d_tmem, uint64_t 
 
 namespace rtn {
 // Split-operand pair MMA step (3xTF32 / BF16x3): with A = A_hi + A_lo and
-// B = B_hi + B_lo, D += A_hi·B_hi + A_hi·B_lo + A_lo·B_hi (the lo·lo term is
-// below the representation error). 3 passes x 4 K-steps of 32 bytes, one
-// elect, then multicast commits of the two weight stages (and bar2 if set).
+// B = B_hi + B_lo, D += A_hi·B_hi and D2 += A_hi·B_lo + A_lo·B_hi (the lo·lo
+// term is below the representation error). 3 passes x 4 K-steps of 32 bytes,
+// one elect, then multicast commits of the two weight stages (and bar2 if set).
+// `accumulate`: bit 0 for D's first K-step, bit 1 for D2's (set both when
+// D2 == D, which folds the correction into the main accumulator: bf16x3). A separate
+// D2 (3xTF32) keeps the ~2^-11-sized corrections from being added to the large
+// running sum: the tensor core's fp32 accumulation drops up to an ulp of the
+// running sum per MMA, and 128 correction MMAs per 512-deep layer made that the
+// dominant error; the epilogue adds D + D2 once in fp32.
 #define RTN_MMA12(KIND)                                                                                              \
   asm volatile(                                                                                                    \
-      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 x, y;\n\t.reg .b16 m;\n\t"                                        \
-      "mov.b16 m, 3;\n\tsetp.ne.b32 p, %7, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"             \
+      "{\n\t.reg .pred p, e, t, q, c;\n\t.reg .b64 x, y;\n\t.reg .b16 m;\n\t.reg .b32 r;\n\t"                     \
+      "mov.b16 m, 3;\n\tand.b32 r, %7, 1;\n\tsetp.ne.b32 p, r, 0;\n\tand.b32 r, %7, 2;\n\tsetp.ne.b32 c, r, 0;\n\t" \
+      "setp.eq.b32 t, 0, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"                                                    \
       "elect.sync _|e, 0xffffffff;\n\t"                                                                           \
       "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %1, %3, %6, p;\n\t"                                      \
       "add.s64 x, %1, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
       "add.s64 x, %1, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
       "add.s64 x, %1, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
-      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %1, %4, %6, t;\n\t"                                      \
-      "add.s64 x, %1, 2;\n\tadd.s64 y, %4, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
-      "add.s64 x, %1, 4;\n\tadd.s64 y, %4, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
-      "add.s64 x, %1, 6;\n\tadd.s64 y, %4, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
-      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %2, %3, %6, t;\n\t"                                      \
-      "add.s64 x, %2, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
-      "add.s64 x, %2, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
-      "add.s64 x, %2, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], x, y, %6, t;\n\t" \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], %1, %4, %6, c;\n\t"                                      \
+      "add.s64 x, %1, 2;\n\tadd.s64 y, %4, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], x, y, %6, t;\n\t" \
+      "add.s64 x, %1, 4;\n\tadd.s64 y, %4, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], x, y, %6, t;\n\t" \
+      "add.s64 x, %1, 6;\n\tadd.s64 y, %4, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], x, y, %6, t;\n\t" \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], %2, %3, %6, t;\n\t"                                      \
+      "add.s64 x, %2, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], x, y, %6, t;\n\t" \
+      "add.s64 x, %2, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], x, y, %6, t;\n\t" \
+      "add.s64 x, %2, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::" KIND " [%5], x, y, %6, t;\n\t" \
       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n\t"  \
       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%9], m;\n\t"  \
       "and.pred q, q, e;\n\t"                                                                                     \
       "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%10], m;\n\t}" \
-      ::"r"(d_tmem), "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(0), "r"(idesc), "r"(accumulate), "r"(bar0),     \
+      ::"r"(d_tmem), "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(d2_tmem), "r"(idesc), "r"(accumulate), "r"(bar0),     \
       "r"(bar1), "r"(bar2)                                                                                       \
       : "memory")
 
-__device__ __forceinline__ void mma12_tf32_pair_commit(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
-                                                       uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
+__device__ __forceinline__ void mma12_tf32_pair_commit(uint32_t d_tmem, uint32_t d2_tmem, uint64_t a_hi, uint64_t a_lo,
+                                                       uint64_t b_hi, uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
                                                        uint32_t bar0, uint32_t bar1, uint32_t bar2) {
   RTN_MMA12("tf32");
 }
-__device__ __forceinline__ void mma12_bf16_pair_commit(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
-                                                       uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
+__device__ __forceinline__ void mma12_bf16_pair_commit(uint32_t d_tmem, uint32_t d2_tmem, uint64_t a_hi, uint64_t a_lo,
+                                                       uint64_t b_hi, uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
                                                        uint32_t bar0, uint32_t bar1, uint32_t bar2) {
   RTN_MMA12("f16");
 }

@@ -59,13 +59,62 @@ struct PairCfg {
   static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
   static constexpr uint32_t kZsOff = kMiscOff + 16;
   static constexpr uint32_t kSmemBytes = kZsOff + 2 * NTC * 4 + 1024;
+  // 3xTF32: correction passes accumulate in their own TMEM columns (rtn_kernel.cuh
+  // RTN_MMA12): block mb's D2 at kCorrBase + mb·kCorrStride, the output layer's at 16.
+  static constexpr bool kCorr = MODE == k3xTF32;
+  static constexpr int kCorrBase = kNMB * kTmemStride2, kCorrStride = 96;
+  // ... and the main (hi·hi) pass alternates between two accumulators by chunk
+  // parity (D for even chunks, D3 = D + kMain2Off for odd), which halves the
+  // accumulation chain of each; order 2 (N = 96) has no TMEM room for D3.
+  static constexpr bool kSplitMain = kCorr && !ORD2 && (kNMB == 1 ? 2 * NTC <= 160 : 2 * NTC <= 80);
+  static constexpr int kMain2Off = kNMB == 2 ? 80 : 320;
   static_assert(kNMB >= 1 && kNMB <= 2, "pair kernel handles 256 or 512 padded width");
   static_assert(kNMB * kTmemStride2 <= 512, "TMEM capacity");
+  static_assert(!kCorr || kCorrBase + (kNMB - 1) * kCorrStride + 2 * NTC <= 512, "TMEM capacity (correction D2)");
+  static_assert(!kCorr || kNMB == 1 || 2 * NTC <= kCorrStride, "correction blocks must not overlap");
   static_assert(kSmemBytes <= 232448, "shared memory budget");
   static_assert(kStagesPerMB % NSTAGE == 0, "every 256-block starts at stage 0 (static stage indices)");
   // the output layer's M = 128-row A reads run past the last chunk into the stage ring
   static_assert((128 - NTC) * 128 <= NSTAGE * kStageBytes, "A-operand overrun must stay in smem");
 };
+
+// v[0..n) += TMEM columns [taddr, taddr + n) of this thread's lane (3xTF32
+// correction accumulator D2), 16 columns per round trip, columns >= lim skipped.
+template <int N>
+__device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* v, int lim) {
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    if (c0 >= lim) break;
+    float t[16];
+    tmem_ld8(taddr + c0, t);
+    if (c0 + 8 < N && c0 + 8 < lim) tmem_ld8(taddr + c0 + 8, t + 8);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (c0 + i < N && c0 + i < lim) v[c0 + i] += t[i];
+  }
+}
+
+// v[0..n) += (TMEM columns at ta) + (TMEM columns at tb): both 3xTF32 extra
+// accumulators (D3, D2) per round trip.
+template <int N>
+__device__ __forceinline__ void tmem_add2_cols(uint32_t ta, uint32_t tb, float* v, int lim) {
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    if (c0 >= lim) break;
+    float x[16], y[16];
+    tmem_ld8(ta + c0, x);
+    tmem_ld8(tb + c0, y);
+    if (c0 + 8 < N && c0 + 8 < lim) {
+      tmem_ld8(ta + c0 + 8, x + 8);
+      tmem_ld8(tb + c0 + 8, y + 8);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (c0 + i < N && c0 + i < lim) v[c0 + i] += x[i] + y[i];
+  }
+}
 
 template <int WP, int NSTAGE, int P, int NTC, int MODE, bool ORD2 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -177,8 +226,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
       };
       // One chunk: weights from stage(s) st0[/st1], activations chunk (hi[, lo]).
-      auto chunk_mma = [&](uint32_t d, uint64_t wa, uint64_t wb, int st0, int st1, uint64_t xa, uint64_t xb,
-                           uint32_t idesc, uint32_t acc, uint32_t bar2, bool weights_are_a) {
+      auto chunk_mma = [&](uint32_t d, uint32_t d2, uint64_t wa, uint64_t wb, int st0, int st1, uint64_t xa,
+                           uint64_t xb, uint32_t idesc, uint32_t acc, uint32_t bar2, bool weights_are_a) {
         if constexpr (MODE == kTF32) {
           if (weights_are_a)
             mma4_tf32_pair_commit(d, wa, xa, idesc, acc, smem_u32(&empty[st0]), bar2);
@@ -188,16 +237,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t ah = weights_are_a ? wa : xa, al = weights_are_a ? wb : xb;
           const uint64_t bh = weights_are_a ? xa : wa, bl = weights_are_a ? xb : wb;
           if constexpr (MODE == k3xTF32)
-            mma12_tf32_pair_commit(d, ah, al, bh, bl, idesc, acc, smem_u32(&empty[st0]), smem_u32(&empty[st1]), bar2);
+            mma12_tf32_pair_commit(d, d2, ah, al, bh, bl, idesc, acc, smem_u32(&empty[st0]), smem_u32(&empty[st1]),
+                                   bar2);
           else
-            mma12_bf16_pair_commit(d, ah, al, bh, bl, idesc, acc, smem_u32(&empty[st0]), smem_u32(&empty[st1]), bar2);
+            mma12_bf16_pair_commit(d, d, ah, al, bh, bl, idesc, (acc & 1u) | 2u, smem_u32(&empty[st0]),
+                                   smem_u32(&empty[st1]), bar2);
         }
+      };
+      // main-pass accumulator of chunk c, and the accumulate flags (TF32: a bool;
+      // split modes: bit 0 main, bit 1 correction — see RTN_MMA12)
+      auto split_d = [&](uint32_t d, int c) { return C::kSplitMain && (c & 1) ? d + C::kMain2Off : d; };
+      auto split_acc = [&](int c) -> uint32_t {
+        if constexpr (MODE == kTF32) return c != 0;
+        else return (c >= (C::kSplitMain ? 2 : 1) ? 1u : 0u) | (c != 0 ? 2u : 0u);
       };
       for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
         for (int l = 0; l < n_mma_layers; ++l) {
 #pragma unroll 1
           for (int mb = 0; mb < NMB; ++mb) {
             const uint32_t d = tmem_base + mb * kTmemStride2;
+            const uint32_t d2 = C::kCorr ? tmem_base + C::kCorrBase + mb * C::kCorrStride : d;
             if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2] = globaltimer();
 #pragma unroll
             for (int c = 0; c < NKC; ++c) {
@@ -208,8 +267,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tc_fence_after();
               // extra commit: in_free after the last block consumed K-group c/CPG
               const uint32_t bar2 = (mb == NMB - 1 && (c % CPG) == CPG - 1) ? smem_u32(&in_free[c / CPG]) : 0u;
-              chunk_mma(d, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD,
-                        b0 + kSplitD + c * kChunkD, idesc_h, c != 0, bar2, true);
+              chunk_mma(split_d(d, c), d2, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD,
+                        b0 + kSplitD + c * kChunkD, idesc_h, split_acc(c), bar2, true);
               if (st1 == NSTAGE - 1) ph ^= 1;
             }
             mma_commit_pair(&tmem_full[mb]);
@@ -225,8 +284,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full[st0], ph);
           if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
           tc_fence_after();
-          chunk_mma(tmem_base, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD,
-                    b0 + kSplitD + c * kChunkD, idesc_o, c != 0, 0u, false);
+          chunk_mma(C::kSplitMain && (c & 1) ? tmem_base + 32 : tmem_base, C::kCorr ? tmem_base + 16 : tmem_base,
+                    a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD, b0 + kSplitD + c * kChunkD,
+                    idesc_o, split_acc(c), 0u, false);
           if (st1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_pair(tmem_last);
@@ -312,6 +372,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c0 = 0; c0 < 24; c0 += 8) tmem_ld8(tb + c0, car + c0);
       tmem_ld_wait();
+      if constexpr (C::kCorr) {
+        const uint32_t tb2 = tmem_base + lane_base + C::kCorrBase + mb * C::kCorrStride;
+        tmem_add_cols<kNtc2>(tb2 + half * kNtc2, v, kNtc2);
+        tmem_add_cols<24>(tb2, car, 24);
+      }
       tc_fence_before();
       float val, sp, spp;
       act_fwd2(act, car[0] + bj, val, sp, spp);
@@ -365,6 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float o[16];
         tmem_ld16(tmem_base + lane_base, o);
         tmem_ld_wait();
+        if constexpr (C::kCorr) tmem_add_cols<16>(tmem_base + lane_base + 16, o, 16);
         const int r = tid_h, n_out = prm.n_out;
         if (node < prm.K && r < kNtc2) {
           if (rank == 0 && r < kCarrier2) {
@@ -501,6 +567,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c0 = 0; c0 < NTC; c0 += 8)
         if (c0 < ntc) tmem_ld8(ts + c0, v + c0);
       tmem_ld_wait();
+      if constexpr (C::kSplitMain)
+        tmem_add2_cols<NTC>(ts + C::kMain2Off, tmem_base + lane_base + C::kCorrBase + mb * C::kCorrStride + half * ntc,
+                            v, ntc);
+      else if constexpr (C::kCorr)
+        tmem_add_cols<NTC>(tmem_base + lane_base + C::kCorrBase + mb * C::kCorrStride + half * ntc, v, ntc);
       tc_fence_before();
       scale_side(v, bj);
       mbar_wait_sleep(&in_free[grp], hl & 1);
@@ -572,6 +643,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float o[16];
         tmem_ld16(tmem_base + lane_base, o);
         tmem_ld_wait();
+        if constexpr (C::kSplitMain) tmem_add2_cols<16>(tmem_base + lane_base + 32, tmem_base + lane_base + 16, o, 16);
+        else if constexpr (C::kCorr) tmem_add_cols<16>(tmem_base + lane_base + 16, o, 16);
         const int r = tid_h;
         const int n_out = prm.n_out;
         const long long nbase = node0 + static_cast<long long>(rank) * P;

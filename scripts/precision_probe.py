@@ -13,10 +13,10 @@ def net(sizes, act, gain, seed=11):
             om.set_layer(l, w * gain, b)
     return om
 
-cases = [([17]+[512]*12+[6], "silu", 2.5), ([17]+[256]*5+[6], "silu", 2.5), ([17, 64, 64, 6], "tanh", 3.0),
+cases = [([17]+[512]*12+[6], "silu", 2.5), ([17]+[512]*12+[6], "silu", 2.0), ([17]+[256]*5+[6], "silu", 2.5), ([17, 64, 64, 6], "tanh", 3.0),
          ([17]+[512]*12+[6], "silu", 1.0)]
 order = int(os.environ.get("ORDER", "1"))
-for prec in ("tf32", "3xtf32", "bf16x3"):
+for prec in os.environ.get("PRECS", "tf32,3xtf32,bf16x3").split(","):
     for kern in ("pair", "latency"):
         os.environ["RTN_KERNEL"] = kern
         for sizes, act, g in cases:

@@ -3,10 +3,18 @@ are O(1); 1/√fan_in-initialised deep nets are nearly constant and would hide
 operand-rounding error). Metric: ‖a−b‖∞/(1+‖b‖∞) per node and block, max
 over nodes (proj/tests/oracles.hpp:30-32) vs the fp64 oracle.
 
-Measured on B200 (scripts/precision_probe.py):
-  tf32   : 12x512 2.2e-3, 5x256 2.3e-3, 2x64 4e-4   (1e-3 bound NOT met on deep conditioned nets)
-  bf16x3 : 12x512 6e-5,   5x256 2e-5,   2x64 5e-6   (1e-3 class, ~20x margin)
-  3xtf32 : 12x512 7e-5,   5x256 1e-5,   2x64 1e-6   (1e-5 on the cfg4 shape)
+Measured on B200 (scripts/precision_probe.py), max over f, A, B:
+                 12x512 g2.0  12x512 g2.5  5x256 g2.5  2x64 tanh g3
+  tf32   :       3.4e-5       2.2e-3       2.3e-3      4.4e-4
+  bf16x3 :       1.4e-6       6.0e-5       2.0e-5      5.0e-6
+  3xtf32 :       2.8e-7       1.2e-5       2.1e-6      2.3e-7
+Gain 2.5 at depth 12 is the edge of the net's stable regime: 1e-7 relative
+noise on every activation moves f by 6e-7 there and by 8e-9 at gain 2.0 (numpy
+fp64 check; plain numpy fp32 reaches 1.2e-6 at gain 2.5), so the north-star
+bounds (1e-3 tf32/bf16, 1e-5 3xtf32) are asserted at gain 2.0 and the gain-2.5
+figures are regression guards. 3xTF32 accumulates its correction passes and the
+odd chunks of its main pass in separate TMEM accumulators (rtn_pair.cuh kCorr,
+kSplitMain): 7e-5 -> 1.2e-5 at 12x512 g2.5.
 """
 import os
 
@@ -41,9 +49,10 @@ def _err(om, prec, k, kernel, monkeypatch):
 CASES = [
     # (sizes, act, gain, {prec: bound})
     ([17] + [256] * 5 + [6], "silu", 2.0, {"3xtf32": 1e-5, "bf16x3": 1e-4}),   # cfg4 shape
-    ([17] + [256] * 5 + [6], "silu", 2.5, {"3xtf32": 2e-5, "bf16x3": 1e-4}),
-    ([17] + [512] * 12 + [6], "silu", 2.5, {"3xtf32": 2e-4, "bf16x3": 2e-4}),  # cfg3/cfg5 shape
-    ([17, 64, 64, 6], "tanh", 3.0, {"3xtf32": 1e-5, "bf16x3": 2e-5}),          # cfg1 shape
+    ([17] + [256] * 5 + [6], "silu", 2.5, {"3xtf32": 5e-6, "bf16x3": 1e-4}),
+    ([17] + [512] * 12 + [6], "silu", 2.0, {"3xtf32": 1e-5, "bf16x3": 1e-5}),  # cfg3/cfg5 shape
+    ([17] + [512] * 12 + [6], "silu", 2.5, {"3xtf32": 3e-5, "bf16x3": 2e-4}),  # edge of stability
+    ([17, 64, 64, 6], "tanh", 3.0, {"3xtf32": 1e-6, "bf16x3": 2e-5}),          # cfg1 shape
 ]
 
 
@@ -57,9 +66,11 @@ def test_split_modes_on_conditioned_nets(prec, case, kernel, monkeypatch):
 
 
 def test_tf32_documented_bound_on_conditioned_nets(monkeypatch):
-    """Single-pass TF32 keeps < 1e-3 on shallow nets; deep conditioned nets
-    reach ~2e-3 (recorded limitation) — guard against regression."""
+    """Single-pass TF32 keeps < 1e-3 on shallow nets and on 12x512 at gain 2.0;
+    at gain 2.5 (edge of stability) it reaches ~2e-3 (recorded limitation,
+    DESIGN.md §4) — guard against regression."""
     assert _err(_net([17, 64, 64, 6], "tanh", 3.0), "tf32", 64, "pair", monkeypatch) < 1e-3
+    assert _err(_net([17] + [512] * 12 + [6], "silu", 2.0), "tf32", 64, "pair", monkeypatch) < 1e-4
     assert _err(_net([17] + [512] * 12 + [6], "silu", 2.5), "tf32", 64, "pair", monkeypatch) < 5e-3
 
 
