@@ -547,6 +547,12 @@ Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
                        K <= 2 * (num_sms / 4);
   if (const char* e = std::getenv("RTN_KERNEL"))
     if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
+  // rows (rtn_rows.cuh): selected inside the pair branch of Enqueue for TF32 width-256 throughput
+  const bool rows_ok = m->has_pair && m->pair_mode == rtn::kTF32 && m->pair_wp == 256 &&
+                       m->n_in >= rtn::kRowsMinIn && m->n_in <= rtn::kRowsMaxInHost &&
+                       m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
+  if (const char* e = std::getenv("RTN_KERNEL"))
+    if (std::strcmp(e, "rows") == 0 && rows_ok) return Kern::kPair;
   if (quad_ok && !std::getenv("RTN_KERNEL")) {
     const char* q = std::getenv("RTN_QUAD");
     if (!(q && q[0] == '0')) return Kern::kQuad;
@@ -641,7 +647,18 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
     cudaError_t e;
     const char* pp = std::getenv("RTN_PINGPONG");
-    if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && prm.P == 4 && m->n_in <= rtn::kMaxIn0 &&
+    const char* rw = std::getenv("RTN_ROWS");
+    const char* fk = std::getenv("RTN_KERNEL");
+    if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && m->n_in >= rtn::kRowsMinIn &&
+        m->n_in <= rtn::kRowsMaxInHost && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost && !(rw && rw[0] == '0') &&
+        !(fk && std::strcmp(fk, "pair") == 0)) {
+      // width 256: activations as the A operand in TMEM (rtn_rows.cuh), 128 rows per CTA
+      prm.P = 128 / (1 + m->n_in);
+      prm.nt = 128;
+      prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);
+      const int g3 = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+      e = rtn::LaunchRowsTF32(prm, m->tmap_h, m->tmap_l, g3, c->stream);
+    } else if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && prm.P == 4 && m->n_in <= rtn::kMaxIn0 &&
         !(pp && pp[0] == '0')) {
       // width 256: two tiles in flight per CTA pair (rtn_pingpong.cuh)
       const long long tile_pairs = (prm.num_tiles + 1) / 2;

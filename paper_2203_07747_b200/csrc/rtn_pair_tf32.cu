@@ -2,6 +2,7 @@
 #include "rtn_pair_launch.cuh"
 #include "rtn_pingpong.cuh"
 #include "rtn_quad.cuh"
+#include "rtn_rows.cuh"
 
 namespace rtn {
 
@@ -51,6 +52,20 @@ cudaError_t LaunchPingPongTF32(const KParams& prm, const CUtensorMap& th, const 
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
+  }
+  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
+  return cudaGetLastError();
+}
+
+cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
+  using Cfg = RowsCfg<6>;
+  auto kern = prm.act == 0 ? rtn_rows_kernel<6, 0> : (prm.act == 1 ? rtn_rows_kernel<6, 1> : rtn_rows_kernel<6, 2>);
+  static bool attr_set[3] = {false, false, false};
+  const int a = prm.act < 0 || prm.act > 2 ? 2 : prm.act;
+  if (!attr_set[a]) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[a] = true;
   }
   kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
   return cudaGetLastError();

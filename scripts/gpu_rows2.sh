@@ -1,0 +1,3 @@
+timeout 60 python scripts/trace_rows.py 2>&1 | tail -12
+RTN_KERNEL=rows timeout 90 python -m pytest tests/test_gpu_parity.py -q -x -k "rows" 2>&1 | tail -2
+timeout 120 python scripts/perf_probe.py 2>&1 | sed -n 1,3p

@@ -15,11 +15,12 @@ TF32_TOL = 1e-3
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["single", "pair", "pingpong", "latency", "quad"])
+@pytest.fixture(params=["single", "pair", "pingpong", "latency", "quad", "rows"])
 def kernel(request, monkeypatch):
     """Every device kernel: single-CTA, CTA-pair throughput (P=4; width 256 uses the two-tile
-    ping-pong variant unless RTN_PINGPONG=0), CTA-pair latency (P=1) and the 4-CTA-cluster latency
-    kernel (width-512 TF32 models, K <= 2·(#SMs/4); others fall back)."""
+    ping-pong variant unless RTN_PINGPONG=0), CTA-pair latency (P=1), the 4-CTA-cluster latency
+    kernel (width-512 TF32 models, K <= 2·(#SMs/4); others fall back) and the width-256
+    rows kernel (activations as the MMA's A operand in TMEM; width 512 falls back)."""
     if request.param == "pingpong":
         monkeypatch.setenv("RTN_KERNEL", "pair")
         monkeypatch.setenv("RTN_PINGPONG", "1")
@@ -129,3 +130,33 @@ def test_pingpong_width256_matches_pair_kernel_bitwise(monkeypatch):
         assert np.array_equal(outs[0].values, outs[1].values) and np.array_equal(outs[0].jacobians, outs[1].jacobians)
         f, j, _ = om.batched_eval(z, 1)
         assert max_node_rel_error(outs[0].jacobians, j) < TF32_TOL
+
+
+def test_rows_kernel_input_widths_and_ragged_tiles(monkeypatch):
+    """rtn_rows.cuh: R = 1 + n_in rows per node, 128 // R nodes per CTA — the
+    quadrotor 'full' (17 → 7 nodes), 'a_u' (7 → 16), 'ground' (26 → 4) and the
+    widest supported input (31 → 4); K around the tile size (2·NPC per pair),
+    one node, and more tiles than CTA pairs; hidden widths below 256 (zero padding)."""
+    monkeypatch.setenv("RTN_KERNEL", "rows")
+    for k in (1, 13, 14, 15, 4099):
+        _check([17] + [256] * 5 + [6], "silu", k)
+    _check([7, 256, 256, 3], "silu", 777)
+    _check([26, 256, 192, 3], "silu", 1000)
+    _check([31, 100, 256, 256, 6], "tanh", 501)
+    _check([17, 256, 6], "relu", 300)  # one hidden layer: no MMA layer before the output
+
+
+def test_rows_kernel_default_for_width256_throughput(monkeypatch):
+    """Without RTN_KERNEL a TF32 width-256 batch above the latency regime runs the
+    rows kernel; its rows are bit-identical to single-node calls forced onto it."""
+    from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
+    om = OracleModel.random_net([17] + [256] * 5 + [6], "silu", 37)
+    z = quad_nodes(6, 3000)
+    monkeypatch.delenv("RTN_KERNEL", raising=False)
+    full = mlp_batched_eval(to_product_model(om), z, EvalOrder.JACOBIAN)
+    f, j, _ = om.batched_eval(z, 1)
+    assert max_node_rel_error(full.values, f) < TF32_TOL and max_node_rel_error(full.jacobians, j) < TF32_TOL
+    monkeypatch.setenv("RTN_KERNEL", "rows")
+    for i in (0, 6, 7, 13, 2999):
+        one = mlp_batched_eval(to_product_model(om), z[i:i + 1], EvalOrder.JACOBIAN)
+        assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
