@@ -279,6 +279,8 @@ def cfg4_bench(torch, tf32_peak, steps=5):
         ms = e0.elapsed_time(e1) / steps
         ach = k * fl / (ms * 1e-3) / 1e12
         out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": ach,
+                     "kernel": ("rtn_rows_kernel (activations as the A operand in TMEM, M = 256 rows x N = 256)"
+                                if name == "tf32" else "rtn_pair_kernel<256,4,4,80,3xTF32> (split accumulators)"),
                      "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
                      "hardware_frac": (3 if name == "3xtf32" else 1) * ach / tf32_peak if tf32_peak else None}
         eng.close()

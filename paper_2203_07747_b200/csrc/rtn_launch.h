@@ -39,7 +39,7 @@ cudaError_t LaunchPingPongTF32(const KParams& prm, const CUtensorMap& th, const 
 // (rtn_rows.cuh): TF32, order <= 1, 7 <= n_in <= 31, prm.P = 128 / (1 + n_in)
 // nodes per CTA, grid = 2 x pairs.
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
-constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 16;
+constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 11;
 
 // Order 2 (value + Jacobian + Hessian; n_in = 17): two pair-tiles per node.
 cudaError_t LaunchPairOrder2(int mode, const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp,

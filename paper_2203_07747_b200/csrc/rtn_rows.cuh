@@ -47,7 +47,7 @@ namespace rtn {
 constexpr int kRowsMaxIn = 31;     // R = 1 + n_in <= 32 → NPC >= 4
 constexpr int kRowsMaxNodes = 16;  // table capacity: R >= 8 → n_in >= 7
 constexpr int kRowsTabStride = 260;  // floats per node row of the σ/σ' tables (bank spread)
-constexpr int kRowsMaxMma = 16;      // hidden→hidden layers whose biases fit the smem copy
+constexpr int kRowsMaxMma = 11;      // hidden→hidden layers whose biases fit the smem copy
 
 template <int NSTAGE>
 struct RowsCfg {
@@ -56,10 +56,11 @@ struct RowsCfg {
   static constexpr uint32_t kW0Off = kStageOff + NSTAGE * kStageBytes;        // 256 x n_in fp32
   static constexpr uint32_t kPreOff = kW0Off + 256 * kRowsMaxIn * 4;                     // [16][260] pre
   static constexpr uint32_t kTabOff = kPreOff + kRowsMaxNodes * kRowsTabStride * 4;      // [16][2][260] σ, σ'
-  static constexpr uint32_t kZsOff = kTabOff + kRowsMaxNodes * 2 * kRowsTabStride * 4;   // [16][32] z
-  static constexpr uint32_t kBhOff = kZsOff + kRowsMaxNodes * 32 * 4;                      // [16][256] hidden biases
+  static constexpr uint32_t kTab0Off = kTabOff + kRowsMaxNodes * 2 * kRowsTabStride * 4; // [16][2][260] layer-0 σ, σ'
+  static constexpr uint32_t kZsOff = kTab0Off + kRowsMaxNodes * 2 * kRowsTabStride * 4;  // [16][32] z
+  static constexpr uint32_t kBhOff = kZsOff + kRowsMaxNodes * 32 * 4;                      // [11][256] hidden biases
   static constexpr uint32_t kBarOff = kBhOff + kRowsMaxMma * 256 * 4;
-  static constexpr uint32_t kNumBars = 2 * NSTAGE + 8 + 2;
+  static constexpr uint32_t kNumBars = 2 * NSTAGE + 16 + 2;
   static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
   static constexpr uint32_t kSmemBytes = kMiscOff + 16 + 1024;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
@@ -154,13 +155,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   float* w0s = reinterpret_cast<float*>(smem + C::kW0Off);
   float* pre_t = reinterpret_cast<float*>(smem + C::kPreOff);
   float* tab = reinterpret_cast<float*>(smem + C::kTabOff);
+  float* tab0 = reinterpret_cast<float*>(smem + C::kTab0Off);
   float* zs = reinterpret_cast<float*>(smem + C::kZsOff);
   float* bhs = reinterpret_cast<float*>(smem + C::kBhOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
-  uint64_t* act = bars + 2 * NSTAGE;  // [8] 32-column K-chunks of the A region being written
-  uint64_t* tmem_full = act + 8;
+  // act[s][c]: K-chunk c (32 columns) of A production k is in TMEM, s = k & 1.
+  // Two sets so that the next tile's layer 0, published while the MMA warp may
+  // still be waiting on the output layer's chunks, never laps a waiter.
+  uint64_t* act = bars + 2 * NSTAGE;
+  uint64_t* tmem_full = act + 16;
   uint64_t* tmem_last = tmem_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kMiscOff);
 
@@ -176,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int g = 0; g < 8; ++g) mbar_init(&act[g], 16);  // 8 epilogue warps x 2 CTAs
+    for (int g = 0; g < 16; ++g) mbar_init(&act[g], 16);  // 8 epilogue warps x 2 CTAs
     mbar_init(tmem_full, 1);
     mbar_init(tmem_last, 1);
     fence_barrier_init();
@@ -207,15 +212,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ph ^= 1;
       }
     };
+    // K-chunk order: the first MMA layer of a tile (the consumer of layer 0)
+    // takes chunks 1..7 then 0, because chunk 0 shares columns with the
+    // previous tile's output-layer accumulator (see the epilogue)
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
       for (int l = 0; l < n_mma; ++l)
-        for (int c = 0; c < NKC; ++c) {
+        for (int i = 0; i < NKC; ++i) {
+          const int c = l == 0 ? (i + 1) & (NKC - 1) : i;
           mbar_wait(&empty[st], ph ^ 1);
           if (leader) mbar_expect_tx_elect(&full[st], 2 * kStageBytes);
           tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * 32, l * 256 + yr, &full[st], pol);
           next();
         }
-      for (int c = 0; c < NKC; ++c) {
+      for (int i = 0; i < NKC; ++i) {
+        const int c = n_mma == 0 ? (i + 1) & (NKC - 1) : i;
         mbar_wait(&empty[st], ph ^ 1);
         if (leader) mbar_expect_tx_elect(&full[st], 2 * 1024);
         tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * 32, static_cast<int>(rank) * 8, &full[st], pol);
@@ -228,35 +238,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t idesc_h = idesc_tf32(256, 256), idesc_o = idesc_tf32(256, kMaxOut);
       const uint64_t b0 = sw128_desc(smem_u32(stage_s));
       constexpr uint32_t kStageD = kStageBytes >> 4;
-      uint32_t ph = 0, ar = 0;
+      uint32_t ph = 0, cons = 0;
       int st = 0;
       long long tix = 0;
-      auto layer = [&](uint32_t a_reg, uint32_t d_reg, uint32_t idesc, int li) {
+      auto layer = [&](uint32_t a_reg, uint32_t d_reg, uint32_t idesc, int li, bool first) {
         unsigned long long* tp = (prm.trace && pair == 0 && tix < 2 && li < 8 && lane == 0) ? prm.trace + tix * 24 + li * 3 : nullptr;
         if (tp) tp[0] = globaltimer();
+        uint64_t* a_set = act + 8 * (cons & 1);
+        const uint32_t par = (cons >> 1) & 1;
 #pragma unroll 1
-        for (int c = 0; c < NKC; ++c) {
-          if (!(prm.dbg & 128)) mbar_wait(&act[c], ar & 1);  // dbg 128: weight stream + MMAs only
+        for (int i = 0; i < NKC; ++i) {
+          const int c = first ? (i + 1) & (NKC - 1) : i;
+          if (!(prm.dbg & 128)) mbar_wait(&a_set[c], par);  // dbg 128: weight stream + MMAs only
           tc_fence_after();
-          if (tp && c == 0) tp[1] = globaltimer();
+          if (tp && i == 0) tp[1] = globaltimer();
           mbar_wait(&full[st], ph);
           tc_fence_after();
-          mma4_tf32_pair_ts_commit(d_reg, a_reg + 32 * c, b0 + st * kStageD, idesc, c != 0, smem_u32(&empty[st]));
+          mma4_tf32_pair_ts_commit(d_reg, a_reg + 32 * c, b0 + st * kStageD, idesc, i != 0, smem_u32(&empty[st]));
           if (++st == NSTAGE) {
             st = 0;
             ph ^= 1;
           }
         }
         if (tp) tp[2] = globaltimer();
-        ++ar;
+        ++cons;
       };
+      // Region of a tile's layer-0 output alternates: the next tile's layer 0 is
+      // written into the region that holds this tile's output-layer accumulator.
+      int b = 0;
       for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tix) {
         for (int l = 0; l < n_mma; ++l) {
-          layer(tmem_base + (l & 1) * 256, tmem_base + ((l + 1) & 1) * 256, idesc_h, l);
+          layer(tmem_base + ((b + l) & 1) * 256, tmem_base + ((b + l + 1) & 1) * 256, idesc_h, l, l == 0);
           mma_commit_pair(tmem_full);
         }
-        layer(tmem_base + (n_mma & 1) * 256, tmem_base + ((n_mma + 1) & 1) * 256, idesc_o, n_mma);
+        layer(tmem_base + ((b + n_mma) & 1) * 256, tmem_base + ((b + n_mma + 1) & 1) * 256, idesc_o, n_mma, n_mma == 0);
         mma_commit_pair(tmem_last);
+        b = (b + n_mma + 1) & 1;
       }
     }
   } else if (warp >= 4 && (prm.dbg & 128)) {
@@ -277,7 +294,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool valid = p < npc;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t act_cl = mapa(smem_u32(act), 0);
-    const float* my_tab = tab + (valid ? p : 0) * 2 * kRowsTabStride + (j == 0 ? 0 : kRowsTabStride);
+    const int tab_row = (valid ? p : 0) * 2 * kRowsTabStride + (j == 0 ? 0 : kRowsTabStride);
+    const float* my_tab = tab + tab_row;
+    const float* my_tab0 = tab0 + tab_row;
     uint32_t hl = 0, tiles_done = 0;
 
     // RTN_TRACE fine stamps (clock64) of one layer's epilogue: pair 0, tile 1, layer 1 (warps 4 and 8)
@@ -292,39 +311,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (prm.trace && pair == 0 && tiles_done < 2 && L < 6 && q == 0 && lane == 0)
         prm.trace[64 + (((rank * 2 + h) * 2 + tiles_done) * 6 + L) * 3 + e] = globaltimer();
     };
+    uint32_t prod = 0;  // A productions published (layer 0 and every hidden layer)
     auto signal = [&](int c) {
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(act_cl + 8 * c);
+      if (lane == 0) mbar_arrive_remote(act_cl + 8 * (8 * (prod & 1) + c));
     };
     // Rewrite 16 columns [c0, c0 + 16) of region `reg` for this thread's row:
     // value rows σ(tab), tangent rows σ'(tab)·m with m the accumulator (hidden
     // layers) or W0'[:, j−1] (layer 0). Padding rows (p >= npc) read node 0's
     // table: finite, and rows are independent through every MMA, so they never
     // reach a stored output.
-    auto rewrite16 = [&](uint32_t reg, int c0, bool layer0) {
-      float t[16], m[16];
-      if (!layer0) tmem_ld16(reg + lane_base + c0, m);
+    // m: the accumulator columns, loaded (tcgen05.ld, asynchronous) by the caller.
+    auto finish16 = [&](uint32_t reg, int c0, const float (&m)[16]) {
+      float t[16];
 #pragma unroll
       for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(t + i) = *reinterpret_cast<const float4*>(my_tab + c0 + i);
-      if (layer0) {
-        const int jw = j > 0 ? j - 1 : 0;
+      tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) m[i] = w0s[(c0 + i) * n_in + jw];
-      } else {
-        tmem_ld_wait();
-      }
+      for (int i = 0; i < 16; ++i) t[i] = to_tf32(j == 0 ? t[i] : t[i] * m[i]);
+      tmem_st16(reg + lane_base + c0, t);
+    };
+    auto rewrite16_layer0 = [&](uint32_t reg, int c0) {
+      float t[16], m[16];
+      const int jw = j > 0 ? j - 1 : 0;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(t + i) = *reinterpret_cast<const float4*>(my_tab0 + c0 + i);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[i] = w0s[(c0 + i) * n_in + jw];
 #pragma unroll
       for (int i = 0; i < 16; ++i) t[i] = to_tf32(j == 0 ? t[i] : t[i] * m[i]);
       tmem_st16(reg + lane_base + c0, t);
     };
     // K-chunks c in [c_lo, c_hi) in MMA order: warp half h takes columns
     // 32c + 16h .. + 16 of every chunk, then the chunk is published.
-    auto rewrite_chunks = [&](uint32_t reg, int c_lo, int c_hi, bool layer0, int L) {
+    auto rewrite_chunks0 = [&](uint32_t reg, int c_lo, int c_hi, int L) {
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; ++c) {
-        rewrite16(reg, 32 * c + 16 * h, layer0);
+        rewrite16_layer0(reg, 32 * c + 16 * h);
         signal(c);
         if (c == 0) trace(L, 1);
         if (c == c_hi - 1) trace(L, 2);
@@ -379,75 +404,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const long long node = tile * (2 * npc) + static_cast<long long>(rank) * npc + zp;
       return (zown && tile < prm.num_tiles && node < prm.K) ? static_cast<float>(load_z(prm, node, zk)) : 0.0f;
     };
+    // Layer-0 σ, σ' tables of `tile` into tab0 (z staged from the register
+    // prefetch). Runs while the tensor core works on the previous tile's output
+    // layer, so the next tile's first K-chunk follows its output epilogue directly.
     float znext = fetch_z(pair);
-    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
-      const long long node0 = tile * (2 * npc) + static_cast<long long>(rank) * npc;
-      trace(0, 0);
-      // ---- layer 0 into R0 -------------------------------------------------
+    auto layer0_tables = [&](long long tile) {
       if (zown) zs[zp * 32 + zk] = znext;
       named_bar(3, 256);
       znext = fetch_z(tile + npairs);
-      {
-        const int n = etid;  // neuron
-        const float bj = __ldg(prm.b0 + n);
-        float w[kRowsMaxIn];
+      const int n = etid;  // neuron
+      const float bj = __ldg(prm.b0 + n);
+      float w[kRowsMaxIn];
 #pragma unroll
-        for (int k = 0; k < kRowsMaxIn; ++k) w[k] = k < n_in ? w0s[n * n_in + k] : 0.0f;
+      for (int k = 0; k < kRowsMaxIn; ++k) w[k] = k < n_in ? w0s[n * n_in + k] : 0.0f;
 #pragma unroll 1
-        for (int p0 = 0; p0 < npc; p0 += 4) {  // four independent chains per pass
-          float pre[4], val[4], sp[4];
+      for (int p0 = 0; p0 < npc; p0 += 4) {  // four independent chains per pass
+        float pre[4], val[4], sp[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) pre[u] = bj;
+        for (int u = 0; u < 4; ++u) pre[u] = bj;
 #pragma unroll
-          for (int k = 0; k < kRowsMaxIn; ++k)
-            if (k < n_in) {
+        for (int k = 0; k < kRowsMaxIn; ++k)
+          if (k < n_in) {
 #pragma unroll
-              for (int u = 0; u < 4; ++u) pre[u] = fmaf(w[k], zs[(p0 + u) * 32 + k], pre[u]);
-            }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) act_rows<ACT>(pre[u], val[u], sp[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            tab[(p0 + u) * 2 * kRowsTabStride + n] = val[u];
-            tab[(p0 + u) * 2 * kRowsTabStride + kRowsTabStride + n] = sp[u];
+            for (int u = 0; u < 4; ++u) pre[u] = fmaf(w[k], zs[(p0 + u) * 32 + k], pre[u]);
           }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) act_rows<ACT>(pre[u], val[u], sp[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          tab0[(p0 + u) * 2 * kRowsTabStride + n] = val[u];
+          tab0[(p0 + u) * 2 * kRowsTabStride + kRowsTabStride + n] = sp[u];
         }
       }
       named_bar(3, 256);
-      rewrite_chunks(tmem_base, 0, 8, true, 0);
-      // ---- hidden layers: D in R_{(l+1)%2}, rewritten in place. Two stages so
-      // that K-chunks 0-1 reach the MMA warp after only 64 columns of tables.
+    };
+    // Tables (values → σ, σ') of the hidden-layer columns [n_lo, n_lo + n_cnt)
+    // (n_cnt = 64 or 192; the value-row loads split over both halves' quadrant-0 warps).
+    auto table_stage = [&](uint32_t reg, int n_lo, int n_cnt, const float* bias) {
+      if (n_cnt == 64) {
+        if (h == 0) publish_values(reg, n_lo, 64);
+      } else {
+        if (h == 0) publish_values(reg, n_lo, 64);
+        else publish_values(reg, n_lo + 64, n_cnt - 64);
+      }
+      named_bar(3, 256);
+      sigma_cols(n_lo, n_cnt, bias);
+      named_bar(3, 256);
+    };
+    layer0_tables(pair);
+    rewrite_chunks0(tmem_base, 1, 8, 0);
+    rewrite_chunks0(tmem_base, 0, 1, 0);
+    ++prod;
+    int b = 0;  // region of this tile's layer-0 output (the MMA warp tracks the same)
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
+      const long long node0 = tile * (2 * npc) + static_cast<long long>(rank) * npc;
+      trace(0, 0);
+      // ---- hidden layers: D in R_{(b+l+1)%2}, rewritten in place. The tables of
+      // K-chunks c+2, c+3 are built while chunk c+1's accumulator load is in flight.
       for (int l = 0; l < n_mma; ++l, ++hl) {
-        const uint32_t reg = tmem_base + ((l + 1) & 1) * 256;
+        const uint32_t reg = tmem_base + ((b + l + 1) & 1) * 256;
         mbar_wait(tmem_full, hl & 1);
         tc_fence_after();
         trace(l + 1, 0);
         fl = l + 1;
         fine(fl, 0, 0);
         const float* bias = bhs + l * 256;
-        if (h == 0) publish_values(reg, 0, 64);
-        named_bar(3, 256);
+        table_stage(reg, 0, 64, bias);
         fine(fl, 0, 1);
-        sigma_cols(0, 64, bias);
-        named_bar(3, 256);
-        fine(fl, 0, 2);
-        rewrite_chunks(reg, 0, 2, false, l + 1);
+        {
+          float m[16];
+          tmem_ld16(reg + lane_base + 16 * h, m);
+          finish16(reg, 16 * h, m);
+          signal(0);
+          trace(l + 1, 1);
+          fine(fl, 0, 2);
+          tmem_ld16(reg + lane_base + 32 + 16 * h, m);  // chunk 1, in flight during the second table stage
+          table_stage(reg, 64, 192, bias);
+          finish16(reg, 32 + 16 * h, m);
+          signal(1);
+        }
+#pragma unroll 1
+        for (int c = 2; c < 8; ++c) {
+          const int c0 = 32 * c + 16 * h;
+          float m[16];
+          tmem_ld16(reg + lane_base + c0, m);
+          finish16(reg, c0, m);
+          signal(c);
+        }
+        ++prod;
+        trace(l + 1, 2);
         fine(fl, 0, 3);
-        if (h == 0) publish_values(reg, 64, 64);
-        else publish_values(reg, 128, 128);
-        named_bar(3, 256);
-        sigma_cols(64, 192, bias);
-        named_bar(3, 256);
-        fine(fl, 0, 4);
-        rewrite_chunks(reg, 2, 8, false, l + 1);
-        fine(fl, 0, 5);
       }
-      // ---- output layer: D_out in columns 0..15 of R_{(n_mma+1)%2} -----------
+      // ---- tile boundary. The output layer accumulates into columns 0..15 of
+      // R_nb (the last hidden layer's A region, free once that layer's MMAs
+      // completed); the next tile's layer 0 goes to the same region: its
+      // K-chunks 1..7 now, while the tensor core runs the output layer, and
+      // chunk 0 (columns 0..31) after the output accumulator has been read.
+      const int nb = (b + n_mma + 1) & 1;
+      const uint32_t reg_next = tmem_base + nb * 256;
+      const bool more = tile + npairs < prm.num_tiles;
+      if (more) {
+        layer0_tables(tile + npairs);
+        rewrite_chunks0(reg_next, 1, 8, 0);
+      }
       mbar_wait(tmem_last, tiles_done & 1);
       tc_fence_after();
       if (h == 0) {
         float o[16];
-        tmem_ld16(tmem_base + ((n_mma + 1) & 1) * 256 + lane_base, o);
+        tmem_ld16(reg_next + lane_base, o);
         tmem_ld_wait();
         const long long node = node0 + p;
         const int n_out = prm.n_out;
@@ -460,6 +524,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
+      if (more) {
+        named_bar(3, 256);  // the output accumulator has been read by both halves' rows
+        rewrite_chunks0(reg_next, 0, 1, 0);
+        ++prod;
+      }
+      b = nb;
     }
   }
   tc_fence_before();

@@ -30,6 +30,6 @@ for tix in range(2):
                 row.append(f"c{r}h{h} {rel(t[i]):7.3f}/{rel(t[i+1]):7.3f}/{rel(t[i+2]):7.3f}")
         print(f"tile {tix} epi L{L}: " + " | ".join(row))
 for h in range(2):
-    c = t[216 + h * 12: 216 + h * 12 + 6]
+    c = t[216 + h * 12: 216 + h * 12 + 4]
     print(f"fine h{h} (cycles from tmem_full seen): " + " ".join(f"{x - c[0]:.0f}" for x in c))
-print("  points: 0 full seen, 1 chunk 0-1 values+bar, 2 sigma+bar, 3 chunks 0-1 published, 4 rest values+sigma, 5 all published")
+print("  points: 0 full seen, 1 table stage 0, 2 chunk 0 published, 3 all published")
