@@ -54,72 +54,90 @@ __device__ void AdvanceRecovery(const FbParams& p, long long inst, int k, int nv
   }
 }
 
-// Left-looking Cholesky of the nf x nf matrix in L (row stride ld), in place:
-// column j: s_i = L(i,j) − Σ_{k<j} L(i,k)·L(j,k) (ascending k, as qp.cpp's LLT), L(j,j) = √s_j.
-// Returns false (for every thread) on a non-positive pivot.
-__device__ bool Cholesky(double* L, int nf, int ld, Shared& sh) {
+// Element (i, j), j <= i, of the free-subproblem factor: full rows of stride
+// ld (PACKED = false) or the packed lower triangle, row i at i(i+1)/2 (only the
+// lower triangle is ever read, so N = 50's 200 x 200 factor fits shared memory).
+template <bool PACKED>
+__device__ __forceinline__ int Lx(int i, int j, int ld) {
+  return PACKED ? ((i * (i + 1)) >> 1) + j : i * ld + j;
+}
+
+// Cholesky of the nf x nf matrix in L, in place, right-looking: after column
+// j is scaled, the trailing matrix takes the rank-1 update L(i,m) −= L(i,j)·L(m,j).
+// Each element therefore sees a(i,j) − l(i,0)l(j,0) − l(i,1)l(j,1) − … in
+// ascending k, the same operation sequence as qp.cpp's left-looking LLT, but
+// the work per column is spread over the CTA instead of one serial dot
+// product per row (the left-looking form's critical path grew as nf²).
+// Two barriers per column. Returns false (for every thread) on a non-positive pivot.
+template <bool PACKED>
+__device__ bool Cholesky(double* L, int nf, int ld, Shared&) {
   for (int j = 0; j < nf; ++j) {
-    for (int i = j + threadIdx.x; i < nf; i += kT) {
-      double s = L[i * ld + j];
-      for (int k = 0; k < j; ++k) s -= L[i * ld + k] * L[j * ld + k];
-      L[i * ld + j] = s;
-    }
+    const double d = L[Lx<PACKED>(j, j, ld)];
+    if (d <= 0.0) return false;  // every thread read the same pivot
+    const double ljj = sqrt(d);
+    for (int i = j + 1 + threadIdx.x; i < nf; i += kT) L[Lx<PACKED>(i, j, ld)] /= ljj;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const double d = L[j * ld + j];
-      if (d <= 0.0) sh.fail = 1;
-      else L[j * ld + j] = sqrt(d);
+    if (threadIdx.x == 0) L[Lx<PACKED>(j, j, ld)] = ljj;  // all threads have read the pivot
+    for (int i = j + 1 + (threadIdx.x >> 3); i < nf; i += kT / 8) {
+      const double lij = L[Lx<PACKED>(i, j, ld)];
+      double* li = L + Lx<PACKED>(i, 0, ld);
+      for (int m = j + 1 + (threadIdx.x & 7); m <= i; m += 8) li[m] -= lij * L[Lx<PACKED>(m, j, ld)];
     }
-    __syncthreads();
-    if (sh.fail) return false;
-    const double ljj = L[j * ld + j];
-    for (int i = j + 1 + threadIdx.x; i < nf; i += kT) L[i * ld + j] /= ljj;
     __syncthreads();
   }
   return true;
 }
 
-// Solve L·Lᵀ·y = b in place (column-oriented substitutions).
+// Solve L·Lᵀ·y = b in place (column-oriented substitutions) on warp 0; the
+// rest of the CTA waits at the closing barrier.
+template <bool PACKED>
 __device__ void CholSolve(const double* L, int nf, int ld, double* y) {
-  for (int i = 0; i < nf; ++i) {
-    if (threadIdx.x == 0) y[i] /= L[i * ld + i];
-    __syncthreads();
-    const double yi = y[i];
-    for (int m = i + 1 + threadIdx.x; m < nf; m += kT) y[m] -= L[m * ld + i] * yi;
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int i = 0; i < nf; ++i) {
+      if (lane == 0) y[i] /= L[Lx<PACKED>(i, i, ld)];
+      __syncwarp();
+      const double yi = y[i];
+      for (int m = i + 1 + lane; m < nf; m += 32) y[m] -= L[Lx<PACKED>(m, i, ld)] * yi;
+      __syncwarp();
+    }
+    for (int i = nf - 1; i >= 0; --i) {
+      if (lane == 0) y[i] /= L[Lx<PACKED>(i, i, ld)];
+      __syncwarp();
+      const double yi = y[i];
+      for (int m = lane; m < i; m += 32) y[m] -= L[Lx<PACKED>(i, m, ld)] * yi;
+      __syncwarp();
+    }
   }
-  for (int i = nf - 1; i >= 0; --i) {
-    if (threadIdx.x == 0) y[i] /= L[i * ld + i];
-    __syncthreads();
-    const double yi = y[i];
-    for (int m = threadIdx.x; m < i; m += kT) y[m] -= L[i * ld + m] * yi;
-    __syncthreads();
-  }
+  __syncthreads();
 }
 
-// SMEM_L: the Cholesky factor of the free subproblem lives in shared memory
-// (N <= 32), which removes its O(nf³) inner-product traffic from L2.
-template <bool SMEM_L>
+// LMODE: where the Cholesky factor of the free subproblem lives — 0 global
+// workspace, 1 shared memory (full rows, N <= 36), 2 shared memory (packed
+// lower triangle, N <= 51). Shared memory removes its O(nf³) inner-product
+// traffic from L2.
+template <int LMODE>
 __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
+  constexpr bool SMEM_L = LMODE != 0, PACKED = LMODE == 2;
   extern __shared__ double dyn[];
   const int N = p.N, nv = N * kNu;
   double* M = dyn;              // 13 x nv
   double* Mn = M + kNx * nv;    // 13 x nv
   double* c = Mn + kNx * nv;    // 13
   double* cn = c + 16;          // 13
-  double* Ls = cn + 16;         // nv x nv (SMEM_L)
-  int* fidx = reinterpret_cast<int*>(Ls + (SMEM_L ? nv * nv : 0));  // nv
+  double* g = cn + 16;          // the QP vectors (gradient, iterate, subproblem rhs/solution,
+  double* x = g + nv;           // bounds, full gradient) in shared memory: the scalar pivot
+  double* y = x + nv;           // loops of the active-set method run on one thread and were
+  double* lb = y + nv;          // latency-bound on L2 reads
+  double* ub = lb + nv;
+  double* grad = ub + nv;
+  double* Ls = grad + nv;       // nv x nv, or nv(nv+1)/2 packed (SMEM_L)
+  int* fidx = reinterpret_cast<int*>(Ls + (SMEM_L ? (PACKED ? (nv * (nv + 1)) / 2 : nv * nv) : 0));  // nv
   signed char* act = reinterpret_cast<signed char*>(fidx + nv);      // nv
   __shared__ Shared sh;
   double* W = p.work + static_cast<long long>(blockIdx.x) * FeedbackWorkPerCta(N);
   double* H = W;               // nv x nv
   double* L = SMEM_L ? Ls : H + nv * nv;  // nv x nv (free subproblem, row stride nv)
-  double* g = H + 2 * nv * nv;             // vectors follow both matrices in the global workspace
-  double* x = g + nv;
-  double* y = x + nv;          // free-subproblem solution / rhs
-  double* lb = y + nv;
-  double* ub = lb + nv;
-  double* grad = ub + nv;
 
   for (long long inst = blockIdx.x; inst < p.n_inst; inst += gridDim.x) {
     // ---------------- condensing (qp.cpp:33-73) ----------------
@@ -208,7 +226,7 @@ __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
         // hff and rhs = −g_f − Σ_{j active} H(f, j)·x_j (qp.cpp:77-92)
         for (int e = threadIdx.x; e < nf * nf; e += kT) {
           const int a = e / nf, b = e - a * nf;
-          L[a * nv + b] = H[fidx[a] * nv + fidx[b]];
+          if (b <= a) L[Lx<PACKED>(a, b, nv)] = H[fidx[a] * nv + fidx[b]];
         }
         for (int a = threadIdx.x; a < nf; a += kT) {
           double dot = 0.0;
@@ -218,7 +236,7 @@ __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
         }
         if (threadIdx.x == 0) sh.fail = 0;
         __syncthreads();
-        if (!Cholesky(L, nf, nv, sh)) {  // regularise once (qp.cpp:94-100)
+        if (!Cholesky<PACKED>(L, nf, nv, sh)) {  // regularise once (qp.cpp:94-100)
           if (threadIdx.x == 0) {
             double tr = 0.0;
             for (int a = 0; a < nf; ++a) tr += H[fidx[a] * nv + fidx[a]];
@@ -228,15 +246,15 @@ __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
           __syncthreads();
           for (int e = threadIdx.x; e < nf * nf; e += kT) {
             const int a = e / nf, b = e - a * nf;
-            L[a * nv + b] = H[fidx[a] * nv + fidx[b]] + (a == b ? sh.trace : 0.0);
+            if (b <= a) L[Lx<PACKED>(a, b, nv)] = H[fidx[a] * nv + fidx[b]] + (a == b ? sh.trace : 0.0);
           }
           __syncthreads();
-          if (!Cholesky(L, nf, nv, sh)) {
+          if (!Cholesky<PACKED>(L, nf, nv, sh)) {
             status = 3;  // not positive definite even after regularisation
             break;
           }
         }
-        CholSolve(L, nf, nv, y);
+        CholSolve<PACKED>(L, nf, nv, y);
         if (threadIdx.x == 0) {  // ratio test toward the subproblem solution (qp.cpp:150-170)
           double alpha = 1.0;
           int blocking = -1;
@@ -351,29 +369,25 @@ __global__ void __launch_bounds__(kT) FeedbackKernel(const FbParams p) {
 
 size_t FeedbackSmemBytes(int N) {
   const size_t nv = static_cast<size_t>(N) * kNu;
-  return sizeof(double) * (2 * kNx * nv + 32) + sizeof(int) * nv + nv + 16;
+  return sizeof(double) * (2 * kNx * nv + 32 + 6 * nv) + sizeof(int) * nv + nv + 16;
 }
 
 cudaError_t LaunchFeedback(const FbParams& p, int grid, cudaStream_t s) {
   if (p.n_inst <= 0) return cudaSuccess;
   const size_t nv = static_cast<size_t>(p.N) * kNu;
-  const size_t base = FeedbackSmemBytes(p.N), with_l = base + sizeof(double) * nv * nv;
-  const bool smem_l = with_l <= 200 * 1024;
-  const size_t smem = smem_l ? with_l : base;
-  static size_t attr[2] = {0, 0};
-  if (smem > attr[smem_l]) {
-    const cudaError_t e =
-        smem_l ? cudaFuncSetAttribute(FeedbackKernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem))
-               : cudaFuncSetAttribute(FeedbackKernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem));
+  const size_t base = FeedbackSmemBytes(p.N);
+  const size_t full = base + sizeof(double) * nv * nv, packed = base + sizeof(double) * (nv * (nv + 1) / 2);
+  constexpr size_t kCap = 220 * 1024;
+  const int mode = full <= kCap ? 1 : (packed <= kCap ? 2 : 0);
+  const size_t smem = mode == 1 ? full : (mode == 2 ? packed : base);
+  static size_t attr[3] = {0, 0, 0};
+  auto kern = mode == 1 ? FeedbackKernel<1> : (mode == 2 ? FeedbackKernel<2> : FeedbackKernel<0>);
+  if (smem > attr[mode]) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr[smem_l] = smem;
+    attr[mode] = smem;
   }
-  if (smem_l)
-    FeedbackKernel<true><<<grid, kT, smem, s>>>(p);
-  else
-    FeedbackKernel<false><<<grid, kT, smem, s>>>(p);
+  kern<<<grid, kT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
