@@ -62,28 +62,52 @@ __device__ __forceinline__ int Lx(int i, int j, int ld) {
   return PACKED ? ((i * (i + 1)) >> 1) + j : i * ld + j;
 }
 
-// Cholesky of the nf x nf matrix in L, in place, right-looking: after column
-// j is scaled, the trailing matrix takes the rank-1 update L(i,m) −= L(i,j)·L(m,j).
-// Each element therefore sees a(i,j) − l(i,0)l(j,0) − l(i,1)l(j,1) − … in
-// ascending k, the same operation sequence as qp.cpp's left-looking LLT, but
-// the work per column is spread over the CTA instead of one serial dot
-// product per row (the left-looking form's critical path grew as nf²).
-// Two barriers per column. Returns false (for every thread) on a non-positive pivot.
+// Cholesky of the nf x nf matrix in L, in place, right-looking in panels of
+// four columns: the panel is factored column by column, then the trailing
+// matrix takes the panel's rank-4 update with one read-modify-write per
+// element. Every element still sees a(i,j) − l(i,0)l(j,0) − l(i,1)l(j,1) − …
+// in ascending k, the operation sequence of qp.cpp's left-looking LLT, but the
+// work per column is spread over the CTA and the trailing matrix's shared-
+// memory traffic is a quarter of the unblocked form's (profiles/r01_ncu_feedback_n50.txt).
+// Returns false (for every thread) on a non-positive pivot.
 template <bool PACKED>
 __device__ bool Cholesky(double* L, int nf, int ld, Shared&) {
-  for (int j = 0; j < nf; ++j) {
-    const double d = L[Lx<PACKED>(j, j, ld)];
-    if (d <= 0.0) return false;  // every thread read the same pivot
-    const double ljj = sqrt(d);
-    for (int i = j + 1 + threadIdx.x; i < nf; i += kT) L[Lx<PACKED>(i, j, ld)] /= ljj;
-    __syncthreads();
-    if (threadIdx.x == 0) L[Lx<PACKED>(j, j, ld)] = ljj;  // all threads have read the pivot
-    for (int i = j + 1 + (threadIdx.x >> 3); i < nf; i += kT / 8) {
-      const double lij = L[Lx<PACKED>(i, j, ld)];
-      double* li = L + Lx<PACKED>(i, 0, ld);
-      for (int m = j + 1 + (threadIdx.x & 7); m <= i; m += 8) li[m] -= lij * L[Lx<PACKED>(m, j, ld)];
+  constexpr int kPw = 4;
+  for (int j0 = 0; j0 < nf; j0 += kPw) {
+    const int jw = min(kPw, nf - j0), pe = j0 + jw;
+    for (int j = j0; j < pe; ++j) {  // panel column j
+      const double d = L[Lx<PACKED>(j, j, ld)];
+      if (d <= 0.0) return false;  // every thread read the same pivot
+      const double ljj = sqrt(d);
+      for (int i = j + 1 + threadIdx.x; i < nf; i += kT) L[Lx<PACKED>(i, j, ld)] /= ljj;
+      __syncthreads();
+      if (threadIdx.x == 0) L[Lx<PACKED>(j, j, ld)] = ljj;  // all threads have read the pivot
+      const int nm = pe - (j + 1);  // panel columns right of j
+      if (nm > 0) {
+        for (int e = threadIdx.x; e < (nf - j - 1) * nm; e += kT) {
+          const int i = j + 1 + e / nm, m = j + 1 + e % nm;
+          if (i >= m) L[Lx<PACKED>(i, m, ld)] -= L[Lx<PACKED>(i, j, ld)] * L[Lx<PACKED>(m, j, ld)];
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (pe < nf) {  // trailing update, rows i >= m >= pe
+      for (int i = pe + (threadIdx.x >> 3); i < nf; i += kT / 8) {
+        double li[kPw];
+#pragma unroll
+        for (int t = 0; t < kPw; ++t) li[t] = t < jw ? L[Lx<PACKED>(i, j0 + t, ld)] : 0.0;
+        double* row = L + Lx<PACKED>(i, 0, ld);
+        for (int m = pe + (threadIdx.x & 7); m <= i; m += 8) {
+          const double* lm = L + Lx<PACKED>(m, j0, ld);
+          double s = row[m];
+#pragma unroll
+          for (int t = 0; t < kPw; ++t)
+            if (t < jw) s -= li[t] * lm[t];
+          row[m] = s;
+        }
+      }
+      __syncthreads();
+    }
   }
   return true;
 }
