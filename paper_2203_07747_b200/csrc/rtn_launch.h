@@ -29,6 +29,8 @@ cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CU
 // Latency kernel on 4-CTA clusters (rtn_quad.cuh): TF32, width 512, order <= 1,
 // one node per CTA side, grid = 4 x ceil(K / 2).
 cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
+cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
+                             cudaStream_t st);
 
 // Width-256 throughput kernel with two tiles in flight per CTA pair
 // (rtn_pingpong.cuh): TF32, order <= 1, P = 4 nodes per CTA side.

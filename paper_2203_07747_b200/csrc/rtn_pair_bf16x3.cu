@@ -1,5 +1,6 @@
 // Pair-kernel instantiations, BF16x3 mode (split hi/lo bf16 operands, 3 kind::f16 passes).
 #include "rtn_pair_launch.cuh"
+#include "rtn_quad.cuh"
 
 namespace rtn {
 
@@ -21,6 +22,20 @@ cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CU
     case 2: return LaunchPairT<512, 4, 2, 80, kBF16x3>(prm, th, tl, grid, st);
     default: return LaunchPairT<512, 4, 4, 80, kBF16x3>(prm, th, tl, grid, st);
   }
+}
+
+cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
+                             cudaStream_t st) {
+  using Cfg = PairCfg<512, 8, 1, 24, kBF16x3, false>;
+  auto kern = rtn_quad_kernel<8, 24, kBF16x3>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
+  return cudaGetLastError();
 }
 
 }  // namespace rtn

@@ -1,4 +1,5 @@
-// rtn_quad.cuh — latency kernel on 4-CTA clusters (two CTA pairs), TF32, order 1.
+// rtn_quad.cuh — latency kernel on 4-CTA clusters (two CTA pairs), order 1,
+// TF32 or bf16x3 (MODE; hi/lo operand split as in rtn_pair.cuh, 3 passes).
 //
 // Why: at one MPC step (K = N nodes) the pair kernel gives each 2-node
 // cluster the WHOLE weight stream; every SM pushes ~5.8 MB of 12x512 weights
@@ -52,6 +53,38 @@ __device__ __forceinline__ void mma4_tf32_pair_commit_m(uint32_t d_tmem, uint64_
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2), "r"(mask), "r"(mask2)
       : "memory");
 }
+// bf16x3 chunk (rtn_pair.cuh RTN_MMA12 with D2 == D) with masked multicast commits:
+// the two weight stages' empty barriers to `mask`, and `bar2` (if non-zero) to `mask2`.
+__device__ __forceinline__ void mma12_bf16_pair_commit_m(uint32_t d, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
+                                                         uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
+                                                         uint32_t bar0, uint32_t bar1, uint32_t mask, uint32_t bar2,
+                                                         uint32_t mask2) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 x, y;\n\t.reg .b16 m, m2;\n\t"
+      "cvt.u16.u32 m, %9;\n\tcvt.u16.u32 m2, %11;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "add.s64 x, %1, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "add.s64 x, %1, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "add.s64 x, %1, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, t;\n\t"
+      "add.s64 x, %1, 2;\n\tadd.s64 y, %4, 2;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "add.s64 x, %1, 4;\n\tadd.s64 y, %4, 4;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "add.s64 x, %1, 6;\n\tadd.s64 y, %4, 6;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, t;\n\t"
+      "add.s64 x, %2, 2;\n\tadd.s64 y, %3, 2;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "add.s64 x, %2, 4;\n\tadd.s64 y, %3, 4;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "add.s64 x, %2, 6;\n\tadd.s64 y, %3, 6;\n\t@e tcgen05.mma.cta_group::2.kind::f16 [%0], x, y, %5, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], m;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%10], m2;\n\t}" ::"r"(d),
+      "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate), "r"(bar0), "r"(bar1), "r"(mask),
+      "r"(bar2), "r"(mask2)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_mask(uint64_t* bar, uint32_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\t"
@@ -63,14 +96,16 @@ __device__ __forceinline__ void mma_commit_mask(uint64_t* bar, uint32_t mask) {
       : "memory");
 }
 
-template <int NSTAGE, int NTC>
+template <int NSTAGE, int NTC, int MODE = kTF32>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_quad_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
   constexpr int WP = 512, P = 1;
-  using C = PairCfg<WP, NSTAGE, P, NTC, kTF32, false>;
-  constexpr int NKC = C::kNKC, CPG = C::kCPG, NG = C::kNG;  // 16 chunks, 4 per group, 4 groups
-  static_assert(NG == 4 && NKC % NSTAGE == 0, "quad kernel: width 512, whole stage rings per layer");
+  static_assert(MODE == kTF32 || MODE == kBF16x3, "quad kernel: TF32 or bf16x3");
+  using C = PairCfg<WP, NSTAGE, P, NTC, MODE, false>;
+  // tf32: 16 chunks of 32 k, 4 per group; bf16: 8 chunks of 64 k, 2 per group; 4 groups
+  constexpr int NKC = C::kNKC, CPG = C::kCPG, NG = C::kNG, SPLIT = C::kSplit, EB = C::kEB;
+  static_assert(NG == 4 && (NKC * SPLIT) % NSTAGE == 0, "quad kernel: width 512, whole stage rings per layer");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* act_s = smem;
@@ -122,40 +157,59 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================== weight producer: this CTA's 128 rows of block pr ====
     const uint64_t pol = l2_evict_last_policy();
     uint32_t ph = 0;
+    // split modes stream the hi tile then the lo tile of each chunk (lo rows at prm.lo_rows)
     for (int l = 0; l < n_mma_layers; ++l) {
       const int y = l * WP + pr * 256 + sub * 128;
 #pragma unroll
-      for (int i = 0; i < NKC; ++i) {
-        const int c = (i + 2 * pr * CPG) % NKC, st = i % NSTAGE;  // rotated K order
+      for (int i = 0; i < NKC * SPLIT; ++i) {
+        const int c = (i / SPLIT + 2 * pr * CPG) % NKC, sp = i % SPLIT, st = i % NSTAGE;  // rotated K order
         mbar_wait(&empty[st], ph ^ 1);
         if (leader) mbar_expect_tx_elect(&full[st], 2 * kStageBytes);
-        tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * C::kCK, y, &full[st], pol);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_h, c * C::kCK, y + sp * prm.lo_rows, &full[st], pol);
         if (st == NSTAGE - 1) ph ^= 1;
       }
     }
     if (pr == 0) {
 #pragma unroll
-      for (int i = 0; i < NKC; ++i) {
-        const int st = i % NSTAGE;
+      for (int i = 0; i < NKC * SPLIT; ++i) {
+        const int c = i / SPLIT, sp = i % SPLIT, st = i % NSTAGE;
         mbar_wait(&empty[st], ph ^ 1);
         if (leader) mbar_expect_tx_elect(&full[st], 2 * kLastHalfBytes);
-        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, i * C::kCK, sub * 8, &full[st], pol);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * C::kCK, sp * 16 + sub * 8, &full[st], pol);
         if (st == NSTAGE - 1) ph ^= 1;
       }
     }
   } else if (warp == 1) {
     // ===================== pair MMA issuer (pair leaders: ranks 0 and 2) ======
     if (leader) {
-      const uint32_t idesc_h = idesc_tf32(256, 2 * ntc);
-      const uint32_t idesc_o = idesc_tf32(256, kMaxOut);
+      const uint32_t idesc_h = MODE == kBF16x3 ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_o = MODE == kBF16x3 ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
-      constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4;
+      constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4, kSplitD = C::kSplitStride >> 4;
       uint32_t ph = 0, ar = 0;
+      // one chunk: weights from stage st0 (hi) [and st0 + 1 (lo)], activations chunk c (hi [, lo])
+      auto chunk = [&](int st0, int c, uint32_t idesc, uint32_t acc, uint32_t bar2, uint32_t mask2, bool weights_are_a) {
+        const uint64_t wa = a0 + st0 * kStageD, xa = b0 + c * kChunkD;
+        if constexpr (MODE == kTF32) {
+          if (weights_are_a)
+            mma4_tf32_pair_commit_m(tmem_base, wa, xa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
+          else
+            mma4_tf32_pair_commit_m(tmem_base, xa, wa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
+        } else {
+          const uint64_t wb = wa + kStageD, xb = xa + kSplitD;
+          if (weights_are_a)
+            mma12_bf16_pair_commit_m(tmem_base, wa, wb, xa, xb, idesc, acc, smem_u32(&empty[st0]),
+                                     smem_u32(&empty[st0 + 1]), pair_mask, bar2, mask2);
+          else
+            mma12_bf16_pair_commit_m(tmem_base, xa, xb, wa, wb, idesc, acc, smem_u32(&empty[st0]),
+                                     smem_u32(&empty[st0 + 1]), pair_mask, bar2, mask2);
+        }
+      };
       for (int l = 0; l < n_mma_layers; ++l) {
 #pragma unroll
         for (int i = 0; i < NKC; ++i) {
-          const int c = (i + 2 * pr * CPG) % NKC, st = i % NSTAGE, g = c / CPG;
+          const int c = (i + 2 * pr * CPG) % NKC, st = (i * SPLIT) % NSTAGE, g = c / CPG;
           if (i == 0) {  // own groups first: inputs ready AND this pair's TMEM block drained
             mbar_wait_cluster(&act_ready[2 * pr], ar & 1);
             mbar_wait_cluster(&act_ready[2 * pr + 1], ar & 1);
@@ -165,11 +219,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           mbar_wait(&full[st], ph);
+          if constexpr (SPLIT == 2) mbar_wait(&full[st + 1], ph);
           tc_fence_after();
           const bool last_of_group = (c % CPG) == CPG - 1;
-          mma4_tf32_pair_commit_m(tmem_base, a0 + st * kStageD, b0 + c * kChunkD, idesc_h, i != 0,
-                                  smem_u32(&empty[st]), pair_mask, last_of_group ? smem_u32(&in_free[g]) : 0u, 0xFu);
-          if (st == NSTAGE - 1) ph ^= 1;
+          chunk(st, c, idesc_h, i != 0, last_of_group ? smem_u32(&in_free[g]) : 0u, 0xFu, true);
+          if (st + SPLIT - 1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_mask(&tmem_full[0], pair_mask);
         ++ar;
@@ -177,16 +231,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
       if (pr == 0) {  // output layer: D[row, o] = Σ_k X[row, k]·W_L'[o, k]; M = 2 x 128 rows, N = 16
 #pragma unroll
         for (int i = 0; i < NKC; ++i) {
-          const int st = i % NSTAGE;
+          const int st = (i * SPLIT) % NSTAGE;
           if ((i % CPG) == 0) {
             mbar_wait_cluster(&act_ready[i / CPG], ar & 1);
             tc_fence_after();
           }
           mbar_wait(&full[st], ph);
+          if constexpr (SPLIT == 2) mbar_wait(&full[st + 1], ph);
           tc_fence_after();
-          mma4_tf32_pair_commit_m(tmem_base, b0 + i * kChunkD, a0 + st * kStageD, idesc_o, i != 0,
-                                  smem_u32(&empty[st]), pair_mask, 0u, 0u);
-          if (st == NSTAGE - 1) ph ^= 1;
+          chunk(st, i, idesc_o, i != 0, 0u, 0u, false);
+          if (st + SPLIT - 1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_mask(tmem_last, pair_mask);
       }
@@ -200,7 +254,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const int act = prm.act;
     const int rows_used = P * (1 + n_in);
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    const int u = ((tid_h * 4) >> 4) & 7;
+    const int u = ((tid_h * EB) >> 4) & 7;
     int swz[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) swz[i] = ((u ^ i) - u) * 16 + i * 128;
@@ -212,14 +266,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     const int grp = static_cast<int>(rank);  // K-group this CTA produces
 
     auto store_side = [&](const float* v, int j) {
-      const uint32_t off = (j / C::kCK) * C::kChunkStride + (((j % C::kCK) * 4) >> 4 << 4) + ((j * 4) & 15);
+      const uint32_t off = (j / C::kCK) * C::kChunkStride + (((j % C::kCK) * EB) >> 4 << 4) + ((j * EB) & 15);
 #pragma unroll
       for (int i = 0; i < NTC; ++i) {
         if ((i & ~7) >= ntc) continue;
         const uint32_t a = off + (i >> 3) * 1024 + swz[i & 7];
-        const float h = to_tf32(v[i]);
-        st_cluster_f32(dst0 + a, h);
-        st_cluster_f32(dst1 + a, h);
+        if constexpr (MODE == kTF32) {
+          const float h = to_tf32(v[i]);
+          st_cluster_f32(dst0 + a, h);
+          st_cluster_f32(dst1 + a, h);
+        } else {  // bf16 hi and lo (rtn_pair.cuh store_side)
+          const uint16_t h = bf16_rn_bits(v[i]);
+          const uint16_t lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
+          st_cluster_u16(dst0 + a, h);
+          st_cluster_u16(dst1 + a, h);
+          st_cluster_u16(dst0 + a + C::kSplitStride, lo);
+          st_cluster_u16(dst1 + a + C::kSplitStride, lo);
+        }
       }
     };
     auto publish = [&]() {

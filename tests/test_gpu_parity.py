@@ -160,3 +160,23 @@ def test_rows_kernel_default_for_width256_throughput(monkeypatch):
     for i in (0, 6, 7, 13, 2999):
         one = mlp_batched_eval(to_product_model(om), z[i:i + 1], EvalOrder.JACOBIAN)
         assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
+
+
+def test_quad_kernel_bf16x3_bitwise_and_ragged(monkeypatch):
+    """bf16x3 on the 4-CTA latency kernel: ragged K up to the cluster limit within
+    the bf16 class tolerance, and rows of a batch bit-identical to single-node calls."""
+    from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
+    from paper_2203_07747_b200 import _lib
+    monkeypatch.setenv("RTN_KERNEL", "quad")
+    om = OracleModel.random_net([17, 512, 512, 512, 6], "silu", 41, True)
+    eng = to_product_model(om).engine(precision=_lib.PRECISIONS["bf16x3"])
+    for k in (1, 2, 5, 74):
+        z = quad_nodes(9, k)
+        f, j, _ = om.batched_eval(z, 1)
+        got = eng.prepare(z, 1)
+        assert max_node_rel_error(got.values, f) < 1e-4 and max_node_rel_error(got.jacobians, j) < 1e-4, k
+    z = quad_nodes(10, 7)
+    full = eng.prepare(z, 1)
+    for i in (0, 3, 6):
+        one = eng.prepare(z[i:i + 1], 1)
+        assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
