@@ -469,27 +469,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fl = l + 1;
         fine(fl, 0, 0);
         const float* bias = bhs + l * 256;
-        table_stage(reg, 0, 64, bias);
+        // stage 0: tables of K-chunks 0..3; the MMAs of chunks 0..2 then cover the
+        // second stage (chunks 4..7), while chunk 3's accumulator load is in flight
+        table_stage(reg, 0, 128, bias);
         fine(fl, 0, 1);
-        {
-          float m[16];
-          tmem_ld16(reg + lane_base + 16 * h, m);
-          finish16(reg, 16 * h, m);
-          signal(0);
-          trace(l + 1, 1);
-          fine(fl, 0, 2);
-          tmem_ld16(reg + lane_base + 32 + 16 * h, m);  // chunk 1, in flight during the second table stage
-          table_stage(reg, 64, 192, bias);
-          finish16(reg, 32 + 16 * h, m);
-          signal(1);
-        }
 #pragma unroll 1
-        for (int c = 2; c < 8; ++c) {
+        for (int c = 0; c < 8; ++c) {
           const int c0 = 32 * c + 16 * h;
           float m[16];
           tmem_ld16(reg + lane_base + c0, m);
+          if (c == 3) table_stage(reg, 128, 128, bias);
           finish16(reg, c0, m);
           signal(c);
+          if (c == 0) {
+            trace(l + 1, 1);
+            fine(fl, 0, 2);
+          }
         }
         ++prod;
         trace(l + 1, 2);
