@@ -488,6 +488,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         ++prod;
         trace(l + 1, 2);
+        // the next tile's layer-0 tables fill the wait for this layer's successor
+        // (tab0 and zs are free once this tile's layer 0 was rewritten)
+        if (l == 0 && tile + npairs < prm.num_tiles) layer0_tables(tile + npairs);
         fine(fl, 0, 3);
       }
       // ---- tile boundary. The output layer accumulates into columns 0..15 of
@@ -499,7 +502,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t reg_next = tmem_base + nb * 256;
       const bool more = tile + npairs < prm.num_tiles;
       if (more) {
-        layer0_tables(tile + npairs);
+        if (n_mma == 0) layer0_tables(tile + npairs);
         rewrite_chunks0(reg_next, 1, 8, 0);
       }
       mbar_wait(tmem_last, tiles_done & 1);
