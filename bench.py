@@ -601,6 +601,7 @@ def run_ours(args, rank, world, local_rank):
             lat = {"cfg3_12x512_N20": latency(torch, SIZES, SEED, 20),
                    "cfg3_12x512_N20_order2": latency(torch, SIZES, SEED, 20, steps=300, order=2),
                    "cfg3_12x512_N20_bf16x3": latency(torch, SIZES, SEED, 20, steps=300, precision=2),
+                   "cfg3_12x512_N20_3xtf32": latency(torch, SIZES, SEED, 20, steps=300, precision=1),
                    "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20),
                    "cfg1_2x64_N10": latency(torch, [17, 64, 64, 6], 2064, 10, steps=300)}
         cfg4 = cfg4_bench(torch, tf32_peak) if world == 1 and not args.no_modes else None

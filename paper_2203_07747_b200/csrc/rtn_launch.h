@@ -31,6 +31,8 @@ cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CU
 cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
                              cudaStream_t st);
+cudaError_t LaunchQuad3xTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
+                             cudaStream_t st);
 
 // Width-256 throughput kernel with two tiles in flight per CTA pair
 // (rtn_pingpong.cuh): TF32, order <= 1, P = 4 nodes per CTA side.

@@ -543,7 +543,7 @@ enum class Kern { kSingle, kPair, kLatency, kQuad };
 Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
   const bool lat_ok = m->has_pair && m->n_in + 1 <= 24;
   // quad: 4-CTA clusters, one tile of 2 nodes each (TF32, width 512; order-1 path only reaches here)
-  const bool quad_ok = lat_ok && (m->pair_mode == rtn::kTF32 || m->pair_mode == rtn::kBF16x3) && m->pair_wp == 512 &&
+  const bool quad_ok = lat_ok && m->pair_wp == 512 &&
                        m->n_in <= rtn::kMaxIn0 &&
                        K <= 2 * (num_sms / 4);
   if (const char* e = std::getenv("RTN_KERNEL"))
@@ -633,8 +633,9 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     prm.num_tiles = (K + 1) / 2;
     prm.lo_rows = m->lo_rows;
     const int g4 = static_cast<int>(4 * prm.num_tiles);
-    const cudaError_t e = m->pair_mode == rtn::kBF16x3 ? rtn::LaunchQuadBF16x3(prm, m->tmap_h, m->tmap_l, g4, c->stream)
-                                                       : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
+    const cudaError_t e = m->pair_mode == rtn::kBF16x3  ? rtn::LaunchQuadBF16x3(prm, m->tmap_h, m->tmap_l, g4, c->stream)
+                          : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
+                                                         : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;

@@ -1,5 +1,7 @@
 // rtn_quad.cuh — latency kernel on 4-CTA clusters (two CTA pairs), order 1,
-// TF32 or bf16x3 (MODE; hi/lo operand split as in rtn_pair.cuh, 3 passes).
+// TF32, bf16x3 or 3xTF32 (MODE; hi/lo operand split as in rtn_pair.cuh, 3
+// passes; 3xTF32 with the split accumulators D/D3 (main pass by chunk parity)
+// and D2 (corrections) at TMEM columns 0, 64, 128).
 //
 // Why: at one MPC step (K = N nodes) the pair kernel gives each 2-node
 // cluster the WHOLE weight stream; every SM pushes ~5.8 MB of 12x512 weights
@@ -85,6 +87,40 @@ __device__ __forceinline__ void mma12_bf16_pair_commit_m(uint32_t d, uint64_t a_
       : "memory");
 }
 
+// 3xTF32 chunk with separate accumulators (rtn_pair.cuh RTN_MMA12): hi·hi into
+// d, hi·lo + lo·hi into d2; `accumulate` bit 0 = d's first K-step accumulates,
+// bit 1 = d2's. Masked multicast commits as mma12_bf16_pair_commit_m.
+__device__ __forceinline__ void mma12_tf32_pair_commit_m(uint32_t d, uint32_t d2, uint64_t a_hi, uint64_t a_lo,
+                                                         uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
+                                                         uint32_t accumulate, uint32_t bar0, uint32_t bar1,
+                                                         uint32_t mask, uint32_t bar2, uint32_t mask2) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t, q, c;\n\t.reg .b64 x, y;\n\t.reg .b16 m, m2;\n\t.reg .b32 r;\n\t"
+      "cvt.u16.u32 m, %10;\n\tcvt.u16.u32 m2, %12;\n\t"
+      "and.b32 r, %7, 1;\n\tsetp.ne.b32 p, r, 0;\n\tand.b32 r, %7, 2;\n\tsetp.ne.b32 c, r, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\tsetp.ne.b32 q, %11, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %2, %4, %6, p;\n\t"
+      "add.s64 x, %2, 2;\n\tadd.s64 y, %4, 2;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%0], x, y, %6, t;\n\t"
+      "add.s64 x, %2, 4;\n\tadd.s64 y, %4, 4;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%0], x, y, %6, t;\n\t"
+      "add.s64 x, %2, 6;\n\tadd.s64 y, %4, 6;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%0], x, y, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], %2, %5, %6, c;\n\t"
+      "add.s64 x, %2, 2;\n\tadd.s64 y, %5, 2;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%1], x, y, %6, t;\n\t"
+      "add.s64 x, %2, 4;\n\tadd.s64 y, %5, 4;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%1], x, y, %6, t;\n\t"
+      "add.s64 x, %2, 6;\n\tadd.s64 y, %5, 6;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%1], x, y, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], %3, %4, %6, t;\n\t"
+      "add.s64 x, %3, 2;\n\tadd.s64 y, %4, 2;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%1], x, y, %6, t;\n\t"
+      "add.s64 x, %3, 4;\n\tadd.s64 y, %4, 4;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%1], x, y, %6, t;\n\t"
+      "add.s64 x, %3, 6;\n\tadd.s64 y, %4, 6;\n\t@e tcgen05.mma.cta_group::2.kind::tf32 [%1], x, y, %6, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%9], m;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%11], m2;\n\t}" ::"r"(d),
+      "r"(d2), "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate), "r"(bar0), "r"(bar1),
+      "r"(mask), "r"(bar2), "r"(mask2)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_mask(uint64_t* bar, uint32_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\t"
@@ -101,7 +137,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_quad_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
   constexpr int WP = 512, P = 1;
-  static_assert(MODE == kTF32 || MODE == kBF16x3, "quad kernel: TF32 or bf16x3");
+  // 3xTF32 accumulators (N = 2·NTC <= 64 columns each): D, D3 (odd chunks), D2 (corrections)
+  constexpr uint32_t kD3 = 64, kD2 = 128;
+  static_assert(MODE != k3xTF32 || 2 * NTC <= 64, "3xTF32 accumulators are 64 columns apart");
   using C = PairCfg<WP, NSTAGE, P, NTC, MODE, false>;
   // tf32: 16 chunks of 32 k, 4 per group; bf16: 8 chunks of 64 k, 2 per group; 4 groups
   constexpr int NKC = C::kNKC, CPG = C::kCPG, NG = C::kNG, SPLIT = C::kSplit, EB = C::kEB;
@@ -182,16 +220,29 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== pair MMA issuer (pair leaders: ranks 0 and 2) ======
     if (leader) {
-      const uint32_t idesc_h = MODE == kBF16x3 ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_h = MODE == kBF16x3 ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);  // tf32: TF32, 3xTF32
       const uint32_t idesc_o = MODE == kBF16x3 ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
       constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4, kSplitD = C::kSplitStride >> 4;
       uint32_t ph = 0, ar = 0;
       // one chunk: weights from stage st0 (hi) [and st0 + 1 (lo)], activations chunk c (hi [, lo])
-      auto chunk = [&](int st0, int c, uint32_t idesc, uint32_t acc, uint32_t bar2, uint32_t mask2, bool weights_are_a) {
+      // i: position of the chunk in this layer's issue order (split accumulators, 3xTF32)
+      auto chunk = [&](int st0, int c, int i, uint32_t idesc, uint32_t acc, uint32_t bar2, uint32_t mask2,
+                       bool weights_are_a) {
         const uint64_t wa = a0 + st0 * kStageD, xa = b0 + c * kChunkD;
-        if constexpr (MODE == kTF32) {
+        if constexpr (MODE == k3xTF32) {
+          const uint64_t wb = wa + kStageD, xb = xa + kSplitD;
+          const uint32_t dm = tmem_base + ((i & 1) ? kD3 : 0u);
+          const uint32_t flags = (i >= 2 ? 1u : 0u) | (i != 0 ? 2u : 0u);
+          (void)acc;
+          if (weights_are_a)
+            mma12_tf32_pair_commit_m(dm, tmem_base + kD2, wa, wb, xa, xb, idesc, flags, smem_u32(&empty[st0]),
+                                     smem_u32(&empty[st0 + 1]), pair_mask, bar2, mask2);
+          else
+            mma12_tf32_pair_commit_m(dm, tmem_base + kD2, xa, xb, wa, wb, idesc, flags, smem_u32(&empty[st0]),
+                                     smem_u32(&empty[st0 + 1]), pair_mask, bar2, mask2);
+        } else if constexpr (MODE == kTF32) {
           if (weights_are_a)
             mma4_tf32_pair_commit_m(tmem_base, wa, xa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
           else
@@ -222,7 +273,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
           if constexpr (SPLIT == 2) mbar_wait(&full[st + 1], ph);
           tc_fence_after();
           const bool last_of_group = (c % CPG) == CPG - 1;
-          chunk(st, c, idesc_h, i != 0, last_of_group ? smem_u32(&in_free[g]) : 0u, 0xFu, true);
+          chunk(st, c, i, idesc_h, i != 0, last_of_group ? smem_u32(&in_free[g]) : 0u, 0xFu, true);
           if (st + SPLIT - 1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_mask(&tmem_full[0], pair_mask);
@@ -239,7 +290,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full[st], ph);
           if constexpr (SPLIT == 2) mbar_wait(&full[st + 1], ph);
           tc_fence_after();
-          chunk(st, i, idesc_o, i != 0, 0u, 0u, false);
+          chunk(st, i, i, idesc_o, i != 0, 0u, 0u, false);
           if (st + SPLIT - 1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_mask(tmem_last, pair_mask);
@@ -275,6 +326,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
           const float h = to_tf32(v[i]);
           st_cluster_f32(dst0 + a, h);
           st_cluster_f32(dst1 + a, h);
+        } else if constexpr (MODE == k3xTF32) {  // tf32 hi and lo
+          const float h = to_tf32(v[i]), lo = to_tf32(v[i] - h);
+          st_cluster_f32(dst0 + a, h);
+          st_cluster_f32(dst1 + a, h);
+          st_cluster_f32(dst0 + a + C::kSplitStride, lo);
+          st_cluster_f32(dst1 + a + C::kSplitStride, lo);
         } else {  // bf16 hi and lo (rtn_pair.cuh store_side)
           const uint16_t h = bf16_rn_bits(v[i]);
           const uint16_t lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
@@ -323,6 +380,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c0 = 0; c0 < NTC; c0 += 8)
         if (c0 < ntc) tmem_ld8(tmem_base + lane_base + half * ntc + c0, v + c0);
       tmem_ld_wait();
+      if constexpr (MODE == k3xTF32)
+        tmem_add2_cols<NTC>(tmem_base + lane_base + kD3 + half * ntc, tmem_base + lane_base + kD2 + half * ntc, v, ntc);
       tc_fence_before();
       float val, sp;
       act_fwd(act, v[0] + bj, val, sp);
@@ -340,6 +399,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
       float o[16];
       tmem_ld16(tmem_base + lane_base, o);
       tmem_ld_wait();
+      if constexpr (MODE == k3xTF32) tmem_add2_cols<16>(tmem_base + lane_base + kD3, tmem_base + lane_base + kD2, o, 16);
       const int r = tid_h, n_out = prm.n_out;
       const long long nd = node0 + sub;
       if (nd < prm.K) {

@@ -60,10 +60,8 @@ CASES = [
 @pytest.mark.parametrize("case", range(len(CASES)))
 @pytest.mark.parametrize("prec", ["3xtf32", "bf16x3"])
 def test_split_modes_on_conditioned_nets(prec, case, kernel, monkeypatch):
-    """quad: the 4-CTA latency kernel (rtn_quad.cuh) also runs bf16x3 at width 512;
-    other shapes fall back to the pair latency kernel."""
-    if kernel == "quad" and prec != "bf16x3":
-        pytest.skip("the quad kernel has TF32 and bf16x3 variants")
+    """quad: the 4-CTA latency kernel (rtn_quad.cuh) also runs bf16x3 and 3xTF32 at
+    width 512; other shapes fall back to the pair latency kernel."""
     sizes, act, gain, bounds = CASES[case]
     err = _err(_net(sizes, act, gain), prec, 64 if kernel == "pair" else 20, kernel, monkeypatch)
     assert err < bounds[prec], f"{prec} {sizes[1]}x{len(sizes) - 2}: {err:.2e}"
