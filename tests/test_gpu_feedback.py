@@ -52,11 +52,14 @@ def _builder(om):
 
 
 @pytest.mark.parametrize("n_inst,n,u_lo,u_hi,status", [(7, 20, 0.0, 6.0, 0), (64, 20, 1.5, 2.2, 0),
-                                                        (9, 50, 0.0, 6.0, 0), (9, 50, 1.6, 2.1, 1)])
+                                                        (9, 50, 0.0, 6.0, 0), (9, 50, 1.6, 2.1, 1),
+                                                        (5, 60, 0.0, 6.0, 0)])
 def test_feedback_matches_oracle(n_inst, n, u_lo, u_hi, status):
-    """The last case binds so many of the 200 inputs that the primal active-set
+    """The fourth case binds so many of the 200 inputs that the primal active-set
     method reaches its 200-pass cap (QpStatus::kMaxIter, qp.cpp:199-207) on both sides:
-    the capped iterates agree as well."""
+    the capped iterates agree as well. The factor lives in shared memory as full
+    rows (N = 20), as the packed lower triangle (N = 50) and in the global
+    workspace (N = 60)."""
     cfg, qpd, qd, xm, xs, us, om = _setup(n_inst, n, seed=n_inst + n, u_lo=u_lo, u_hi=u_hi)
     ref = oracle.solve_feedback(n, qd, xm, xs, us)
     got = _builder(om).solve_feedback(cfg, qpd, xm, xs, us)
