@@ -144,6 +144,8 @@ def test_rows_kernel_input_widths_and_ragged_tiles(monkeypatch):
     _check([26, 256, 192, 3], "silu", 1000)
     _check([31, 100, 256, 256, 6], "tanh", 501)
     _check([17, 256, 6], "relu", 300)  # one hidden layer: no MMA layer before the output
+    _check([17] + [256] * 12 + [6], "silu", 2000)  # 11 hidden->hidden layers: the bias-table capacity
+    _check([17] + [256] * 13 + [6], "silu", 500)   # one more: falls back to the pair kernel
 
 
 def test_rows_kernel_default_for_width256_throughput(monkeypatch):
