@@ -1,0 +1,189 @@
+// rtn_internal.h — host-side internals shared by the C-ABI translation units
+// (rtn_mpc.cu: models, contexts, PrepareNodes / BuildQp / feedback entry
+// points; rtn_comm.cu: the partitioned multi-GPU entry). Not installed.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rtn_mpc.h"
+#include "rtn_blocks.h"
+#include "rtn_launch.h"
+
+namespace rtn_host {
+
+extern thread_local std::string g_err;  // rtn_last_error()
+
+struct Error : std::runtime_error {
+  rtn_status code;
+  Error(rtn_status c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+#define CUDA_CHECK(x)                                                                              \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess)                                                                         \
+      throw ::rtn_host::Error(RTN_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+// Runs f and maps every exception to a status code + thread-local message:
+// no entry point throws or aborts.
+template <typename F>
+rtn_status Guard(F&& f) {
+  try {
+    f();
+    return RTN_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return RTN_ECONFIG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RTN_ECONFIG;
+  }
+}
+
+}  // namespace rtn_host
+
+struct rtn_model {
+  int device = 0;
+  rtn_precision prec = RTN_TF32;
+  int n_in = 0, n_out = 0, n_layers = 0, n_hidden = 0, act = 0, wp = 0;
+  int pair_wp = 0;            // padded width of the packs (256 or 512)
+  float* d_bh_pair = nullptr; // hidden biases with pair_wp stride
+  double* d_mu = nullptr;     // in_mean (fp64, subtracted before layer 0)
+  float* d_w0 = nullptr;
+  float* d_b0 = nullptr;
+  float* d_bl = nullptr;
+  // pair (cta_group::2) kernel: plain row-major tf32 weights behind TMA maps
+  void* d_wt_hidden = nullptr;  // split x (n_hidden-1)·wp rows x wp cols (fp32 or bf16)
+  void* d_wt_last = nullptr;    // split x 16 rows x wp cols
+  CUtensorMap tmap_h{}, tmap_l{};
+  int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3
+  int lo_rows = 0;     // row offset of the lo tiles in the stacked hidden map
+  ~rtn_model() {
+    int prev;
+    if (cudaGetDevice(&prev) == cudaSuccess) {
+      cudaSetDevice(device);
+      cudaFree(d_mu);
+      cudaFree(d_w0);
+      cudaFree(d_b0);
+      cudaFree(d_bl);
+      cudaFree(d_wt_hidden);
+      cudaFree(d_wt_last);
+      cudaFree(d_bh_pair);
+      cudaSetDevice(prev);
+    }
+  }
+};
+
+struct rtn_ctx {
+  const rtn_model* model = nullptr;
+  long long max_rows = 0;
+  int max_order = 1;
+  int latency_mode = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  double* d_z = nullptr;
+  double* d_f = nullptr;
+  double* d_jac = nullptr;
+  double* d_hess = nullptr;
+  double* h_hess = nullptr;
+  double* h_z = nullptr;  // pinned staging
+  double* h_f = nullptr;
+  double* h_jac = nullptr;
+  int num_sms = 148;
+  unsigned long long calls = 0, points = 0, launches = 0;
+  // end-to-end pipeline: copy-in / copy-out streams and per-chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k;
+  // latency mode: one captured graph (H2D, kernel, D2H) per (K, order)
+  struct Graph {
+    long long K;
+    int order;
+    cudaGraphExec_t exec;
+    const void* io[4];  // caller buffers of a direct (zero-copy) graph; null = staged
+  };
+  std::vector<Graph> graphs;
+  // continuity-block builder: contiguous device in/out areas and pinned
+  // staging, grown on demand; the per-call error word; cycle graphs.
+  double* d_qin = nullptr;
+  double* d_qout = nullptr;
+  double* h_qin = nullptr;
+  double* h_qout = nullptr;
+  size_t qin_cap = 0, qout_cap = 0, hqin_cap = 0, hqout_cap = 0;  // doubles
+  unsigned long long* d_bad = nullptr;
+  unsigned long long* h_bad = nullptr;
+  // feedback solve workspace (grown on demand)
+  double* d_fb = nullptr;
+  size_t fb_cap = 0;  // doubles
+  char* d_fb_small = nullptr;
+  size_t fb_small_cap = 0;  // bytes (status, iterations, active)
+  unsigned char* h_status = nullptr;  // zero-copy latency mode: per-node status bytes
+  long long status_cap = 0;
+  // A captured cycle / BuildQp graph bakes in the kernel arguments (every
+  // BlkParams field: dt, weights, bounds, quad parameters, variant, buffer
+  // pointers) and the staging buffers its copies use; a replay is only valid
+  // for the identical set, so all of it is the cache key.
+  struct QpGraph {
+    long long n_inst;
+    int N, order;
+    unsigned mask;
+    rtn::BlkParams blk;
+    const void* bufs[4];  // h_qin, h_qout, d_qin, d_qout at capture
+    cudaGraphExec_t exec;
+    unsigned long long kernels;  // kernel nodes per replay
+  };
+  std::vector<QpGraph> qp_graphs;
+  ~rtn_ctx() {
+    int prev;
+    if (cudaGetDevice(&prev) == cudaSuccess) {
+      cudaSetDevice(model->device);
+      cudaFree(d_z);
+      cudaFree(d_f);
+      cudaFree(d_jac);
+      cudaFree(d_hess);
+      cudaFreeHost(h_hess);
+      cudaFreeHost(h_z);
+      cudaFreeHost(h_f);
+      cudaFreeHost(h_jac);
+      if (own_stream) cudaStreamDestroy(own_stream);
+      if (s_in) cudaStreamDestroy(s_in);
+      if (s_out) cudaStreamDestroy(s_out);
+      for (auto e : ev_in) cudaEventDestroy(e);
+      for (auto e : ev_k) cudaEventDestroy(e);
+      for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+      for (auto& g : qp_graphs) cudaGraphExecDestroy(g.exec);
+      cudaFree(d_qin);
+      cudaFree(d_qout);
+      cudaFreeHost(h_qin);
+      cudaFreeHost(h_qout);
+      cudaFree(d_bad);
+      cudaFreeHost(h_bad);
+      cudaFree(d_fb);
+      cudaFree(d_fb_small);
+      cudaFreeHost(h_status);
+      cudaSetDevice(prev);
+    }
+  }
+};
+
+namespace rtn_host {
+
+constexpr int kMaxChunks = 8;  // end-to-end pipeline depth (chunks per call)
+
+// Enqueues one PrepareNodes launch on the context stream (kernel choice,
+// tile geometry; rtn_mpc.cu). d_zx/d_zu: gather [x_k; u_k] from an iterate.
+void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac,
+             double* d_hess = nullptr, const double* d_zx = nullptr, const double* d_zu = nullptr, int zN = 0);
+bool IsPinned(const void* p);
+void EnsureStaging(rtn_ctx* c);
+void CheckCall(const rtn_ctx* c, long long K, int order);
+
+}  // namespace rtn_host

@@ -39,10 +39,7 @@
 
 namespace rtn {
 
-constexpr int kNT = 80;             // max tile rows (MMA N); multiple of 16
-constexpr int kTmemStride = 80;     // TMEM columns per neuron block region
-constexpr int kStageBytes = 16384;  // one weight block: 128 neurons x 32 k fp32
-constexpr int kLastBlockBytes = 2048;  // output-layer block: 16 outputs x 32 k
+constexpr int kStageBytes = 16384;  // one weight stage: 128 neurons x 128 bytes of k
 constexpr int kThreads = 384;       // 4 control warps + 8 epilogue warps
 constexpr int kMaxOut = 16;
 
@@ -60,12 +57,12 @@ struct KParams {
   int P;             // nodes per tile (power of two)
   int nt;            // tile rows used (= roundup8(P·(1+n_in))), MMA N
   int lo_rows;       // pair kernel split modes: row offset of the lo weight tiles in the stacked map
+  int ord2_g;        // order 2: pair tiles per node (Hessian slot groups)
   unsigned long long* trace;  // optional event timestamps (RTN_TRACE), pair 0 only
-  int dbg;           // perf-isolation switches (RTN_DEBUG): 1 = MMA ignores act_ready, 2 = 1 KB weight copies
-  const uint8_t* w_hidden;  // (n_hidden-1) x NMB x NKC blocks of kStageBytes
-  const uint8_t* w_last;    // NKC blocks of kLastBlockBytes
-  const float* w0;   // WP x n_in   (normalisation folded)
-  const float* b0;   // WP
+  int dbg;           // perf-isolation switches (RTN_DEBUG): 4 = skip epilogue math, 8 = local stores, 128 = stream only
+  const double* mu;  // n_in: in_mean, subtracted in fp64 before the fp32 layer 0
+  const float* w0;   // WP x n_in   (W0·diag(1/in_scale))
+  const float* b0;   // WP          (the layer-0 bias; the mean is NOT folded in)
   const float* bh;   // (n_hidden-1) x WP
   const float* bl;   // kMaxOut     (out_scale ⊙ b_L + out_mean)
   // Gather mode (rtn_cycle_qp, 'full' variant): when zx != null, row k is the
@@ -92,11 +89,20 @@ __device__ __forceinline__ float layer0_pre(float b, const float (&w)[kMaxIn0], 
   return pre;
 }
 
-// Element k of node row `node` of the MLP input.
+// Element k of node row `node` of the MLP input, centred in fp64: z_k − in_mean_k.
+// The reference normalises in fp64 before the first layer
+// (proj/src/neural.cpp:107-109); folding the mean into the fp32 layer-0 bias
+// instead (b0 − W0'·μ) cancels catastrophically for inputs far from zero
+// relative to in_scale, so only the 1/in_scale scaling is folded into W0'.
 __device__ __forceinline__ double load_z(const KParams& prm, long long node, int k) {
-  if (prm.zx == nullptr) return prm.z[node * prm.n_in + k];
-  const long long xrow = node + node / prm.zN;  // inst·(N+1) + n
-  return k < 13 ? prm.zx[xrow * 13 + k] : prm.zu[node * 4 + (k - 13)];
+  double v;
+  if (prm.zx == nullptr) {
+    v = prm.z[node * prm.n_in + k];
+  } else {
+    const long long xrow = node + node / prm.zN;  // inst·(N+1) + n
+    v = k < 13 ? prm.zx[xrow * 13 + k] : prm.zu[node * 4 + (k - 13)];
+  }
+  return v - __ldg(prm.mu + k);
 }
 
 // ----------------------------------------------------------------------------
@@ -552,11 +558,20 @@ __host__ __device__ constexpr PairAB pair_ab(int p, int n) {
   }
   return PairAB{a, a + p};
 }
-constexpr int kNin2 = 17;                         // order-2 device path: quadrotor inputs
+constexpr int kMaxIn2 = 31;                       // order 2, generic tiles: 1 + n_in carrier rows <= 32
+constexpr int kNin2 = 17;                         // order-2 specialised tiles: quadrotor inputs
 constexpr int kPairs2 = kNin2 * (kNin2 + 1) / 2;  // 153 packed Hessian rows per node
 constexpr int kCarrier2 = 1 + kNin2;              // value + tangent rows carried by every tile
 constexpr int kNtc2 = 48;                         // rows per CTA side in order-2 tiles
 constexpr int kSlots2 = 2 * kNtc2 - kCarrier2;    // 78 Hessian rows per tile → 2 tiles per node
+
+// Order-2 tile plan for n_in inputs and NTC rows per CTA side: the carrier
+// (value + n_in tangents) sits in side-0 rows [0, 1+n_in); the other
+// 2·NTC − (1+n_in) rows are Hessian slots; a node takes ceil(pairs / slots) tiles.
+__host__ __device__ constexpr int ord2_slots(int n_in, int ntc) { return 2 * ntc - (1 + n_in); }
+__host__ __device__ constexpr int ord2_tiles(int n_in, int ntc) {
+  return (n_in * (n_in + 1) / 2 + ord2_slots(n_in, ntc) - 1) / ord2_slots(n_in, ntc);
+}
 
 // Activation value, slope and curvature (second-order tangents need σ'').
 __device__ __forceinline__ void act_fwd2(int act, float pre, float& val, float& sp, float& spp) {

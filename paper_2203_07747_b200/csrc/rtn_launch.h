@@ -1,14 +1,34 @@
 // rtn_launch.h — host-side launchers of the pair kernel, one translation unit
-// per precision mode (rtn_pair_{tf32,3xtf32,bf16x3}.cu) so they compile in
-// parallel; rtn_mpc.cu dispatches.
+// per precision mode (rtn_pair_{tf32,3xtf32,bf16x3,order2}.cu) so they compile
+// in parallel; rtn_mpc.cu dispatches.
 #pragma once
 
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "rtn_kernel.cuh"
 
 namespace rtn {
+
+// cudaFuncSetAttribute applies per device: remember every (kernel, device)
+// pair it was set for (a process may drive several devices through the C-ABI's
+// `device` argument, from several threads).
+inline cudaError_t EnsureSmem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kern, dev});
+  return e;
+}
 
 struct PairGeom {
   int P;        // nodes per CTA
@@ -26,7 +46,7 @@ cudaError_t LaunchPair3xTF32(const KParams& prm, const CUtensorMap& th, const CU
 cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
                              int grid, cudaStream_t st);
 
-// Latency kernel on 4-CTA clusters (rtn_quad.cuh): TF32, width 512, order <= 1,
+// Latency kernel on 4-CTA clusters (rtn_quad.cuh): width 512, order <= 1,
 // one node per CTA side, grid = 4 x ceil(K / 2).
 cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
@@ -34,18 +54,18 @@ cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CU
 cudaError_t LaunchQuad3xTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
                              cudaStream_t st);
 
-// Width-256 throughput kernel with two tiles in flight per CTA pair
-// (rtn_pingpong.cuh): TF32, order <= 1, P = 4 nodes per CTA side.
-cudaError_t LaunchPingPongTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
-                               cudaStream_t st);
-
 // Width-256 throughput kernel with the activations as the A operand in TMEM
 // (rtn_rows.cuh): TF32, order <= 1, 7 <= n_in <= 31, prm.P = 128 / (1 + n_in)
 // nodes per CTA, grid = 2 x pairs.
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 11;
 
-// Order 2 (value + Jacobian + Hessian; n_in = 17): two pair-tiles per node.
+// Order 2 (value + Jacobian + Hessian), n_in <= kMaxIn2. Order2Ntc picks the
+// tile (rows per CTA side): 48 for the quadrotor's 17 inputs in TF32/bf16x3
+// (compile-time slot tables), else 24 (n_in <= 23; 3xTF32 then rotates over 4
+// main accumulators) or 40. Launch with prm.nt = that value and
+// prm.ord2_g = ord2_tiles(n_in, nt) pair tiles per node (prm.num_tiles = g·K).
+int Order2Ntc(int mode, int n_in);
 cudaError_t LaunchPairOrder2(int mode, const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp,
                              int grid, cudaStream_t st);
 

@@ -1,6 +1,7 @@
 // rtn_mpc.cu — C-ABI (include/rtn_mpc.h): model loader/packer, contexts and
 // the PrepareNodes/MlpBatchedEval-equivalent entry points. Every compute call
-// runs the sm_100a kernels in rtn_fused.cuh; there is no CPU fallback.
+// runs the sm_100a kernels (rtn_pair.cuh, rtn_quad.cuh, rtn_rows.cuh,
+// rtn_blocks.cu, rtn_qpsolve.cu); there is no CPU fallback.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -19,42 +20,16 @@
 
 #include "../../include/rtn_mpc.h"
 #include "rtn_blocks.h"
-#include "rtn_qpsolve.h"
-#include "rtn_fused.cuh"
+#include "rtn_internal.h"
 #include "rtn_launch.h"
+#include "rtn_qpsolve.h"
+
+namespace rtn_host {
+thread_local std::string g_err;
+}  // namespace rtn_host
+using namespace rtn_host;
 
 namespace {
-
-thread_local std::string g_err;
-
-struct Error : std::runtime_error {
-  rtn_status code;
-  Error(rtn_status c, const std::string& w) : std::runtime_error(w), code(c) {}
-};
-
-#define CUDA_CHECK(x)                                                                              \
-  do {                                                                                             \
-    cudaError_t e_ = (x);                                                                          \
-    if (e_ != cudaSuccess)                                                                         \
-      throw Error(RTN_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));                     \
-  } while (0)
-
-template <typename F>
-rtn_status Guard(F&& f) {
-  try {
-    f();
-    return RTN_OK;
-  } catch (const Error& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    g_err = "out of host memory";
-    return RTN_ECONFIG;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return RTN_ECONFIG;
-  }
-}
 
 // Host-side copy of resmpc::MlpModel (proj/include/resmpc/neural.hpp:19-34).
 struct HostModel {
@@ -114,134 +89,9 @@ uint16_t Bf16Bits(float x) {
 
 }  // namespace
 
-// ----------------------------------------------------------------------------
-struct rtn_model {
-  int device = 0;
-  rtn_precision prec = RTN_TF32;
-  int n_in = 0, n_out = 0, n_layers = 0, n_hidden = 0, act = 0, wp = 0;
-  int pair_wp = 0;            // padded width of the pair-kernel packs (256 or 512)
-  float* d_bh_pair = nullptr; // hidden biases with pair_wp stride
-  void* d_w_hidden = nullptr;  // packed SW128 blocks
-  void* d_w_last = nullptr;
-  float* d_w0 = nullptr;
-  float* d_b0 = nullptr;
-  float* d_bh = nullptr;
-  float* d_bl = nullptr;
-  size_t hidden_bytes = 0;
-  // pair (cta_group::2) kernel: plain row-major tf32 weights behind TMA maps
-  void* d_wt_hidden = nullptr;  // split x (n_hidden-1)·wp rows x wp cols (fp32 or bf16)
-  void* d_wt_last = nullptr;    // split x 16 rows x wp cols
-  CUtensorMap tmap_h{}, tmap_l{};
-  bool has_pair = false;
-  int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3
-  int lo_rows = 0;     // row offset of the lo tiles in the stacked hidden map
-  ~rtn_model() {
-    int prev;
-    if (cudaGetDevice(&prev) == cudaSuccess) {
-      cudaSetDevice(device);
-      cudaFree(d_w_hidden);
-      cudaFree(d_w_last);
-      cudaFree(d_w0);
-      cudaFree(d_b0);
-      cudaFree(d_bh);
-      cudaFree(d_bl);
-      cudaFree(d_wt_hidden);
-      cudaFree(d_wt_last);
-      cudaFree(d_bh_pair);
-      cudaSetDevice(prev);
-    }
-  }
-};
-
-struct rtn_ctx {
-  const rtn_model* model = nullptr;
-  long long max_rows = 0;
-  int max_order = 1;
-  int latency_mode = 0;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;
-  double* d_z = nullptr;
-  double* d_f = nullptr;
-  double* d_jac = nullptr;
-  double* d_hess = nullptr;
-  double* h_hess = nullptr;
-  double* h_z = nullptr;  // pinned staging
-  double* h_f = nullptr;
-  double* h_jac = nullptr;
-  int num_sms = 148;
-  unsigned long long calls = 0, points = 0, launches = 0;
-  // end-to-end pipeline: copy-in / copy-out streams and per-chunk events
-  cudaStream_t s_in = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_k;
-  // latency mode: one captured graph (H2D, kernel, D2H) per (K, order)
-  struct Graph {
-    long long K;
-    int order;
-    cudaGraphExec_t exec;
-    const void* io[4];  // caller buffers of a direct (zero-copy) graph; null = staged
-  };
-  std::vector<Graph> graphs;
-  // continuity-block builder: contiguous device in/out areas and pinned
-  // staging, grown on demand; the per-call error word; cycle graphs.
-  double* d_qin = nullptr;
-  double* d_qout = nullptr;
-  double* h_qin = nullptr;
-  double* h_qout = nullptr;
-  size_t qin_cap = 0, qout_cap = 0, hqin_cap = 0, hqout_cap = 0;  // doubles
-  unsigned long long* d_bad = nullptr;
-  unsigned long long* h_bad = nullptr;
-  // feedback solve workspace (grown on demand)
-  double* d_fb = nullptr;
-  size_t fb_cap = 0;  // doubles
-  char* d_fb_small = nullptr;
-  size_t fb_small_cap = 0;  // bytes (status, iterations, active)
-  unsigned char* h_status = nullptr;  // zero-copy latency mode: per-node status bytes
-  long long status_cap = 0;
-  struct QpGraph {
-    long long n_inst;
-    int N, order;
-    unsigned mask;
-    cudaGraphExec_t exec;
-    unsigned long long kernels;  // kernel nodes per replay
-  };
-  std::vector<QpGraph> qp_graphs;
-  ~rtn_ctx() {
-    int prev;
-    if (cudaGetDevice(&prev) == cudaSuccess) {
-      cudaSetDevice(model->device);
-      cudaFree(d_z);
-      cudaFree(d_f);
-      cudaFree(d_jac);
-      cudaFree(d_hess);
-      cudaFreeHost(h_hess);
-      cudaFreeHost(h_z);
-      cudaFreeHost(h_f);
-      cudaFreeHost(h_jac);
-      if (own_stream) cudaStreamDestroy(own_stream);
-      if (s_in) cudaStreamDestroy(s_in);
-      if (s_out) cudaStreamDestroy(s_out);
-      for (auto e : ev_in) cudaEventDestroy(e);
-      for (auto e : ev_k) cudaEventDestroy(e);
-      for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
-      for (auto& g : qp_graphs) cudaGraphExecDestroy(g.exec);
-      cudaFree(d_qin);
-      cudaFree(d_qout);
-      cudaFreeHost(h_qin);
-      cudaFreeHost(h_qout);
-      cudaFree(d_bad);
-      cudaFreeHost(h_bad);
-      cudaFree(d_fb);
-      cudaFree(d_fb_small);
-      cudaFreeHost(h_status);
-      cudaSetDevice(prev);
-    }
-  }
-};
-
-namespace {
+namespace rtn_host {
 
 unsigned long long* trace_buf = nullptr;  // RTN_TRACE device buffer
-constexpr int kMaxChunks = 8;                 // end-to-end pipeline depth
 constexpr long long kGraphMaxRows = 4096;     // latency mode: graph-captured steps up to this K
 constexpr long long kChunkMinRows = 1 << 17;  // chunk only batches this large
 
@@ -254,10 +104,12 @@ bool ZeroCopy() {
   return on;
 }
 
+// Hidden widths are zero-padded to the kernels' 256- or 512-neuron layouts
+// (any width in (256, 512] pads to 512; > 512 is rejected by the caller).
 int PaddedWidth(const std::vector<int>& sizes) {
   int w = 0;
   for (size_t l = 1; l + 1 < sizes.size(); ++l) w = std::max(w, sizes[l]);
-  return ((w + 127) / 128) * 128;
+  return w <= 256 ? 256 : (w <= 512 ? 512 : ((w + 255) / 256) * 256);
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -295,10 +147,10 @@ CUtensorMap MakeTmap(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows
 
 // Folds the normalisation into the first/last layer in fp64
 // (proj/include/resmpc/neural.hpp:14-18: y = out_scale ⊙ net((z−μ)⊘s) + out_mean):
-//   W0' = W0·diag(1/s),  b0' = b0 − W0'·μ,
+//   W0' = W0·diag(1/s)   (μ is subtracted from z in fp64 by the kernels, load_z),
 //   WL' = diag(out_scale)·WL,  bL' = out_scale ⊙ bL + out_mean,
-// then packs every tensor-core layer into 128-byte-swizzled K-major blocks in
-// the exact order the kernel streams them.
+// then packs the hidden and output layers as row-major operand copies behind
+// TMA tensor maps (hi/lo stacked in the split precision modes).
 rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   Validate(hm);
   if (prec != RTN_TF32 && prec != RTN_3XTF32 && prec != RTN_BF16X3) throw Error(RTN_ECONFIG, "unknown precision mode");
@@ -306,63 +158,21 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   const int L = static_cast<int>(hm.sizes.size()) - 1;
   const int n_in = hm.sizes.front(), n_out = hm.sizes.back();
   if (L < 2) throw Error(RTN_EUNSUPPORTED, "device path needs at least one hidden layer");
-  // single-CTA kernel: padded width 128/256/512 (TF32 only); pair kernel
-  // (every precision, order 2): 256/512
-  const int wp = PaddedWidth(hm.sizes);
-  if (wp > 512) throw Error(RTN_EUNSUPPORTED, "hidden width > 512 not supported by the fused kernel");
-  const int pwp = std::max(256, wp);
+  const int pwp = PaddedWidth(hm.sizes);
+  if (pwp > 512) throw Error(RTN_EUNSUPPORTED, "hidden width > 512 not supported by the device kernels");
   if (n_out > rtn::kMaxOut) throw Error(RTN_EUNSUPPORTED, "n_out > 16 not supported");
-  if (1 + n_in > rtn::kNT) throw Error(RTN_EUNSUPPORTED, "n_in > 79 not supported");
+  if (n_in > 79) throw Error(RTN_EUNSUPPORTED, "n_in > 79 not supported");
   const int H = L - 1;  // hidden layers (each followed by the activation)
-  const int nkc = wp / 32, nmb = wp / 128;
 
-  // layer 0 (CUDA cores, fp32)
+  // layer 0 (CUDA cores, fp32): W0' = W0·diag(1/in_scale); the bias stays b0
   std::vector<float> w0(static_cast<size_t>(pwp) * n_in, 0.0f), b0(pwp, 0.0f);
   for (int j = 0; j < hm.sizes[1]; ++j) {
-    double acc = hm.b[0][j];
-    for (int k = 0; k < n_in; ++k) {
-      const double w = hm.W[0][static_cast<size_t>(j) * n_in + k] / hm.in_scale[k];
-      w0[static_cast<size_t>(j) * n_in + k] = static_cast<float>(w);
-      acc -= w * hm.in_mean[k];
-    }
-    b0[j] = static_cast<float>(acc);
+    for (int k = 0; k < n_in; ++k)
+      w0[static_cast<size_t>(j) * n_in + k] = static_cast<float>(hm.W[0][static_cast<size_t>(j) * n_in + k] / hm.in_scale[k]);
+    b0[j] = static_cast<float>(hm.b[0][j]);
   }
-  // hidden → hidden layers (tcgen05, tf32)
-  const size_t blocks = static_cast<size_t>(H - 1) * nmb * nkc;
-  std::vector<uint8_t> wh(blocks * rtn::kStageBytes, 0);
-  std::vector<float> bh(static_cast<size_t>(std::max(H - 1, 1)) * wp, 0.0f);
-  for (int l = 1; l < H; ++l) {
-    const int rows = hm.sizes[l + 1], cols = hm.sizes[l];
-    const std::vector<double>& W = hm.W[l];
-    for (int mb = 0; mb < nmb; ++mb)
-      for (int c = 0; c < nkc; ++c) {
-        uint8_t* blk = wh.data() + ((static_cast<size_t>(l - 1) * nmb + mb) * nkc + c) * rtn::kStageBytes;
-        for (int i = 0; i < 128; ++i)
-          for (int kk = 0; kk < 32; ++kk) {
-            const int j = mb * 128 + i, k = c * 32 + kk;
-            const float v = (j < rows && k < cols) ? RoundTf32(static_cast<float>(W[static_cast<size_t>(j) * cols + k])) : 0.0f;
-            std::memcpy(blk + rtn::sw128_offset(i, kk, 0), &v, 4);
-          }
-      }
-    for (int j = 0; j < rows; ++j) bh[static_cast<size_t>(l - 1) * wp + j] = static_cast<float>(hm.b[l][j]);
-  }
-  // output layer (tcgen05 N = 16)
-  std::vector<uint8_t> wl(static_cast<size_t>(nkc) * rtn::kLastBlockBytes, 0);
   std::vector<float> bl(rtn::kMaxOut, 0.0f);
-  {
-    const int cols = hm.sizes[L - 1];
-    const std::vector<double>& W = hm.W[L - 1];
-    for (int c = 0; c < nkc; ++c)
-      for (int o = 0; o < 16; ++o)
-        for (int kk = 0; kk < 32; ++kk) {
-          const int k = c * 32 + kk;
-          const float v = (o < n_out && k < cols)
-                              ? RoundTf32(static_cast<float>(hm.out_scale[o] * W[static_cast<size_t>(o) * cols + k]))
-                              : 0.0f;
-          std::memcpy(wl.data() + c * rtn::kLastBlockBytes + rtn::sw128_offset(o, kk, 0), &v, 4);
-        }
-    for (int o = 0; o < n_out; ++o) bl[o] = static_cast<float>(hm.out_scale[o] * hm.b[L - 1][o] + hm.out_mean[o]);
-  }
+  for (int o = 0; o < n_out; ++o) bl[o] = static_cast<float>(hm.out_scale[o] * hm.b[L - 1][o] + hm.out_mean[o]);
 
   int ndev = 0;
   CUDA_CHECK(cudaGetDeviceCount(&ndev));
@@ -379,17 +189,14 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   m->n_layers = L;
   m->n_hidden = H;
   m->act = hm.act;
-  m->wp = wp;
-  m->hidden_bytes = wh.size();
+  m->wp = pwp;
   auto up = [](void** d, const void* h, size_t n) {
     CUDA_CHECK(cudaMalloc(d, std::max<size_t>(n, 16)));
     if (n) CUDA_CHECK(cudaMemcpy(*d, h, n, cudaMemcpyHostToDevice));
   };
-  up(&m->d_w_hidden, wh.data(), wh.size());
-  up(&m->d_w_last, wl.data(), wl.size());
+  up(reinterpret_cast<void**>(&m->d_mu), hm.in_mean.data(), hm.in_mean.size() * 8);
   up(reinterpret_cast<void**>(&m->d_w0), w0.data(), w0.size() * 4);
   up(reinterpret_cast<void**>(&m->d_b0), b0.data(), b0.size() * 4);
-  up(reinterpret_cast<void**>(&m->d_bh), bh.data(), bh.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
   {
     std::vector<float> bh2(static_cast<size_t>(std::max(H - 1, 1)) * pwp, 0.0f);
@@ -441,11 +248,9 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
     }
     m->tmap_h = MakeTmap(m->d_wt_hidden, split * hid_rows, wp, 128, bf16);
     m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(split) * 16, wp, 8, bf16);
-    m->has_pair = true;
     m->pair_mode = mode;
     m->lo_rows = static_cast<int>(hid_rows);
   }
-  if (mode != rtn::kTF32) m->wp = pwp;  // split precisions exist only on the pair kernel
   return m.release();
 }
 
@@ -502,84 +307,38 @@ HostModel ReadRmlp(const char* path) {
   return m;
 }
 
-int NodesPerTile(int n_in) {
-  const int rpn = 1 + n_in;
-  int p = 16;
-  while (p > 1 && p * rpn > rtn::kNT) p >>= 1;
-  return p;
-}
-
-template <int WP, int NS, int P>
-void LaunchT(const rtn::KParams& prm, int grid, cudaStream_t st) {
-  using Cfg = rtn::FusedCfg<WP, NS, P>;
-  auto kern = rtn::rtn_fused_kernel<WP, NS, P>;
-  static bool attr_set = false;  // per instantiation, per process (device-independent attribute)
-  if (!attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
-    attr_set = true;
-  }
-  kern<<<grid, rtn::kThreads, Cfg::kSmemBytes, st>>>(prm);
-  CUDA_CHECK(cudaGetLastError());
-}
-
-template <int WP, int NS>
-void LaunchP(const rtn::KParams& prm, int grid, cudaStream_t st) {
-  switch (prm.P) {
-    case 1: return LaunchT<WP, NS, 1>(prm, grid, st);
-    case 2: return LaunchT<WP, NS, 2>(prm, grid, st);
-    case 4: return LaunchT<WP, NS, 4>(prm, grid, st);
-    case 8: return LaunchT<WP, NS, 8>(prm, grid, st);
-    default: return LaunchT<WP, NS, 16>(prm, grid, st);
-  }
-}
-
-// Kernel choice (padded width 256/512; RTN_KERNEL=pair|latency|single forces one):
-//   throughput: pair kernel, P = 4 nodes per CTA (N = 144), when the batch
-//               fills at least half the pairs;
-//   latency   : pair kernel, P = 1 node per CTA (N = 48), one node per SM,
-//               deep weight pipeline — small batches (one MPC step, K = N);
-//   single    : one-CTA kernel (padded width 128, or forced).
-enum class Kern { kSingle, kPair, kLatency, kQuad };
-Kern Choose(const rtn_model* m, long long K, int P, int num_sms) {
-  const bool lat_ok = m->has_pair && m->n_in + 1 <= 24;
-  // quad: 4-CTA clusters, one tile of 2 nodes each (TF32, width 512; order-1 path only reaches here)
-  const bool quad_ok = lat_ok && m->pair_wp == 512 &&
-                       m->n_in <= rtn::kMaxIn0 &&
-                       K <= 2 * (num_sms / 4);
-  if (const char* e = std::getenv("RTN_KERNEL"))
-    if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
-  // rows (rtn_rows.cuh): selected inside the pair branch of Enqueue for TF32 width-256 throughput
-  const bool rows_ok = m->has_pair && m->pair_mode == rtn::kTF32 && m->pair_wp == 256 &&
-                       m->n_in >= rtn::kRowsMinIn && m->n_in <= rtn::kRowsMaxInHost &&
-                       m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
-  if (const char* e = std::getenv("RTN_KERNEL"))
-    if (std::strcmp(e, "rows") == 0 && rows_ok) return Kern::kPair;
-  if (quad_ok && !std::getenv("RTN_KERNEL")) {
-    const char* q = std::getenv("RTN_QUAD");
-    if (!(q && q[0] == '0')) return Kern::kQuad;
-  }
-  if (m->pair_mode != rtn::kTF32) {  // split precisions exist only on the pair kernel
-    if (const char* e = std::getenv("RTN_KERNEL"))
-      if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
-    if (const char* e = std::getenv("RTN_KERNEL"))
-      if (std::strcmp(e, "pair") == 0) return Kern::kPair;
-    return (lat_ok && K <= num_sms) ? Kern::kLatency : Kern::kPair;
-  }
+// Kernel choice (RTN_KERNEL=pair|latency|quad|rows forces one where it applies):
+//   quad    : width 512, order <= 1, K <= 2·(#SMs/4) — 4-CTA clusters, each
+//             CTA pair computes one 256-neuron block (rtn_quad.cuh): one MPC step;
+//   latency : pair kernel with one node per CTA side, K <= #SMs;
+//   rows    : TF32 width-256 throughput batches, activations as the A operand
+//             in TMEM (rtn_rows.cuh);
+//   pair    : pair-kernel throughput tiles (rtn_pair.cuh).
+enum class Kern { kPair, kLatency, kQuad, kRows };
+Kern Choose(const rtn_model* m, long long K, int num_sms) {
+  const bool lat_ok = m->n_in + 1 <= 24;
+  const bool quad_ok = lat_ok && m->pair_wp == 512 && m->n_in <= rtn::kMaxIn0 && K <= 2 * (num_sms / 4);
+  const bool rows_ok = m->pair_mode == rtn::kTF32 && m->pair_wp == 256 && m->n_in >= rtn::kRowsMinIn &&
+                       m->n_in <= rtn::kRowsMaxInHost && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
   if (const char* e = std::getenv("RTN_KERNEL")) {
-    if (std::strcmp(e, "pair") == 0 && m->has_pair) return Kern::kPair;
+    if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
+    if (std::strcmp(e, "rows") == 0 && rows_ok) return Kern::kRows;
     if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
-    if (std::strcmp(e, "single") == 0) return Kern::kSingle;
+    if (std::strcmp(e, "pair") == 0) return Kern::kPair;
+    // a kernel that does not apply to this model: the default choice below
   }
-  if (!m->has_pair) return Kern::kSingle;
-  if (K >= static_cast<long long>(P) * num_sms) return Kern::kPair;
+  const char* q = std::getenv("RTN_QUAD");
+  if (quad_ok && !(q && q[0] == '0')) return Kern::kQuad;
   if (lat_ok && K <= num_sms) return Kern::kLatency;
+  const char* r = std::getenv("RTN_ROWS");
+  if (rows_ok && !(r && r[0] == '0')) return Kern::kRows;
   return Kern::kPair;
 }
 
 // d_zx/d_zu (optional): gather the quadrotor rows [x_k; u_k] from an iterate
 // (n_inst x (N+1) x 13 states, K x 4 inputs) instead of reading d_z.
-void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac,
-             double* d_hess = nullptr, const double* d_zx = nullptr, const double* d_zu = nullptr, int zN = 0) {
+void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac, double* d_hess,
+             const double* d_zx, const double* d_zu, int zN) {
   const rtn_model* m = c->model;
   if (K == 0) return;
   rtn::KParams prm{};
@@ -589,104 +348,81 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   prm.zN = zN;
   prm.f = d_f;
   prm.jac = order >= 1 ? d_jac : nullptr;
+  prm.hess = nullptr;
   prm.K = K;
   prm.n_in = m->n_in;
   prm.n_out = m->n_out;
   prm.n_hidden = m->n_hidden;
   prm.act = m->act;
   prm.order = order;
-  prm.P = NodesPerTile(m->n_in);
-  prm.nt = ((prm.P * (1 + m->n_in) + 7) / 8) * 8;
-  if (prm.nt < 16) prm.nt = 16;
-  prm.num_tiles = (K + prm.P - 1) / prm.P;
+  prm.lo_rows = m->lo_rows;
+  prm.mu = m->d_mu;
+  prm.w0 = m->d_w0;
+  prm.b0 = m->d_b0;
+  prm.bh = m->d_bh_pair;
+  prm.bl = m->d_bl;
   if (const char* d = std::getenv("RTN_DEBUG")) prm.dbg = std::atoi(d);
   if (std::getenv("RTN_TRACE")) {  // per-event timestamps of pair 0 (profiling aid)
     if (!trace_buf) CUDA_CHECK(cudaMalloc(&trace_buf, 256 * 8));
     CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 256 * 8, c->stream));
     prm.trace = trace_buf;
   }
-  prm.w_hidden = static_cast<const uint8_t*>(m->d_w_hidden);
-  prm.w_last = static_cast<const uint8_t*>(m->d_w_last);
-  prm.w0 = m->d_w0;
-  prm.b0 = m->d_b0;
-  prm.bh = m->d_bh;
-  prm.bl = m->d_bl;
-  prm.hess = nullptr;
+  cudaError_t e;
   if (order == 2) {
+    // pair tiles of the node's carrier (value + tangents) plus Hessian slots
     prm.P = 1;
-    prm.nt = rtn::kNtc2;
-    prm.lo_rows = m->lo_rows;
-    prm.bh = m->d_bh_pair;
+    prm.nt = rtn::Order2Ntc(m->pair_mode, m->n_in);
+    prm.ord2_g = rtn::ord2_tiles(m->n_in, prm.nt);
     prm.hess = d_hess;
-    prm.num_tiles = 2 * K;  // two Hessian groups per node
+    prm.num_tiles = static_cast<long long>(prm.ord2_g) * K;
     const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
-    const cudaError_t e = rtn::LaunchPairOrder2(m->pair_mode, prm, m->tmap_h, m->tmap_l, m->pair_wp, grid, c->stream);
+    e = rtn::LaunchPairOrder2(m->pair_mode, prm, m->tmap_h, m->tmap_l, m->pair_wp, grid, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("order-2 kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }
-  const Kern kern = Choose(m, K, prm.P, c->num_sms);
+  const Kern kern = Choose(m, K, c->num_sms);
   if (kern == Kern::kQuad) {
-    prm.bh = m->d_bh_pair;
     prm.P = 1;
     prm.nt = ((1 + m->n_in + 7) / 8) * 8;
     prm.num_tiles = (K + 1) / 2;
-    prm.lo_rows = m->lo_rows;
     const int g4 = static_cast<int>(4 * prm.num_tiles);
-    const cudaError_t e = m->pair_mode == rtn::kBF16x3  ? rtn::LaunchQuadBF16x3(prm, m->tmap_h, m->tmap_l, g4, c->stream)
-                          : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
-                                                         : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
+    e = m->pair_mode == rtn::kBF16x3  ? rtn::LaunchQuadBF16x3(prm, m->tmap_h, m->tmap_l, g4, c->stream)
+        : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
+                                       : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }
-  if (kern != Kern::kSingle) {
-    prm.bh = m->d_bh_pair;
-    const bool lat = kern == Kern::kLatency;
-    const rtn::PairGeom g = rtn::PairGeometry(m->pair_mode, m->pair_wp, lat, m->n_in);
-    prm.P = g.P;
-    prm.nt = ((g.P * (1 + m->n_in) + 7) / 8) * 8;
-    if (prm.nt > g.ntc_max) throw Error(RTN_EUNSUPPORTED, "node rows exceed the pair tile");
-    prm.lo_rows = m->lo_rows;
-    prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
-    const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
-    cudaError_t e;
-    const char* pp = std::getenv("RTN_PINGPONG");
-    const char* rw = std::getenv("RTN_ROWS");
-    const char* fk = std::getenv("RTN_KERNEL");
-    if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && m->n_in >= rtn::kRowsMinIn &&
-        m->n_in <= rtn::kRowsMaxInHost && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost && !(rw && rw[0] == '0') &&
-        !(fk && std::strcmp(fk, "pair") == 0)) {
-      // width 256: activations as the A operand in TMEM (rtn_rows.cuh), 128 rows per CTA
-      prm.P = 128 / (1 + m->n_in);
-      prm.nt = 128;
-      prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);
-      const int g3 = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
-      e = rtn::LaunchRowsTF32(prm, m->tmap_h, m->tmap_l, g3, c->stream);
-    } else if (m->pair_mode == rtn::kTF32 && !lat && m->pair_wp == 256 && prm.P == 4 && m->n_in <= rtn::kMaxIn0 &&
-        !(pp && pp[0] == '0')) {
-      // width 256: two tiles in flight per CTA pair (rtn_pingpong.cuh)
-      const long long tile_pairs = (prm.num_tiles + 1) / 2;
-      const int g2 = 2 * static_cast<int>(std::min<long long>(tile_pairs, c->num_sms / 2));
-      e = rtn::LaunchPingPongTF32(prm, m->tmap_h, m->tmap_l, g2, c->stream);
-    } else if (m->pair_mode == rtn::kTF32)
-      e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
-    else if (m->pair_mode == rtn::k3xTF32) e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
-    else e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
-    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));
+  if (kern == Kern::kRows) {
+    // width 256: activations as the A operand in TMEM (rtn_rows.cuh), 128 rows per CTA
+    prm.P = 128 / (1 + m->n_in);
+    prm.nt = 128;
+    prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);
+    const int g3 = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+    e = rtn::LaunchRowsTF32(prm, m->tmap_h, m->tmap_l, g3, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("rows kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }
-  const int grid = static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms));
-  switch (m->wp) {
-    case 128: LaunchP<128, 8>(prm, grid, c->stream); break;
-    case 256: LaunchP<256, 8>(prm, grid, c->stream); break;
-    default: LaunchP<512, 3>(prm, grid, c->stream); break;
-  }
+  const bool lat = kern == Kern::kLatency;
+  const rtn::PairGeom g = rtn::PairGeometry(m->pair_mode, m->pair_wp, lat, m->n_in);
+  prm.P = g.P;
+  prm.nt = ((g.P * (1 + m->n_in) + 7) / 8) * 8;
+  if (prm.nt > g.ntc_max) throw Error(RTN_EUNSUPPORTED, "node rows exceed the pair tile");
+  prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);  // pair tiles of 2P nodes
+  const int grid = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+  if (m->pair_mode == rtn::kTF32)
+    e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+  else if (m->pair_mode == rtn::k3xTF32)
+    e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+  else
+    e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+  if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));
   c->launches += 1;
 }
 
-}  // namespace
+}  // namespace rtn_host
 
 // ----------------------------------------------------------------------------
 extern "C" {
@@ -754,8 +490,8 @@ rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order,
     if (max_order == 2) {
       if (m->act == RTN_ACT_RELU)
         throw Error(RTN_EUNSUPPORTED, "mlp hessian: relu networks are not twice differentiable");
-      if (m->n_in != rtn::kNin2 || m->n_out > rtn::kMaxOut)
-        throw Error(RTN_EUNSUPPORTED, "second-order device path is built for 17 inputs (quadrotor z = [x; u])");
+      if (m->n_in > rtn::kMaxIn2)
+        throw Error(RTN_EUNSUPPORTED, "second-order device path supports at most 31 inputs (1 + n_in carrier rows <= 32)");
     }
     CUDA_CHECK(cudaSetDevice(m->device));
     std::unique_ptr<rtn_ctx> c(new rtn_ctx());
@@ -811,7 +547,10 @@ rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* calls, unsigne
   });
 }
 
-static void EnsureStaging(rtn_ctx* c) {
+}  // extern "C"
+
+namespace rtn_host {
+void EnsureStaging(rtn_ctx* c) {
   if (c->h_z) return;
   const rtn_model* m = c->model;
   const size_t zr = sizeof(double) * m->n_in, fr = sizeof(double) * m->n_out, jr = fr * m->n_in;
@@ -821,7 +560,7 @@ static void EnsureStaging(rtn_ctx* c) {
   if (c->max_order >= 2) CUDA_CHECK(cudaMallocHost(&c->h_hess, jr * m->n_in * c->max_rows));
 }
 
-static bool IsPinned(const void* p) {
+bool IsPinned(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
@@ -830,7 +569,7 @@ static bool IsPinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-static void CheckCall(const rtn_ctx* c, long long K, int order) {
+void CheckCall(const rtn_ctx* c, long long K, int order) {
   if (!c) throw Error(RTN_ECONFIG, "null context");
   if (order < 0 || order > 2) throw Error(RTN_ECONFIG, "prepare nodes: order must be 0, 1 or 2");
   if (order == 2 && c->model->act == RTN_ACT_RELU)
@@ -838,6 +577,9 @@ static void CheckCall(const rtn_ctx* c, long long K, int order) {
   if (order > c->max_order) throw Error(RTN_EUNSUPPORTED, "order exceeds the context's max_order");
   if (K < 0 || K > c->max_rows) throw Error(RTN_EDOMAIN, "K outside [0, max_rows]");
 }
+}  // namespace rtn_host
+
+extern "C" {
 
 rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int order, double* f, double* jac,
                        double* hess) {
@@ -1026,7 +768,8 @@ void ValidateCfg(const rtn_ocp_config& c) {
 }
 
 rtn::BlkParams MakeBlk(const rtn_quad_params& p, const rtn_ocp_config& c, long long n_inst) {
-  rtn::BlkParams b{};
+  rtn::BlkParams b;
+  std::memset(&b, 0, sizeof b);  // padding too: the struct is compared bytewise as a graph-cache key
   b.n_inst = n_inst;
   b.N = c.horizon;
   b.order = c.taylor_order;
@@ -1295,9 +1038,12 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
     };
     if (c->latency_mode && K <= kGraphMaxRows) {
       const unsigned key = mask | (cycle ? 1u << 31 : 0) | (zc ? 1u << 30 : 0);
+      const void* bufs[4] = {c->h_qin, c->h_qout, c->d_qin, c->d_qout};
       const rtn_ctx::QpGraph* g = nullptr;
       for (const auto& e : c->qp_graphs)
-        if (e.n_inst == n_inst && e.N == N && e.order == order && e.mask == key) g = &e;
+        if (e.n_inst == n_inst && e.N == N && e.order == order && e.mask == key &&
+            std::memcmp(&e.blk, &b, sizeof b) == 0 && std::memcmp(e.bufs, bufs, sizeof bufs) == 0)
+          g = &e;
       if (!g) {
         body(s);  // first run outside capture (kernel attributes, lazy loading)
         CUDA_CHECK(cudaStreamSynchronize(s));
@@ -1311,7 +1057,20 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
         c->launches = l0;  // the capture pass launched nothing
         CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
         CUDA_CHECK(cudaGraphDestroy(graph));
-        c->qp_graphs.push_back({n_inst, N, order, key, exec, per});
+        if (c->qp_graphs.size() >= 64) {  // bounded cache
+          cudaGraphExecDestroy(c->qp_graphs.front().exec);
+          c->qp_graphs.erase(c->qp_graphs.begin());
+        }
+        rtn_ctx::QpGraph qg{};
+        qg.n_inst = n_inst;
+        qg.N = N;
+        qg.order = order;
+        qg.mask = key;
+        std::memcpy(&qg.blk, &b, sizeof b);
+        std::memcpy(qg.bufs, bufs, sizeof bufs);
+        qg.exec = exec;
+        qg.kernels = per;
+        c->qp_graphs.push_back(qg);
       } else {
         CUDA_CHECK(cudaGraphLaunch(g->exec, s));
         c->launches += g->kernels;

@@ -16,6 +16,21 @@
 //   kBF16x3 : same split in bf16 (8+8 mantissa bits), three kind::f16 passes
 //             at twice the tf32 rate; operand bytes equal to tf32 mode.
 //
+// 3xTF32 accumulation (PairCfg::kChains): the tensor core adds each K = 8 MMA
+// into its fp32 accumulator with an error proportional to the running sum's
+// ulp, so the error of a 512-deep layer grows with the number of MMAs that
+// land in one accumulator (measured on B200: 192 → 64 → 32 MMAs per chain gave
+// 7e-5 → 2.4e-5 → 1.2e-5 at 12x512, gain 2.5). The hi·hi pass therefore
+// rotates over kChains accumulators by K-chunk (4 where TMEM allows: 16 MMAs
+// per chain), the small hi·lo + lo·hi corrections go to their own accumulator,
+// and the epilogue adds them once in fp32: D0 + ((D1 + D2 + D3) + Dcorr).
+//
+// Order 2 (ORD2): 1 = quadrotor tiles (n_in = 17, compile-time Hessian slot
+// tables, NTC = 48); 2 = generic tiles for any n_in <= 31 (runtime slot table
+// in shared memory). Both carry the node's value + tangent rows (the
+// "carrier") in side-0 rows [0, 1+n_in) and packed Hessian rows (a <= b) in
+// every other row: h' = σ'·(W h)_ab + σ''·(W t_a)(W t_b).
+//
 // Data movement per layer:
 //   weights    : 2-SM TMA tile loads (tensor map, SWIZZLE_128B), each CTA its
 //                128-neuron half (hi and lo tiles in split modes), bytes
@@ -34,13 +49,12 @@
 
 namespace rtn {
 
-constexpr int kTmemStride2 = 160;     // TMEM columns per 256-neuron block (pair N ≤ 160)
 constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x 128 B
 
 // NTC = operand row stride per CTA (max rows per CTA): 80 for throughput
-// tiles (P = 4 quadrotor nodes = 72 rows; P = 2 in 3xTF32 at width 512),
-// 24 for latency tiles (P = 1).
-template <int WP, int NSTAGE, int P, int NTC, int MODE, bool ORD2 = false>
+// tiles (P = 4 quadrotor nodes = 72 rows), 24 for latency tiles (P = 1) and
+// for 3xTF32 at width 512, 48 / 24 / 40 for order-2 tiles.
+template <int WP, int NSTAGE, int P, int NTC, int MODE, int ORD2 = 0>
 struct PairCfg {
   static constexpr int kEB = MODE == kBF16x3 ? 2 : 4;  // operand element bytes
   static constexpr int kCK = 128 / kEB;                // k per 128-byte chunk row
@@ -58,70 +72,71 @@ struct PairCfg {
   static constexpr uint32_t kNumBars = 2 * NSTAGE + 13;
   static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
   static constexpr uint32_t kZsOff = kMiscOff + 16;
-  static constexpr uint32_t kSmemBytes = kZsOff + 2 * NTC * 4 + 1024;
-  // 3xTF32: correction passes accumulate in their own TMEM columns (rtn_kernel.cuh
-  // RTN_MMA12): block mb's D2 at kCorrBase + mb·kCorrStride, the output layer's at 16.
+  // generic order 2: per-thread tangent rows T_a (2 halves x 32 x 128 fp32) and the slot → (a, b) table
+  static constexpr uint32_t kTsOff = (kZsOff + 2 * NTC * 4 + 15) & ~15u;
+  static constexpr uint32_t kTsBytes = ORD2 == 2 ? 2 * 32 * 128 * 4 : 0;
+  static constexpr uint32_t kAbOff = kTsOff + kTsBytes;
+  static constexpr uint32_t kAbBytes = ORD2 == 2 ? 512 * 2 : 0;
+  static constexpr uint32_t kSmemBytes = kAbOff + kAbBytes + 1024;
+  // TMEM: 256-neuron block mb at column mb·kBlkCols; inside it kChains main
+  // accumulators of kN = 2·NTC columns, then (3xTF32) the correction accumulator.
+  static constexpr int kN = 2 * NTC;
   static constexpr bool kCorr = MODE == k3xTF32;
-  static constexpr int kCorrBase = kNMB * kTmemStride2, kCorrStride = 96;
-  // ... and the main (hi·hi) pass alternates between two accumulators by chunk
-  // parity (D for even chunks, D3 = D + kMain2Off for odd), which halves the
-  // accumulation chain of each; order 2 (N = 96) has no TMEM room for D3.
-  static constexpr bool kSplitMain = kCorr && !ORD2 && (kNMB == 1 ? 2 * NTC <= 160 : 2 * NTC <= 80);
-  static constexpr int kMain2Off = kNMB == 2 ? 80 : 320;
+  static constexpr int kBlkCols = 512 / kNMB;
+  static constexpr int kChains = !kCorr ? 1 : (5 * kN <= kBlkCols ? 4 : (3 * kN <= kBlkCols ? 2 : 1));
+  static constexpr int kCorrOff = kChains * kN;
   static_assert(kNMB >= 1 && kNMB <= 2, "pair kernel handles 256 or 512 padded width");
-  static_assert(kNMB * kTmemStride2 <= 512, "TMEM capacity");
-  static_assert(!kCorr || kCorrBase + (kNMB - 1) * kCorrStride + 2 * NTC <= 512, "TMEM capacity (correction D2)");
-  static_assert(!kCorr || kNMB == 1 || 2 * NTC <= kCorrStride, "correction blocks must not overlap");
+  static_assert(kN % 16 == 0 && kN <= 256, "pair MMA N");
+  static_assert((kChains + (kCorr ? 1 : 0)) * kN <= kBlkCols, "TMEM capacity");
+  static_assert(5 * 16 <= kBlkCols, "output-layer accumulators");
   static_assert(kSmemBytes <= 232448, "shared memory budget");
   static_assert(kStagesPerMB % NSTAGE == 0, "every 256-block starts at stage 0 (static stage indices)");
   // the output layer's M = 128-row A reads run past the last chunk into the stage ring
   static_assert((128 - NTC) * 128 <= NSTAGE * kStageBytes, "A-operand overrun must stay in smem");
 };
 
-// v[0..n) += TMEM columns [taddr, taddr + n) of this thread's lane (3xTF32
-// correction accumulator D2), 16 columns per round trip, columns >= lim skipped.
-template <int N>
-__device__ __forceinline__ void tmem_add_cols(uint32_t taddr, float* v, int lim) {
+// v[0..N) = this lane's accumulator columns [t, t + N) summed over the main
+// chains (t + c·kN) and the 3xTF32 correction accumulator (t + kCorrOff) —
+// v = D0 + ((D1 + D2 + D3) + Dcorr) — 16 columns per round trip; columns
+// >= lim are not read. `stride` is kN for hidden blocks, 16 for the output layer.
+template <class C, int N>
+__device__ __forceinline__ void tmem_read_acc(uint32_t t, float* v, int lim, uint32_t stride, uint32_t corr_off) {
 #pragma unroll
-  for (int c0 = 0; c0 < N; c0 += 16) {
-    if (c0 >= lim) break;
-    float t[16];
-    tmem_ld8(taddr + c0, t);
-    if (c0 + 8 < N && c0 + 8 < lim) tmem_ld8(taddr + c0 + 8, t + 8);
-    tmem_ld_wait();
+  for (int c0 = 0; c0 < N; c0 += 8)
+    if (c0 < lim) tmem_ld8(t + c0, v + c0);
+  tmem_ld_wait();
+  constexpr int kExtra = C::kChains - 1 + (C::kCorr ? 1 : 0);
+  if constexpr (kExtra > 0) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (c0 + i < N && c0 + i < lim) v[c0 + i] += t[i];
-  }
-}
-
-// v[0..n) += (TMEM columns at ta) + (TMEM columns at tb): both 3xTF32 extra
-// accumulators (D3, D2) per round trip.
-template <int N>
-__device__ __forceinline__ void tmem_add2_cols(uint32_t ta, uint32_t tb, float* v, int lim) {
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      if (c0 >= lim) break;
+      float x[kExtra][16];
 #pragma unroll
-  for (int c0 = 0; c0 < N; c0 += 16) {
-    if (c0 >= lim) break;
-    float x[16], y[16];
-    tmem_ld8(ta + c0, x);
-    tmem_ld8(tb + c0, y);
-    if (c0 + 8 < N && c0 + 8 < lim) {
-      tmem_ld8(ta + c0 + 8, x + 8);
-      tmem_ld8(tb + c0 + 8, y + 8);
+      for (int e = 0; e < kExtra; ++e) {
+        const uint32_t te = t + (e < C::kChains - 1 ? (e + 1) * stride : corr_off) + c0;
+        tmem_ld8(te, x[e]);
+        if (c0 + 8 < N && c0 + 8 < lim) tmem_ld8(te + 8, x[e] + 8);
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (c0 + i < N && c0 + i < lim) {
+          float s = x[0][i];
+#pragma unroll
+          for (int e = 1; e < kExtra; ++e) s += x[e][i];
+          v[c0 + i] += s;
+        }
+      }
     }
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (c0 + i < N && c0 + i < lim) v[c0 + i] += x[i] + y[i];
   }
 }
 
-template <int WP, int NSTAGE, int P, int NTC, int MODE, bool ORD2 = false>
+template <int WP, int NSTAGE, int P, int NTC, int MODE, int ORD2 = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_pair_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
   using C = PairCfg<WP, NSTAGE, P, NTC, MODE, ORD2>;
-  static_assert(!ORD2 || NTC == kNtc2, "order-2 tiles are 2 x 48 rows");
+  static_assert(ORD2 != 1 || NTC == kNtc2, "quadrotor order-2 tiles are 2 x 48 rows");
   constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG, SPLIT = C::kSplit, CPG = C::kCPG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -162,6 +177,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_l);
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  if constexpr (ORD2 == 2) {  // slot → (a, b) table of the packed upper triangle
+    uint16_t* ab = reinterpret_cast<uint16_t*>(smem + C::kAbOff);
+    const int np = n_in * (n_in + 1) / 2;
+    for (int p = threadIdx.x; p < np; p += blockDim.x) {
+      const PairAB q = pair_ab(p, n_in);
+      ab[p] = static_cast<uint16_t>(q.a | (q.b << 8));
+    }
+    __syncthreads();
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -244,19 +268,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                    smem_u32(&empty[st1]), bar2);
         }
       };
-      // main-pass accumulator of chunk c, and the accumulate flags (TF32: a bool;
-      // split modes: bit 0 main, bit 1 correction — see RTN_MMA12)
-      auto split_d = [&](uint32_t d, int c) { return C::kSplitMain && (c & 1) ? d + C::kMain2Off : d; };
-      auto split_acc = [&](int c) -> uint32_t {
+      // main-pass accumulator of chunk c (rotating over kChains), and the
+      // accumulate flags (TF32: a bool; split modes: bit 0 main, bit 1 correction)
+      auto chain_acc = [&](int c) -> uint32_t {
         if constexpr (MODE == kTF32) return c != 0;
-        else return (c >= (C::kSplitMain ? 2 : 1) ? 1u : 0u) | (c != 0 ? 2u : 0u);
+        else return (c >= C::kChains ? 1u : 0u) | (c != 0 ? 2u : 0u);
       };
       for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
         for (int l = 0; l < n_mma_layers; ++l) {
 #pragma unroll 1
           for (int mb = 0; mb < NMB; ++mb) {
-            const uint32_t d = tmem_base + mb * kTmemStride2;
-            const uint32_t d2 = C::kCorr ? tmem_base + C::kCorrBase + mb * C::kCorrStride : d;
+            const uint32_t d = tmem_base + mb * C::kBlkCols;
+            const uint32_t d2 = C::kCorr ? d + C::kCorrOff : d;
             if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2] = globaltimer();
 #pragma unroll
             for (int c = 0; c < NKC; ++c) {
@@ -267,8 +290,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tc_fence_after();
               // extra commit: in_free after the last block consumed K-group c/CPG
               const uint32_t bar2 = (mb == NMB - 1 && (c % CPG) == CPG - 1) ? smem_u32(&in_free[c / CPG]) : 0u;
-              chunk_mma(split_d(d, c), d2, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD,
-                        b0 + kSplitD + c * kChunkD, idesc_h, split_acc(c), bar2, true);
+              chunk_mma(d + (c % C::kChains) * C::kN, d2, a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1,
+                        b0 + c * kChunkD, b0 + kSplitD + c * kChunkD, idesc_h, chain_acc(c), bar2, true);
               if (st1 == NSTAGE - 1) ph ^= 1;
             }
             mma_commit_pair(&tmem_full[mb]);
@@ -276,7 +299,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           ++ar;
         }
-        // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]; M = 2 x 128 rows, N = 16
+        // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]; M = 2 x 128 rows, N = 16;
+        // main chains at columns 16·c, the correction accumulator at 16·kChains
 #pragma unroll
         for (int c = 0; c < NKC; ++c) {
           const int st0 = (c * SPLIT) % NSTAGE, st1 = (c * SPLIT + SPLIT - 1) % NSTAGE;
@@ -284,9 +308,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full[st0], ph);
           if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
           tc_fence_after();
-          chunk_mma(C::kSplitMain && (c & 1) ? tmem_base + 32 : tmem_base, C::kCorr ? tmem_base + 16 : tmem_base,
+          chunk_mma(tmem_base + (c % C::kChains) * 16, C::kCorr ? tmem_base + 16 * C::kChains : tmem_base,
                     a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD, b0 + kSplitD + c * kChunkD,
-                    idesc_o, split_acc(c), 0u, false);
+                    idesc_o, chain_acc(c), 0u, false);
           if (st1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_pair(tmem_last);
@@ -294,50 +318,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-   if constexpr (ORD2) {
-    // ===================== order-2 epilogue ==================================
-    // Pair-tile t holds node t/2, Hessian group g = t%2: side 0 rows 0..17 are
-    // the carrier (value + 17 tangents), side-0 rows 18..47 and side-1 rows
-    // 0..47 are packed Hessian rows g·78 + slot. Every thread sees all 96
-    // columns of its neuron in TMEM, so the carrier's pre-activations (value,
-    // tangents T_a) are at hand for h' = σ'·H + σ''·T_a·T_b.
+    // ===================== epilogue (8 warps per CTA) ========================
+    // Thread = one neuron (TMEM lane) of this CTA's 128-neuron half of a
+    // 256-block; warp half h owns the rows of side h (the nodes whose operand
+    // rows live in CTA h), i.e. TMEM columns [h·ntc, (h+1)·ntc). Results stay
+    // in registers until the layer's last block has consumed the input group
+    // they overwrite (in_free), then go straight to the owning CTA's shared
+    // memory (DSMEM for the peer side).
     const int half = (warp - 4) >> 2;
     const int q = warp & 3;
     const int tid_h = q * 32 + lane;
     const int etid = threadIdx.x - 128;
     const int act = prm.act;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    // Row r of a K-major SW128 operand lives at  col + (r/8)·1024 + (r%8)·128
+    // + ((u ^ r%8) − u)·16  relative to row 0 of this thread's neuron column,
+    // with u the neuron's 16-byte unit inside its 128-byte chunk row.
     const int u = ((tid_h * C::kEB) >> 4) & 7;
     int swz[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) swz[i] = ((u ^ i) - u) * 16 + i * 128;
     const uint32_t act_local = smem_u32(act_s);
-    const bool local_side = half == static_cast<int>(rank);
+    const bool local_side = half == static_cast<int>(rank) || (prm.dbg & 8);  // dbg 8: timing only
     const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
     uint32_t ready_cl[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);
     uint32_t hl = 0, tiles_done = 0;
-    using Seq0 = std::make_integer_sequence<int, kNtc2 - kCarrier2>;  // side-0 Hessian slots
-    using Seq1 = std::make_integer_sequence<int, kNtc2>;              // side-1 Hessian slots
 
+    // Store one neuron column (rows 0..ntc-1) of one side into its operand
+    // buffer(s), rounding / splitting per precision mode.
     auto store_side = [&](const float* v, int j) {
       const uint32_t base =
           side_base + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) + ((j * C::kEB) & 15);
 #pragma unroll
       for (int i = 0; i < NTC; ++i) {
+        if ((i & ~7) >= ntc) continue;
         const uint32_t a = base + (i >> 3) * 1024 + swz[i & 7];
         if constexpr (MODE == kTF32) {
-          if (local_side) st_shared_f32(a, to_tf32(v[i]));
-          else st_cluster_f32(a, to_tf32(v[i]));
+          const float h = to_tf32(v[i]);
+          if (local_side) st_shared_f32(a, h);
+          else st_cluster_f32(a, h);
         } else if constexpr (MODE == k3xTF32) {
-          const float h = to_tf32(v[i]), lo = to_tf32(v[i] - h);
-          if (local_side) { st_shared_f32(a, h); st_shared_f32(a + C::kSplitStride, lo); }
-          else { st_cluster_f32(a, h); st_cluster_f32(a + C::kSplitStride, lo); }
+          const float h = to_tf32(v[i]);
+          const float lo = to_tf32(v[i] - h);
+          if (local_side) {
+            st_shared_f32(a, h);
+            st_shared_f32(a + C::kSplitStride, lo);
+          } else {
+            st_cluster_f32(a, h);
+            st_cluster_f32(a + C::kSplitStride, lo);
+          }
         } else {
-          const uint16_t h = bf16_rn_bits(v[i]), lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
-          if (local_side) { st_shared_u16(a, h); st_shared_u16(a + C::kSplitStride, lo); }
-          else { st_cluster_u16(a, h); st_cluster_u16(a + C::kSplitStride, lo); }
+          const uint16_t h = bf16_rn_bits(v[i]);
+          const uint16_t lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
+          if (local_side) {
+            st_shared_u16(a, h);
+            st_shared_u16(a + C::kSplitStride, lo);
+          } else {
+            st_cluster_u16(a, h);
+            st_cluster_u16(a + C::kSplitStride, lo);
+          }
         }
       }
     };
@@ -346,6 +387,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(ready_cl[grp]);
     };
+    // output-layer accumulator of this lane (row), columns = outputs
+    auto read_out = [&](float* o) {
+      tmem_read_acc<C, 16>(tmem_base + lane_base, o, 16, 16u, 16u * C::kChains);
+    };
+
+   if constexpr (ORD2 == 1) {
+    // ===================== order-2 epilogue, quadrotor tiles ===================
+    // Pair-tile t holds node t/2, Hessian group g = t%2: side 0 rows 0..17 are
+    // the carrier (value + 17 tangents), side-0 rows 18..47 and side-1 rows
+    // 0..47 are packed Hessian rows g·78 + slot. Every thread sees all 96
+    // columns of its neuron in TMEM, so the carrier's pre-activations (value,
+    // tangents T_a) are at hand for h' = σ'·H + σ''·T_a·T_b.
+    using Seq0 = std::make_integer_sequence<int, kNtc2 - kCarrier2>;  // side-0 Hessian slots
+    using Seq1 = std::make_integer_sequence<int, kNtc2>;              // side-1 Hessian slots
     // v: this half's 48 rows; T: carrier tangents (pre-activation); hg: Hessian group.
     auto epi_rows = [&](float* v, const float* T, float val, float sp, float spp, int hg) {
       if (half == 0) {
@@ -363,20 +418,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int grp = 2 * mb + static_cast<int>(rank);
       const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
       const float bj = __ldg(prm.bh + l * WP + j);
-      const uint32_t tb = tmem_base + lane_base + mb * kTmemStride2;
+      const uint32_t tb = tmem_base + lane_base + mb * C::kBlkCols;
       mbar_wait_sleep(&tmem_full[mb], hl & 1);
       tc_fence_after();
       float v[kNtc2], car[24];
-#pragma unroll
-      for (int c0 = 0; c0 < kNtc2; c0 += 8) tmem_ld8(tb + half * kNtc2 + c0, v + c0);
-#pragma unroll
-      for (int c0 = 0; c0 < 24; c0 += 8) tmem_ld8(tb + c0, car + c0);
-      tmem_ld_wait();
-      if constexpr (C::kCorr) {
-        const uint32_t tb2 = tmem_base + lane_base + C::kCorrBase + mb * C::kCorrStride;
-        tmem_add_cols<kNtc2>(tb2 + half * kNtc2, v, kNtc2);
-        tmem_add_cols<24>(tb2, car, 24);
-      }
+      tmem_read_acc<C, kNtc2>(tb + half * kNtc2, v, kNtc2, C::kN, C::kCorrOff);
+      tmem_read_acc<C, 24>(tb, car, 24, C::kN, C::kCorrOff);
       tc_fence_before();
       float val, sp, spp;
       act_fwd2(act, car[0] + bj, val, sp, spp);
@@ -428,9 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (half == 0) {
         float o[16];
-        tmem_ld16(tmem_base + lane_base, o);
-        tmem_ld_wait();
-        if constexpr (C::kCorr) tmem_add_cols<16>(tmem_base + lane_base + 16, o, 16);
+        read_out(o);
         const int r = tid_h, n_out = prm.n_out;
         if (node < prm.K && r < kNtc2) {
           if (rank == 0 && r < kCarrier2) {
@@ -456,36 +501,132 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
     }
+   } else if constexpr (ORD2 == 2) {
+    // ===================== order-2 epilogue, generic tiles (n_in <= 31) ========
+    // Same recurrence with the slot → (a, b) map read from the shared table and
+    // the carrier tangents T_a parked in this thread's private shared-memory
+    // column (Ts[half][a][tid_h]; registers cannot be indexed at run time).
+    constexpr int kCar = NTC < 32 ? NTC : 32;  // carrier columns read (1 + n_in <= kCar)
+    const uint16_t* ab_s = reinterpret_cast<const uint16_t*>(smem + C::kAbOff);
+    float* ts = reinterpret_cast<float*>(smem + C::kTsOff) + half * 32 * 128 + tid_h;  // ts[a·128]
+    const int car_rows = 1 + n_in, slots = 2 * NTC - car_rows, np = n_in * (n_in + 1) / 2;
+    const int G = prm.ord2_g;
+    // packed pair of row i of this half in group hg (-1: carrier row or padding)
+    auto pair_of = [&](int i, int hg) -> int {
+      const int s = half == 0 ? i - car_rows : NTC - car_rows + i;
+      const int p = hg * slots + s;
+      return (s >= 0 && p < np) ? p : -1;
+    };
+    // rows of this half: carrier (half 0) from (val, sp·t), Hessian rows
+    // h' = σ'·h + σ''·T_a·T_b (h = 0 and T = W0' columns at layer 0)
+    auto epi_rows = [&](float* v, const float* tcar, float val, float sp, float spp, int hg, bool first) {
+#pragma unroll
+      for (int i = 0; i < NTC; ++i) {
+        if (half == 0 && i < car_rows) {
+          constexpr int kLast = kCar - 2;  // car_rows <= kCar: tcar index i - 1 <= kCar - 2
+          const int ti = i == 0 ? 0 : (i - 1 < kLast ? i - 1 : kLast);  // compile-time once unrolled
+          v[i] = i == 0 ? val : sp * tcar[ti];
+        } else {
+          const int p = pair_of(i, hg);
+          if (p >= 0) {
+            const uint32_t abv = ab_s[p];
+            const float t2 = ts[(abv & 0xff) * 128] * ts[(abv >> 8) * 128];
+            v[i] = first ? spp * t2 : fmaf(spp, t2, sp * v[i]);
+          } else {
+            v[i] = 0.0f;
+          }
+        }
+      }
+    };
+    auto do_block = [&](int mb, int l, int hg) {
+      const int grp = 2 * mb + static_cast<int>(rank);
+      const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
+      const float bj = __ldg(prm.bh + l * WP + j);
+      const uint32_t tb = tmem_base + lane_base + mb * C::kBlkCols;
+      mbar_wait_sleep(&tmem_full[mb], hl & 1);
+      tc_fence_after();
+      float v[NTC], car[kCar];
+      tmem_read_acc<C, NTC>(tb + half * NTC, v, NTC, C::kN, C::kCorrOff);
+      tmem_read_acc<C, kCar>(tb, car, car_rows, C::kN, C::kCorrOff);
+      tc_fence_before();
+      float val, sp, spp;
+      act_fwd2(act, car[0] + bj, val, sp, spp);
+#pragma unroll
+      for (int a = 0; a + 1 < kCar; ++a)
+        if (a < n_in) ts[a * 128] = car[1 + a];
+      epi_rows(v, car + 1, val, sp, spp, hg, false);
+      mbar_wait_sleep(&in_free[grp], hl & 1);
+      store_side(v, j);
+      publish(grp);
+    };
+
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
+      const long long node = tile / G;
+      const int hg = static_cast<int>(tile - node * G);
+      if (tiles_done > 0) {
+        mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
+        tc_fence_after();
+      }
+      if (etid < n_in) zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, etid)) : 0.0f;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // ---- layer 0: v = σ(pre), t_a = σ'·W0'[:,a], h_ab = σ''·W0'[:,a]·W0'[:,b]
+      for (int g = static_cast<int>(rank); g < NG; g += 2) {
+        const int j = g * 128 + tid_h;
+        float w[kCar];
+        float pre = __ldg(prm.b0 + j);
+#pragma unroll
+        for (int k = 0; k < kCar; ++k) {
+          w[k] = k < n_in ? __ldg(prm.w0 + j * n_in + k) : 0.0f;
+          if (k < n_in) {
+            pre = fmaf(w[k], zs[k], pre);
+            ts[k * 128] = w[k];
+          }
+        }
+        float val, sp, spp;
+        act_fwd2(act, pre, val, sp, spp);
+        float v[NTC];
+        epi_rows(v, w, val, sp, spp, hg, true);
+        store_side(v, j);
+        publish(g);
+      }
+      for (int l = 0; l < n_mma_layers; ++l, ++hl)
+        for (int mb = 0; mb < NMB; ++mb) do_block(mb, l, hg);
+      // ---- output layer: lane = this CTA side's row; columns = outputs
+      mbar_wait_sleep(tmem_last, tiles_done & 1);
+      tc_fence_after();
+      if (half == 0) {
+        float o[16];
+        read_out(o);
+        const int r = tid_h, n_out = prm.n_out;
+        if (node < prm.K && r < NTC) {
+          if (rank == 0 && r < car_rows) {
+            if (hg == 0) {
+              if (r == 0)
+                for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+              else
+                for (int oo = 0; oo < n_out; ++oo) prm.jac[(node * n_out + oo) * n_in + (r - 1)] = static_cast<double>(o[oo]);
+            }
+          } else {
+            const int s = rank == 0 ? r - car_rows : NTC - car_rows + r;
+            const int p = hg * slots + s;
+            if (p < np && prm.hess != nullptr) {
+              const uint32_t abv = ab_s[p];
+              const int a = abv & 0xff, b = abv >> 8;
+              for (int oo = 0; oo < n_out; ++oo) {
+                double* h = prm.hess + (node * n_out + oo) * n_in * n_in;
+                h[a * n_in + b] = static_cast<double>(o[oo]);
+                h[b * n_in + a] = static_cast<double>(o[oo]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+    }
    } else if (!(prm.dbg & 128)) {
-    // ===================== epilogue (8 warps per CTA) ========================
-    // Thread = one neuron (TMEM lane) of this CTA's 128-neuron half of a
-    // 256-block; warp half h owns the rows of side h (the P nodes whose
-    // operand rows live in CTA h), i.e. TMEM columns [h·ntc, (h+1)·ntc).
-    // Results stay in registers until the layer's last block has consumed
-    // the input group they overwrite (in_free), then go straight to the
-    // owning CTA's shared memory (DSMEM for the peer side).
-    const int half = (warp - 4) >> 2;
-    const int q = warp & 3;
-    const int tid_h = q * 32 + lane;
-    const int etid = threadIdx.x - 128;
-    const int act = prm.act;
+    // ===================== order-1 epilogue ===================================
     const int rows_used = P * (1 + n_in);   // rows per side
     const bool no_pad = rows_used == ntc;
-    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    // Row r of a K-major SW128 operand lives at  col + (r/8)·1024 + (r%8)·128
-    // + ((u ^ r%8) − u)·16  relative to row 0 of this thread's neuron column,
-    // with u the neuron's 16-byte unit inside its 128-byte chunk row.
-    const int u = ((tid_h * C::kEB) >> 4) & 7;
-    int swz[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) swz[i] = ((u ^ i) - u) * 16 + i * 128;
-    const uint32_t act_local = smem_u32(act_s);
-    const bool local_side = half == static_cast<int>(rank) || (prm.dbg & 8);  // dbg 8: timing only
-    const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
-    uint32_t ready_cl[4];
-#pragma unroll
-    for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);
-    uint32_t hl = 0, tiles_done = 0;
 
     // Activation epilogue on one side's rows (fp32): value rows → σ(pre+b),
     // tangent rows → σ'(pre)·t, padding → 0.
@@ -503,54 +644,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int i = P; i < NTC; ++i) v[i] = i < rows_used ? v[i] * sp[i % P] : 0.0f;
       }
     };
-    // Store one neuron column (rows 0..ntc-1) of one side into its operand
-    // buffer(s), rounding / splitting per precision mode.
-    auto store_side = [&](const float* v, int j) {
-      const uint32_t base =
-          side_base + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) + ((j * C::kEB) & 15);
-#pragma unroll
-      for (int i = 0; i < NTC; ++i) {
-        if ((i & ~7) >= ntc) continue;
-        const uint32_t a = base + (i >> 3) * 1024 + swz[i & 7];
-        if constexpr (MODE == kTF32) {
-          const float h = to_tf32(v[i]);
-          if (local_side) st_shared_f32(a, h);
-          else st_cluster_f32(a, h);
-        } else if constexpr (MODE == k3xTF32) {
-          const float h = to_tf32(v[i]);
-          const float lo = to_tf32(v[i] - h);
-          if (local_side) {
-            st_shared_f32(a, h);
-            st_shared_f32(a + C::kSplitStride, lo);
-          } else {
-            st_cluster_f32(a, h);
-            st_cluster_f32(a + C::kSplitStride, lo);
-          }
-        } else {
-          const uint16_t h = bf16_rn_bits(v[i]);
-          const uint16_t lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
-          if (local_side) {
-            st_shared_u16(a, h);
-            st_shared_u16(a + C::kSplitStride, lo);
-          } else {
-            st_cluster_u16(a, h);
-            st_cluster_u16(a + C::kSplitStride, lo);
-          }
-        }
-      }
-    };
-    auto publish = [&](int grp) {
-      fence_proxy_async_cluster();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ready_cl[grp]);
-    };
     // Hidden block mb: TMEM (this CTA's 128 neurons, this half's side) →
     // registers → epilogue → operand buffer of K-group 2·mb + rank.
     auto do_block = [&](int mb, int l) {
       const int grp = 2 * mb + static_cast<int>(rank);
       const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
       const float bj = __ldg(prm.bh + l * WP + j);
-      const uint32_t ts = tmem_base + lane_base + mb * kTmemStride2 + half * ntc;
+      const uint32_t ts = tmem_base + lane_base + mb * C::kBlkCols + half * ntc;
       mbar_wait_sleep(&tmem_full[mb], hl & 1);
       tc_fence_after();
       const bool tr = prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0;
@@ -563,15 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         return;
       }
       float v[NTC];
-#pragma unroll
-      for (int c0 = 0; c0 < NTC; c0 += 8)
-        if (c0 < ntc) tmem_ld8(ts + c0, v + c0);
-      tmem_ld_wait();
-      if constexpr (C::kSplitMain)
-        tmem_add2_cols<NTC>(ts + C::kMain2Off, tmem_base + lane_base + C::kCorrBase + mb * C::kCorrStride + half * ntc,
-                            v, ntc);
-      else if constexpr (C::kCorr)
-        tmem_add_cols<NTC>(tmem_base + lane_base + C::kCorrBase + mb * C::kCorrStride + half * ntc, v, ntc);
+      tmem_read_acc<C, NTC>(ts, v, ntc, C::kN, C::kCorrOff);
       tc_fence_before();
       scale_side(v, bj);
       mbar_wait_sleep(&in_free[grp], hl & 1);
@@ -641,10 +733,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0) prm.trace[194 + rank] = globaltimer();
       if (half == 0) {
         float o[16];
-        tmem_ld16(tmem_base + lane_base, o);
-        tmem_ld_wait();
-        if constexpr (C::kSplitMain) tmem_add2_cols<16>(tmem_base + lane_base + 32, tmem_base + lane_base + 16, o, 16);
-        else if constexpr (C::kCorr) tmem_add_cols<16>(tmem_base + lane_base + 16, o, 16);
+        read_out(o);
         const int r = tid_h;
         const int n_out = prm.n_out;
         const long long nbase = node0 + static_cast<long long>(rank) * P;

@@ -26,16 +26,7 @@ cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CU
 
 cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
                              cudaStream_t st) {
-  using Cfg = PairCfg<512, 8, 1, 24, kBF16x3, false>;
-  auto kern = rtn_quad_kernel<8, 24, kBF16x3>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
-  return cudaGetLastError();
+  return LaunchQuadT<8, 24, kBF16x3>(prm, th, tl, grid, st);
 }
 
 }  // namespace rtn

@@ -4,19 +4,26 @@
 
 #include "rtn_launch.h"
 #include "rtn_pair.cuh"
+#include "rtn_quad.cuh"
 
 namespace rtn {
 
-template <int WP, int NS, int P, int NTC, int MODE, bool ORD2 = false>
+template <int WP, int NS, int P, int NTC, int MODE, int ORD2 = 0>
 cudaError_t LaunchPairT(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
   using Cfg = PairCfg<WP, NS, P, NTC, MODE, ORD2>;
   auto kern = rtn_pair_kernel<WP, NS, P, NTC, MODE, ORD2>;
-  static bool attr_set = false;  // per instantiation, per process
-  if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
+  return cudaGetLastError();
+}
+
+template <int NS, int NTC, int MODE>
+cudaError_t LaunchQuadT(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
+  using Cfg = PairCfg<512, NS, 1, NTC, MODE, 0>;
+  auto kern = rtn_quad_kernel<NS, NTC, MODE>;
+  const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
   return cudaGetLastError();
 }

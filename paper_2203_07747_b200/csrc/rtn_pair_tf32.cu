@@ -1,6 +1,6 @@
-// Pair-kernel instantiations, TF32 mode (one kind::tf32 pass).
+// Pair-kernel instantiations, TF32 mode (one kind::tf32 pass), plus the TF32
+// quad (latency) and rows (width-256 throughput) kernels.
 #include "rtn_pair_launch.cuh"
-#include "rtn_pingpong.cuh"
 #include "rtn_quad.cuh"
 #include "rtn_rows.cuh"
 
@@ -31,50 +31,24 @@ cudaError_t LaunchPairTF32(const KParams& prm, const CUtensorMap& th, const CUte
 }
 
 cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
-  using Cfg = PairCfg<512, 8, 1, 24, kTF32, false>;
-  auto kern = rtn_quad_kernel<8, 24>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
-  return cudaGetLastError();
-}
-
-cudaError_t LaunchPingPongTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
-                               cudaStream_t st) {
-  using Cfg = PingCfg<4, 4, 80>;
-  auto kern = rtn_pingpong_kernel<4, 4, 80>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
-  return cudaGetLastError();
+  return LaunchQuadT<8, 24, kTF32>(prm, th, tl, grid, st);
 }
 
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
   using Cfg = RowsCfg<6>;
   auto kern = prm.act == 0 ? rtn_rows_kernel<6, 0> : (prm.act == 1 ? rtn_rows_kernel<6, 1> : rtn_rows_kernel<6, 2>);
-  static bool attr_set[3] = {false, false, false};
-  const int a = prm.act < 0 || prm.act > 2 ? 2 : prm.act;
-  if (!attr_set[a]) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set[a] = true;
-  }
+  const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
   return cudaGetLastError();
 }
 
-// Geometry for every mode lives here (host-only logic).
+// Geometry for every mode lives here (host-only logic). 3xTF32 at width 512
+// always takes the 24-row tile: its TMEM fits four main accumulators per
+// 256-neuron block (rtn_pair.cuh, kChains), which keeps the mode within 1e-5.
 PairGeom PairGeometry(int mode, int wp, bool latency, int n_in) {
-  if (latency) return {1, 24};
-  const int ntc = (mode == k3xTF32 && wp == 512) ? 40 : 80;
+  if (latency || (mode == k3xTF32 && wp == 512)) return {1, 24};
+  const int ntc = 80;
   int p = mode == kTF32 ? 16 : 4;
   while (p > 1 && p * (1 + n_in) > ntc) p >>= 1;
   return {p, ntc};

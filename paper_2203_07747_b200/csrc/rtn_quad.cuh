@@ -1,7 +1,7 @@
 // rtn_quad.cuh — latency kernel on 4-CTA clusters (two CTA pairs), order 1,
 // TF32, bf16x3 or 3xTF32 (MODE; hi/lo operand split as in rtn_pair.cuh, 3
-// passes; 3xTF32 with the split accumulators D/D3 (main pass by chunk parity)
-// and D2 (corrections) at TMEM columns 0, 64, 128).
+// passes; 3xTF32 with the main pass rotating over PairCfg::kChains = 4
+// accumulators by K-chunk and the corrections in a fifth, rtn_pair.cuh).
 //
 // Why: at one MPC step (K = N nodes) the pair kernel gives each 2-node
 // cluster the WHOLE weight stream; every SM pushes ~5.8 MB of 12x512 weights
@@ -137,10 +137,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_quad_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
                     const __grid_constant__ CUtensorMap tmap_l) {
   constexpr int WP = 512, P = 1;
-  // 3xTF32 accumulators (N = 2·NTC <= 64 columns each): D, D3 (odd chunks), D2 (corrections)
-  constexpr uint32_t kD3 = 64, kD2 = 128;
-  static_assert(MODE != k3xTF32 || 2 * NTC <= 64, "3xTF32 accumulators are 64 columns apart");
-  using C = PairCfg<WP, NSTAGE, P, NTC, MODE, false>;
+  using C = PairCfg<WP, NSTAGE, P, NTC, MODE, 0>;
+  // one 256-neuron block per CTA: main chains at c·kN, corrections at kCorrOff (< 256 columns)
+  static_assert((C::kChains + (C::kCorr ? 1 : 0)) * C::kN <= 256, "quad TMEM allocation");
   // tf32: 16 chunks of 32 k, 4 per group; bf16: 8 chunks of 64 k, 2 per group; 4 groups
   constexpr int NKC = C::kNKC, CPG = C::kCPG, NG = C::kNG, SPLIT = C::kSplit, EB = C::kEB;
   static_assert(NG == 4 && (NKC * SPLIT) % NSTAGE == 0, "quad kernel: width 512, whole stage rings per layer");
@@ -233,14 +232,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t wa = a0 + st0 * kStageD, xa = b0 + c * kChunkD;
         if constexpr (MODE == k3xTF32) {
           const uint64_t wb = wa + kStageD, xb = xa + kSplitD;
-          const uint32_t dm = tmem_base + ((i & 1) ? kD3 : 0u);
-          const uint32_t flags = (i >= 2 ? 1u : 0u) | (i != 0 ? 2u : 0u);
+          // hidden layers: chains c·kN, corrections kCorrOff; output layer: 16·c, 16·kChains
+          const uint32_t cs = weights_are_a ? C::kN : 16u, co = weights_are_a ? C::kCorrOff : 16u * C::kChains;
+          const uint32_t dm = tmem_base + (i % C::kChains) * cs;
+          const uint32_t flags = (i >= C::kChains ? 1u : 0u) | (i != 0 ? 2u : 0u);
           (void)acc;
           if (weights_are_a)
-            mma12_tf32_pair_commit_m(dm, tmem_base + kD2, wa, wb, xa, xb, idesc, flags, smem_u32(&empty[st0]),
+            mma12_tf32_pair_commit_m(dm, tmem_base + co, wa, wb, xa, xb, idesc, flags, smem_u32(&empty[st0]),
                                      smem_u32(&empty[st0 + 1]), pair_mask, bar2, mask2);
           else
-            mma12_tf32_pair_commit_m(dm, tmem_base + kD2, xa, xb, wa, wb, idesc, flags, smem_u32(&empty[st0]),
+            mma12_tf32_pair_commit_m(dm, tmem_base + co, xa, xb, wa, wb, idesc, flags, smem_u32(&empty[st0]),
                                      smem_u32(&empty[st0 + 1]), pair_mask, bar2, mask2);
         } else if constexpr (MODE == kTF32) {
           if (weights_are_a)
@@ -376,12 +377,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(&tmem_full[0], l & 1);
       tc_fence_after();
       float v[NTC];
-#pragma unroll
-      for (int c0 = 0; c0 < NTC; c0 += 8)
-        if (c0 < ntc) tmem_ld8(tmem_base + lane_base + half * ntc + c0, v + c0);
-      tmem_ld_wait();
-      if constexpr (MODE == k3xTF32)
-        tmem_add2_cols<NTC>(tmem_base + lane_base + kD3 + half * ntc, tmem_base + lane_base + kD2 + half * ntc, v, ntc);
+      tmem_read_acc<C, NTC>(tmem_base + lane_base + half * ntc, v, ntc, C::kN, C::kCorrOff);
       tc_fence_before();
       float val, sp;
       act_fwd(act, v[0] + bj, val, sp);
@@ -397,9 +393,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(tmem_last, 0);
       tc_fence_after();
       float o[16];
-      tmem_ld16(tmem_base + lane_base, o);
-      tmem_ld_wait();
-      if constexpr (MODE == k3xTF32) tmem_add2_cols<16>(tmem_base + lane_base + kD3, tmem_base + lane_base + kD2, o, 16);
+      tmem_read_acc<C, 16>(tmem_base + lane_base, o, 16, 16u, 16u * C::kChains);
       const int r = tid_h, n_out = prm.n_out;
       const long long nd = node0 + sub;
       if (nd < prm.K) {

@@ -15,18 +15,13 @@ TF32_TOL = 1e-3
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["single", "pair", "pingpong", "latency", "quad", "rows"])
+@pytest.fixture(params=["pair", "latency", "quad", "rows"])
 def kernel(request, monkeypatch):
-    """Every device kernel: single-CTA, CTA-pair throughput (P=4; width 256 uses the two-tile
-    ping-pong variant unless RTN_PINGPONG=0), CTA-pair latency (P=1), the 4-CTA-cluster latency
-    kernel (width-512 TF32 models, K <= 2·(#SMs/4); others fall back) and the width-256
-    rows kernel (activations as the MMA's A operand in TMEM; width 512 falls back)."""
-    if request.param == "pingpong":
-        monkeypatch.setenv("RTN_KERNEL", "pair")
-        monkeypatch.setenv("RTN_PINGPONG", "1")
-    else:
-        monkeypatch.setenv("RTN_KERNEL", request.param)
-        monkeypatch.setenv("RTN_PINGPONG", "0")
+    """Every device kernel: CTA-pair throughput tiles, CTA-pair latency tiles (P=1), the
+    4-CTA-cluster latency kernel (width-512 models, K <= 2·(#SMs/4); others fall back) and
+    the width-256 rows kernel (activations as the MMA's A operand in TMEM; TF32 width-256
+    models with 7 <= n_in <= 31, others fall back)."""
+    monkeypatch.setenv("RTN_KERNEL", request.param)
     return request.param
 
 
@@ -113,23 +108,6 @@ def test_quad_latency_kernel_ragged_and_bitwise(monkeypatch):
     for i in (0, 4, 8):
         one = mlp_batched_eval(pm, z[i:i + 1], EvalOrder.JACOBIAN)
         assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
-
-
-def test_pingpong_width256_matches_pair_kernel_bitwise(monkeypatch):
-    """rtn_pingpong.cuh (two tiles in flight) keeps the pair kernel's accumulation
-    order: results are bit-identical, including odd tile counts (a half-empty pair)."""
-    from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
-    om = OracleModel.random_net([17] + [256] * 5 + [6], "silu", 31)
-    for k in (9, 1184, 2001):
-        z = quad_nodes(4, k)
-        outs = []
-        for pp in ("1", "0"):
-            monkeypatch.setenv("RTN_PINGPONG", pp)
-            monkeypatch.setenv("RTN_KERNEL", "pair")
-            outs.append(mlp_batched_eval(to_product_model(om), z, EvalOrder.JACOBIAN))
-        assert np.array_equal(outs[0].values, outs[1].values) and np.array_equal(outs[0].jacobians, outs[1].jacobians)
-        f, j, _ = om.batched_eval(z, 1)
-        assert max_node_rel_error(outs[0].jacobians, j) < TF32_TOL
 
 
 def test_rows_kernel_input_widths_and_ragged_tiles(monkeypatch):
