@@ -115,6 +115,46 @@ def cpu_throughput(target_s: float, threads: int, sizes=SIZES, seed=SEED):
     return k / dt, f"{inst} instances x {HORIZON} nodes = {k} nodes of cfg5 in {dt:.2f} s", dt
 
 
+def cpu_model() -> str:
+    """CPU model of this host (lscpu's 'Model name', from /proc/cpuinfo)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_latency(sizes, act, seed, k, order, threads, steps):
+    """The reference's per-step approximation on the host (oracle BatchedCore,
+    fp64, RESMPC thread pool; PrepareNodes of one instance = one batched call of
+    K = N nodes): p50/p99 over `steps` calls, like proj/src/bench.cpp:70-87."""
+    import oracle
+    om = oracle.OracleModel.make_mlp(sizes, act, seed)
+    z = oracle.quad_nodes(7, k)
+    om.batched_eval(z, order, threads)  # warm
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        om.batched_eval(z, order, threads)
+        ts.append((time.perf_counter() - t0) * 1e6)
+    ts.sort()
+    return {"p50_us": ts[len(ts) // 2], "p99_us": ts[min(len(ts) - 1, int(len(ts) * 0.99))], "steps": steps,
+            "threads": threads}
+
+
+def cpu_nodes_per_s(sizes, seed, k, threads):
+    """node-lin/s of the oracle's BatchedCore on a bounded sample of k nodes."""
+    import oracle
+    om = oracle.OracleModel.make_mlp(sizes, "silu", seed)
+    z = oracle.quad_nodes(2203, k)
+    om.batched_eval(z[:min(k, 64)], 1, threads)
+    t0 = time.perf_counter()
+    om.batched_eval(z, 1, threads)
+    return k / (time.perf_counter() - t0)
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -136,8 +176,11 @@ def run_reference(args, rank, world):
                    "note": "reference algorithm = oracle/ restatement of proj/src/neural.cpp BatchedCore "
                            "(reverse mode, fp64, fork/join pool); the reference itself needs Eigen/yaml-cpp "
                            "and cannot be built here; ms_per_step extrapolated linearly from the sample"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": samples[-1]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": samples[-1],
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extrapolated": True,
+        "extrapolation": "value is measured on the bounded sample; ms_per_step = the full cfg5 node count / value",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -165,13 +208,16 @@ def measured_tf32_peak(torch):
     return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
 
 
-def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0):
+def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0, act="silu", tf32_peak=None):
     """Per-MPC-step approximation latency: K = N nodes of one instance
-    through rtn_prepare (host z -> host f, J), and device-only (events)."""
+    through rtn_prepare (host z -> host f, J), and device-only (events), with
+    the roofline fraction of the device time (forward-mode FLOPs of the step
+    vs the TF32 tensor peak; the latency kernels are bounded by the serial
+    chain of layers, not by either roofline, so the fraction is small)."""
     import numpy as np
-    from paper_2203_07747_b200 import _lib, make_mlp, synth_quad_nodes
+    from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp, synth_quad_nodes
     from paper_2203_07747_b200.errors import raise_for_status
-    m = make_mlp(sizes, "silu", "full", seed)
+    m = make_mlp(sizes, act, "full", seed)
     eng = m.engine(latency_mode=1, precision=precision)  # graph-captured H2D -> kernel -> D2H per step
     eng._ensure(k, order)
     L = _lib.lib()
@@ -210,18 +256,27 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0):
     raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, None))
     ts.sort()
     dev.sort()
-    return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)], "device_p50_us": dev[len(dev) // 2],
-            "device_p99_us": dev[int(len(dev) * 0.99)], "steps": steps}
+    eng.close()
+    fl = k * flops_per_node(sizes, order)
+    d50 = dev[len(dev) // 2]
+    ach = fl / (d50 * 1e-6) / 1e12
+    return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)], "device_p50_us": d50,
+            "device_p99_us": dev[int(len(dev) * 0.99)], "steps": steps, "nodes": k, "order": order,
+            "precision": ["tf32", "3xtf32", "bf16x3"][precision],
+            "roofline": {"bound": "tensor (serial layer chain)", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
+                         "frac": ach / tf32_peak if tf32_peak else None, "flop_per_step": fl,
+                         "time": "device p50 (CUDA events)"}}
 
 
-def precision_modes(torch, z, k, sizes, steps=2):
+def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
     """Same workload in the split-precision modes (device-resident, 1 warm-up
-    + `steps` timed launches each). Accuracy per mode is pinned by
+    + `steps` timed launches each). Returns the timings and, per mode, a reader
+    of sampled output rows for the parity leg. Accuracy per mode is pinned by
     tests/test_gpu_precision.py."""
     from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp
     from paper_2203_07747_b200.errors import raise_for_status
     L = _lib.lib()
-    out = {}
+    out, runs = {}, {}
     fl = flops_per_node(sizes, 1)
     for name in ("bf16x3", "3xtf32"):
         m = make_mlp(sizes, "silu", "full", SEED)
@@ -241,15 +296,21 @@ def precision_modes(torch, z, k, sizes, steps=2):
             e1.record(st)
         e1.synchronize()
         ms = e0.elapsed_time(e1) / steps
-        out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": k * fl / (ms * 1e-3) / 1e12}
+        ach = k * fl / (ms * 1e-3) / 1e12
+        out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": ach,
+                     "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
+                     "hardware_frac": 3 * ach / tf32_peak if tf32_peak else None,
+                     "kernel": ("rtn_pair_kernel<512,8,1,24,3xTF32> (four main accumulators)" if name == "3xtf32"
+                                else "rtn_pair_kernel<512,4,4,80,bf16x3>")}
         eng.close()
-        del f, j
-    return out
+        runs[name] = (lambda f_, j_: (lambda idx: (f_[idx].cpu().numpy(), j_[idx].cpu().numpy())))(f, j)
+    return out, runs
 
 
-def cfg4_bench(torch, tf32_peak, steps=5):
+def cfg4_bench(torch, tf32_peak, with_cpu=True, steps=5):
     """BASELINE configs[3]: 4096 instances x N=20 x MLP 5x256 SiLU, throughput mode on
-    1 B200, TF32 and 3xTF32 (device-resident, CUDA events on the launching stream)."""
+    1 B200, TF32 and 3xTF32 (device-resident, CUDA events on the launching stream),
+    beside the reference's CPU path (oracle BatchedCore) on a bounded sample."""
     from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp, synth_quad_nodes
     from paper_2203_07747_b200.errors import raise_for_status
     L = _lib.lib()
@@ -280,10 +341,16 @@ def cfg4_bench(torch, tf32_peak, steps=5):
         ach = k * fl / (ms * 1e-3) / 1e12
         out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": ach,
                      "kernel": ("rtn_rows_kernel (activations as the A operand in TMEM, M = 256 rows x N = 256)"
-                                if name == "tf32" else "rtn_pair_kernel<256,4,4,80,3xTF32> (split accumulators)"),
+                                if name == "tf32" else "rtn_pair_kernel<256,4,4,80,3xTF32> (two main accumulators + corrections)"),
                      "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
                      "hardware_frac": (3 if name == "3xtf32" else 1) * ach / tf32_peak if tf32_peak else None}
         eng.close()
+    if with_cpu:
+        threads = os.cpu_count() or 1
+        out["cpu_baseline"] = {"value": cpu_nodes_per_s(sizes, 5256, 8192, threads), "unit": UNIT, "cores": threads,
+                               "value_1thread": cpu_nodes_per_s(sizes, 5256, 2048, 1), "kind": "port",
+                               "sample": "8,192 (all threads) / 2,048 (1 thread) of the 81,920 cfg4 nodes",
+                               "cpu_model": cpu_model()}
     return out
 
 
@@ -458,20 +525,69 @@ def blocks_bench(torch, hbm_peak, steps=5):
             "latency": lat}
 
 
+def parity_leg(torch, eng_dev, z_dev, k, modes_engines, threads):
+    """CPU-baseline leg, checker role: the oracle (fp64 BatchedCore) on a bounded
+    sample of the bench's own nodes and on the conditioned cfg3 net (12x512
+    SiLU, hidden weights x2.5, |J| ~ 2), against the device output of each
+    precision mode. Metric ‖a−b‖∞/(1+‖b‖∞) per node and block
+    (proj/tests/oracles.hpp:30-32), max over the sample."""
+    import numpy as np
+    import oracle
+    from paper_2203_07747_b200 import _lib, make_mlp, synth_quad_nodes
+    from paper_2203_07747_b200.neural import MlpModel
+    idx = np.unique(np.concatenate([np.arange(0, k, max(1, k // 256)), [k - 1]]))
+    z_s = z_dev[torch.from_numpy(idx).to(z_dev.device)].cpu().numpy()
+    om = oracle.OracleModel.make_mlp(SIZES, "silu", SEED)
+    f_ref, j_ref, _ = om.batched_eval(z_s, 1, threads)
+
+    def errs(f, j, fr, jr):
+        return {"f": oracle.max_node_rel_error(f, fr), "A": oracle.max_node_rel_error(j[:, :, :13], jr[:, :, :13]),
+                "B": oracle.max_node_rel_error(j[:, :, 13:], jr[:, :, 13:])}
+
+    # the conditioned net: |J| ~ 2, the case where single-pass TF32 error is visible
+    cn = oracle.OracleModel.random_net(SIZES, "silu", 11, True)
+    for l, (w, b) in enumerate(cn.layers()):
+        if l < len(SIZES) - 2:
+            cn.set_layer(l, w * 2.5, b)
+    z_c = oracle.quad_nodes(2203, 256)
+    fc, jc, _ = cn.batched_eval(z_c, 1, threads)
+    ws, bs = zip(*cn.layers())
+    im, isc, omn, osc = cn.norm()
+    cm = MlpModel(list(SIZES), list(ws), list(bs), "silu", "full", im, isc, omn, osc)
+    out = {}
+    for name, run in modes_engines.items():
+        f, j = run(idx)
+        e_bench = errs(f, j, f_ref, j_ref)
+        got = cm.engine(precision=_lib.PRECISIONS[name]).prepare(z_c, 1)
+        e_cond = errs(got.values, got.jacobians, fc, jc)
+        bound = 1e-5 if name == "3xtf32" else 1e-3
+        out[name] = {"bench_inputs": e_bench, "bench_inputs_max": max(e_bench.values()),
+                     "conditioned_net": e_cond, "conditioned_net_max": max(e_cond.values()),
+                     "north_star_bound": bound,
+                     "meets_bound": {"bench_inputs": max(e_bench.values()) < bound,
+                                     "conditioned_net": max(e_cond.values()) < bound}}
+    cm.invalidate()
+    out["sample"] = (f"{len(idx)} of the {k} bench nodes (MakeMlp seed {SEED}); conditioned net: RandomNet(11) "
+                     "12x512 SiLU hidden weights x2.5 (|J|max ~2.3), 256 quadrotor nodes")
+    out["metric"] = "max over nodes of ||a-b||inf/(1+||b||inf) per block f, A, B vs the fp64 oracle"
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp, synth_quad_nodes
     from paper_2203_07747_b200.errors import raise_for_status
-    from paper_2203_07747_b200.sharding import partition_instances
+    from paper_2203_07747_b200.sharding import Gatherer, all_partitions, partitioned_step
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    part = partition_instances(INSTANCES, HORIZON, rank, world)
-    k = part.num_nodes
+    parts = all_partitions(INSTANCES, HORIZON, world)
+    k = parts[rank].num_nodes
+    counts = [p.num_nodes for p in parts]
     n_in, n_out = SIZES[0], SIZES[-1]
     L = _lib.lib()
 
@@ -485,37 +601,40 @@ def run_ours(args, rank, world, local_rank):
 
     z_host = torch.from_numpy(synth_quad_nodes(2203 + rank, k))
     z = z_host.to(dev)
-    # kernel outputs are the gather send buffers (no extra copy in the step)
-    f = torch.empty((k, n_out), dtype=torch.float64, device=dev)
-    jac = torch.empty((k, n_out, n_in), dtype=torch.float64, device=dev)
-    k_max = partition_instances(INSTANCES, HORIZON, 0, world).num_nodes
     if world > 1:
-        f_send = torch.zeros((k_max, n_out), dtype=torch.float64, device=dev)
-        j_send = torch.zeros((k_max, n_out, n_in), dtype=torch.float64, device=dev)
-        f, jac = f_send[:k], j_send[:k]
-        f_recv = [torch.empty_like(f_send) for _ in range(world)] if rank == 0 else None
-        j_recv = [torch.empty_like(j_send) for _ in range(world)] if rank == 0 else None
+        # the kernel writes straight into the gather send buffers (sharding.Gatherer),
+        # and chunk i's NCCL gather overlaps chunk i+1's kernel (sharding.partitioned_step)
+        gf = Gatherer(counts, (n_out,), torch.float64, dev)
+        gj = Gatherer(counts, (n_out, n_in), torch.float64, dev)
+        f, jac = gf.local, gj.local
+    else:
+        f = torch.empty((k, n_out), dtype=torch.float64, device=dev)
+        jac = torch.empty((k, n_out, n_in), dtype=torch.float64, device=dev)
 
     def launches():
         a, b, c = C.c_ulonglong(), C.c_ulonglong(), C.c_ulonglong()
         L.rtn_ctx_counters(eng.ctx_ptr, C.byref(a), C.byref(b), C.byref(c))
         return c.value
 
-    kern_ms = []
+    zb, fb, jb = n_in * 8, n_out * 8, n_out * n_in * 8
 
-    def step(record_kernel):
-        e0 = e1 = None
+    def step(ev):
+        """One step: all of this rank's nodes (+ the gather of (f, A, B) to rank 0)."""
         with torch.cuda.stream(stream):
-            if record_kernel:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            raise_for_status(L.rtn_prepare_device(eng.ctx_ptr, z.data_ptr(), k, 1, f.data_ptr(), jac.data_ptr(), None))
-            if record_kernel:
-                e1.record(stream)
+            def compute(lo, hi):
+                if ev is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                raise_for_status(L.rtn_prepare_device(eng.ctx_ptr, z.data_ptr() + lo * zb, hi - lo, 1,
+                                                      f.data_ptr() + lo * fb, jac.data_ptr() + lo * jb, None))
+                if ev is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(stream)
+                    ev.append((e0, e1))
             if world > 1:
-                dist.gather(f_send, f_recv, dst=0)
-                dist.gather(j_send, j_recv, dst=0)
-        return (e0, e1)
+                partitioned_step(compute, [gf, gj], k, args.gather_chunks)
+            else:
+                compute(0, k)
 
     def barrier():
         if world > 1:
@@ -523,23 +642,23 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step(False)
+        step(None)
     barrier()
     l0 = launches()
-    ev_pairs = []
+    ev = []
     with ClockSampler(local_rank) as clk:
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            ev_pairs.append(step(True))
+            step(ev)
         t1.record(stream)
         barrier()
     clocks = clk.summary()
     n_launch = launches() - l0
     elapsed = t0.elapsed_time(t1)
-    kern_ms = [a.elapsed_time(b) for a, b in ev_pairs]
+    kern_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps  # kernel time per step (all chunks)
     tmax = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    kmax = torch.tensor([statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+    kmax = torch.tensor([kern_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         dist.all_reduce(kmax, op=dist.ReduceOp.MAX)
@@ -586,34 +705,36 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             pass
         cpu = None
+        modes = None
+        parity = None
+        if world == 1 and not args.no_modes:
+            modes, mode_runs = precision_modes(torch, z, k, SIZES, tf32_peak)
+            mode_runs["tf32"] = lambda idx: (f[idx].cpu().numpy(), jac[idx].cpu().numpy())
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
             v_all, sample, _ = cpu_throughput(12.0, threads)
             v_one, sample1, _ = cpu_throughput(3.0, 1)
             cpu = {"value": v_all, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
-                   "value_1thread": v_one, "sample_1thread": sample1,
+                   "value_1thread": v_one, "sample_1thread": sample1, "cpu_model": cpu_model(),
                    "algorithm": "oracle/ restatement of proj/src/neural.cpp BatchedCore (reverse mode, fp64)"}
-        modes = None
-        if world == 1 and not args.no_modes:
-            modes = precision_modes(torch, z, k, SIZES)
-        lat = None
-        if not args.no_latency:
-            lat = {"cfg3_12x512_N20": latency(torch, SIZES, SEED, 20),
-                   "cfg3_12x512_N20_order2": latency(torch, SIZES, SEED, 20, steps=300, order=2),
-                   "cfg3_12x512_N20_bf16x3": latency(torch, SIZES, SEED, 20, steps=300, precision=2),
-                   "cfg3_12x512_N20_3xtf32": latency(torch, SIZES, SEED, 20, steps=300, precision=1),
-                   "cfg2_5x256_N20": latency(torch, [17] + [256] * 5 + [6], 5256, 20),
-                   "cfg1_2x64_N10": latency(torch, [17, 64, 64, 6], 2064, 10, steps=300)}
-        cfg4 = cfg4_bench(torch, tf32_peak) if world == 1 and not args.no_modes else None
+            if modes is not None:
+                order_ = {"tf32": mode_runs["tf32"], "3xtf32": mode_runs["3xtf32"], "bf16x3": mode_runs["bf16x3"]}
+                parity = parity_leg(torch, eng, z, k, order_, threads)
+        cfg4 = cfg4_bench(torch, tf32_peak, not args.no_cpu) if world == 1 and not args.no_modes else None
         blocks = None
         if world == 1 and not args.no_blocks:
             blocks = blocks_bench(torch, peaks.get("hbm_gbs"))
+        lat = None
+        if not args.no_latency:
+            lat = latency_suite(torch, tf32_peak, with_cpu=world == 1 and not args.no_cpu)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "nodes": total_nodes, "nodes_per_rank": k,
-                       "parallelism": f"instance partition x{world}" + (" + NCCL gather of (f,A,B) to rank 0" if world > 1 else ""),
+                       "parallelism": f"instance partition x{world}" + (
+                           f" + NCCL gather of (f,A,B) to rank 0 in {args.gather_chunks} chunks overlapping the kernel"
+                           if world > 1 else ""),
                        "l2": "inputs larger than L2 (z 446 MB + outputs 2.8 GB per step); weights (11.6 MB) stay L2-resident by design",
                        "io": "fp64 z in, fp64 f/J out (reference layout)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(zp.numel() * 8),
@@ -625,28 +746,61 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                          "frac": achieved / tf32_peak if tf32_peak else None, "traffic": traffic,
                          "peak_source": "cuBLAS tf32 8192^3 burst measured in this run (MEASURED_PEAKS.json has bf16 only; "
-                                        f"bf16/2 = {peaks.get('bf16_tflops', 0) / 2:.1f})",
+                                        f"bf16/2 = {peaks.get('bf16_tflops', 0) / 2:.1f} burst, "
+                                        f"{peaks.get('bf16_tflops_sustained', 0) / 2:.1f} sustained)",
+                         "frac_of_sustained_bf16_half": (achieved / (peaks["bf16_tflops_sustained"] / 2)
+                                                         if peaks.get("bf16_tflops_sustained") else None),
                          "flop_per_node": fl, "flops_definition": "2*(1+n_in)*sum(n_l*n_{l+1}) forward-mode (BASELINE.md s2)",
-                         "kernel": "rtn_pair_kernel<512,4,4> (tcgen05 cta_group::2 tf32)"},
+                         "kernel": "rtn_pair_kernel<512,4,4,80,TF32> (tcgen05 cta_group::2 tf32)"},
             "clocks": clocks,
         }
         if cpu:
             result["cpu_baseline"] = cpu
+        if parity:
+            result["parity"] = parity
         if modes:
             result["precision_modes"] = modes
-        if lat:
-            result["latency"] = lat
         if cfg4:
             result["cfg4"] = cfg4
         if blocks:
             result["blocks"] = blocks
             result["feedback"] = feedback_bench()
+        if lat:
+            result["latency"] = lat  # last: the driver's stdout tail keeps the per-step latency lines
     if world > 1:
         dist.barrier(device_ids=[local_rank])
         dist.destroy_process_group()
     if result is not None:
         print(json.dumps(result), flush=True)
     return 0
+
+
+def latency_suite(torch, tf32_peak, with_cpu):
+    """p50/p99 per MPC step at 1 GPU (BASELINE configs[0..2]) through rtn_prepare,
+    each beside the reference's CPU path on this host (oracle BatchedCore: 1
+    thread and all threads, CPU model stated)."""
+    threads = os.cpu_count() or 1
+    cases = [("cfg3_12x512_N20", SIZES, SEED, 20, 1, 0, "silu", 1000),
+             ("cfg3_12x512_N20_order2", SIZES, SEED, 20, 2, 0, "silu", 300),
+             ("cfg3_12x512_N20_bf16x3", SIZES, SEED, 20, 1, 2, "silu", 300),
+             ("cfg3_12x512_N20_3xtf32", SIZES, SEED, 20, 1, 1, "silu", 300),
+             ("cfg2_5x256_N20", [17] + [256] * 5 + [6], 5256, 20, 1, 0, "silu", 1000),
+             ("cfg1_2x64_N10", [17, 64, 64, 6], 2064, 10, 1, 0, "tanh", 1000)]
+    out = {}
+    for name, sizes, seed, k, order, prec, act, steps in cases:
+        out[name] = latency(torch, sizes, seed, k, steps=steps, order=order, precision=prec, act=act,
+                            tf32_peak=tf32_peak)
+        if with_cpu and prec == 0:
+            cpu = {"cpu_model": cpu_model(), "kind": "port",
+                   "algorithm": "oracle BatchedCore (reverse mode, fp64), one batched call of K = N nodes per step"}
+            if order == 1:
+                cpu["1_thread"] = cpu_latency(sizes, act, seed, k, order, 1, 20 if sizes[1] == 512 else 100)
+            cpu[f"{threads}_threads"] = cpu_latency(sizes, act, seed, k, order, threads,
+                                                    3 if order == 2 else (20 if sizes[1] == 512 else 100))
+            if order == 2:
+                cpu["note"] = "order 2 (HessianSingle per node) takes seconds per step on one core: all threads only"
+            out[name]["cpu_baseline"] = cpu
+    return out
 
 
 def main():
@@ -659,6 +813,7 @@ def main():
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-modes", action="store_true")
     ap.add_argument("--no-blocks", action="store_true")
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N>1: gather chunks overlapping the kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = _env_int("RANK", 0)

@@ -47,7 +47,7 @@ typedef enum {
   RTN_EDOMAIN = 2,      /* InputDomainError: feature dim mismatch, K out of range */
   RTN_EUNSUPPORTED = 3, /* UnsupportedError: e.g. Hessians of a relu net */
   RTN_ECUDA = 4,        /* CUDA runtime failure (or no sm_100 device) */
-  RTN_ENCCL = 5,        /* reserved for the multi-GPU gather */
+  RTN_ENCCL = 5,        /* NCCL unavailable or failed (multi-GPU entry, rtn_comm_*) */
   RTN_ERUNTIME = 6      /* std::runtime_error of BuildQp: "build qp: node k: ..." (sqp_rti.cpp:134-138) */
 } rtn_status;
 
@@ -106,6 +106,37 @@ rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* batched_calls,
                             unsigned long long* batched_points, unsigned long long* kernel_launches);
 
 const char* rtn_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU entry: MPC instances are independent, so each rank
+ * (one process or thread per GPU, with its own model + context on its device)
+ * evaluates its contiguous block of node rows, and the one exchange step is the
+ * gather of the (f, A, B) blocks to the consumer rank over NCCL (NVLink /
+ * NVSwitch). Replaces the reference's process-global fork/join pool
+ * (/root/reference/proj/include/resmpc/threadpool.hpp:41-62) as the path's
+ * parallel backend. NCCL is loaded at run time; failures -> RTN_ENCCL.
+ * ------------------------------------------------------------------------- */
+typedef struct rtn_comm rtn_comm; /* opaque: one NCCL communicator + stream per rank */
+
+/* 128-byte NCCL unique id, created on one rank and sent to the others by the caller. */
+rtn_status rtn_comm_unique_id(unsigned char id[128]);
+/* Collective over the nranks ranks: every rank calls it with the same id. */
+rtn_status rtn_comm_create(const unsigned char id[128], int nranks, int rank, int device, rtn_comm** out);
+void rtn_comm_free(rtn_comm* comm);
+
+/* Instance-partitioned PrepareNodes (order 0 or 1; Hessians stay on their rank):
+ * every rank passes its own K_local node rows (host, row-major K_local x n_in);
+ * the root receives all ranks' rows concatenated in rank order into f_all
+ * (sum K x n_out) and jac_all (sum K x n_out x n_in) — host buffers, NULL on the
+ * other ranks. Collective and blocking; counts one batched call of K_local points. */
+rtn_status rtn_prepare_partitioned(rtn_ctx* c, rtn_comm* comm, const double* z_local, long long K_local, int n_cols,
+                                   int order, int root, double* f_all, double* jac_all);
+/* Device-pointer variant, enqueued on the context stream: the rank's rows are
+ * evaluated in `chunks` pieces and piece i's NCCL transfer to the root overlaps
+ * piece i+1's kernel. d_f_all / d_jac_all: the root's device receive buffers. */
+rtn_status rtn_prepare_partitioned_device(rtn_ctx* c, rtn_comm* comm, const double* d_z, long long K_local, int order,
+                                          double* d_f, double* d_jac, int root, double* d_f_all, double* d_jac_all,
+                                          int chunks);
 
 /* ---------------------------------------------------------------------------
  * Continuity-block builder (the step after PrepareNodes).

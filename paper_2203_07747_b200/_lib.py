@@ -25,6 +25,8 @@ EXPORTS = (
     "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
     "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_last_error",
     "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp", "rtn_solve_feedback",
+    "rtn_comm_unique_id", "rtn_comm_create", "rtn_comm_free", "rtn_prepare_partitioned",
+    "rtn_prepare_partitioned_device",
 )
 
 
@@ -101,11 +103,18 @@ def lib() -> C.CDLL:
                                C.POINTER(IterateC), C.POINTER(QpBlocksC), _vp, _vp, _vp]
     L.rtn_solve_feedback.argtypes = [_vp, C.POINTER(OcpConfigC), C.c_longlong, C.POINTER(QpBlocksC), _vp,
                                      C.POINTER(IterateC), C.POINTER(FeedbackC)]
+    L.rtn_comm_unique_id.argtypes = [C.c_char_p]
+    L.rtn_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.rtn_comm_free.argtypes = [_vp]
+    L.rtn_comm_free.restype = None
+    L.rtn_prepare_partitioned.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp]
+    L.rtn_prepare_partitioned_device.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int, _vp, _vp, C.c_int, _vp, _vp,
+                                                 C.c_int]
     L.rtn_make_mlp.argtypes = [_ip, C.c_int, C.c_ulonglong, C.POINTER(_dp), C.POINTER(_dp)]
     L.rtn_synth_quad_nodes.argtypes = [C.c_ulonglong, C.c_longlong, _dp]
     L.rtn_synth_quad_nodes.restype = None
     for name in EXPORTS:
-        if name not in ("rtn_last_error", "rtn_model_free", "rtn_ctx_free"):
+        if name not in ("rtn_last_error", "rtn_model_free", "rtn_ctx_free", "rtn_comm_free"):
             getattr(L, name).restype = C.c_int
     L.rtn_make_mlp.restype = C.c_int
     _lib = L

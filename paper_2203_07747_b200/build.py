@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-ccbin", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++",
 ]
 
-SOURCES = ["rtn_mpc.cu", "rtn_pair_tf32.cu", "rtn_pair_3xtf32.cu", "rtn_pair_bf16x3.cu", "rtn_pair_order2.cu",
+SOURCES = ["rtn_mpc.cu", "rtn_comm.cu", "rtn_pair_tf32.cu", "rtn_pair_3xtf32.cu", "rtn_pair_bf16x3.cu", "rtn_pair_order2.cu",
            "rtn_blocks.cu", "rtn_qpsolve.cu", "rtn_synth.cpp"]
 HEADERS = ["rtn_kernel.cuh", "rtn_pair.cuh", "rtn_pair_launch.cuh", "rtn_launch.h", "rtn_blocks.h", "rtn_quad.cuh",
            "rtn_qpsolve.h", "rtn_rows.cuh", "rtn_internal.h"]
@@ -63,7 +63,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     failed = [src for src, p in procs if p.wait() != 0]
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", NVCC_FLAGS[-1], *objs, "-o", LIB]
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", NVCC_FLAGS[-1], *objs, "-ldl",
+            "-o", LIB]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)

@@ -81,25 +81,80 @@ def gather_blocks(local, dst: int = 0, group=None):
 
 
 class Gatherer:
-    """Preallocated fixed-shape gather used in the timed loop: every rank
-    sends the same-sized block (balanced partitions, padded), rank `dst`
-    receives into persistent buffers, so the step issues exactly one NCCL
-    gather per output tensor and no allocations."""
+    """Preallocated fixed-shape gather of one per-node output tensor, used in the
+    timed loop: every rank sends the same `rows_max` rows (balanced partitions
+    differ by at most one instance; the tail is zero padding), rank `dst`
+    receives into persistent per-rank buffers. The kernel writes its rows
+    straight into `send` (no copy in the step), and the gather can be issued
+    in row chunks [lo, hi) so chunk i's transfer overlaps chunk i+1's compute
+    (SURVEY §8e). `counts[r]` are the valid rows of rank r; `result()` trims."""
 
-    def __init__(self, shape_per_rank, dtype, device, dst: int = 0, group=None):
+    def __init__(self, counts, row_shape, dtype, device, dst: int = 0, group=None):
         import torch
         import torch.distributed as dist
         self.dst = dst
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.send = torch.zeros(shape_per_rank, dtype=dtype, device=device)
-        self.recv = ([torch.empty(shape_per_rank, dtype=dtype, device=device) for _ in range(self.world)]
+        if len(counts) != self.world:
+            raise ValueError("one row count per rank")
+        self.counts = [int(c) for c in counts]
+        self.rows_max = max(self.counts)
+        shape = (self.rows_max,) + tuple(row_shape)
+        self.send = torch.zeros(shape, dtype=dtype, device=device)  # tail rows stay zero
+        self.recv = ([torch.empty(shape, dtype=dtype, device=device) for _ in range(self.world)]
                      if self.rank == dst else None)
 
-    def __call__(self, local):
+    @property
+    def local(self):
+        """This rank's valid rows of the send buffer (the kernel's output)."""
+        return self.send[:self.counts[self.rank]]
+
+    def start(self, lo: int, hi: int):
+        """Asynchronous gather of rows [lo, hi) of every rank's block."""
         import torch.distributed as dist
-        n = local.shape[0]
-        self.send[:n].copy_(local)
-        dist.gather(self.send, self.recv, dst=self.dst, group=self.group)
-        return self.recv
+        recv = [r[lo:hi] for r in self.recv] if self.recv is not None else None
+        return dist.gather(self.send[lo:hi], recv, dst=self.dst, group=self.group, async_op=True)
+
+    def __call__(self, local=None):
+        """Whole-block gather (optionally copying `local` into the send rows
+        first); returns the trimmed per-rank blocks on dst, None elsewhere."""
+        if local is not None:
+            n = local.shape[0]
+            self.send[:n].copy_(local)
+            self.send[n:].zero_()
+        self.start(0, self.rows_max).wait()
+        return self.result()
+
+    def result(self):
+        if self.recv is None:
+            return None
+        return [r[:c] for r, c in zip(self.recv, self.counts)]
+
+
+def chunk_bounds(rows: int, chunks: int) -> list[tuple[int, int]]:
+    """[lo, hi) row ranges of `chunks` near-equal pieces of `rows` (empty pieces dropped)."""
+    if rows <= 0:
+        return []
+    chunks = max(1, min(int(chunks), rows))
+    per = -(-rows // chunks)
+    return [(lo, min(rows, lo + per)) for lo in range(0, rows, per)]
+
+
+def partitioned_step(compute, gatherers, n_local: int, chunks: int = 1):
+    """One instance-partitioned step (the body bench.py times under torchrun):
+    for every row chunk [lo, hi) of the common padded block, `compute(lo, hi)`
+    enqueues this rank's rows [lo, min(hi, n_local)) into the gatherers' send
+    buffers, then the chunk's gathers are issued asynchronously so they overlap
+    the next chunk's compute. Every rank issues the same gathers (same padded
+    shapes), including chunks past its own rows. Waits on all gathers (on GPUs:
+    the current stream waits for NCCL; the host does not block)."""
+    rows_max = gatherers[0].rows_max
+    works = []
+    for lo, hi in chunk_bounds(rows_max, chunks):  # identical on every rank (common rows_max)
+        if lo < n_local:
+            compute(lo, min(hi, n_local))
+        for g in gatherers:
+            works.append(g.start(lo, hi))
+    for w in works:
+        w.wait()
