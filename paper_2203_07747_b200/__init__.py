@@ -7,6 +7,7 @@ the step after it (`resmpc::BuildQp`'s RK4 continuity blocks, qp.py).
 """
 from .errors import ConfigError, DeviceError, InputDomainError, UnsupportedError
 from .neural import (BatchEval, Engine, EvalCounters, EvalOrder, MlpModel, flops_per_node, load_model, make_mlp,
+                     make_zero_network,
                      mlp_batched_eval, mlp_forward, mlp_hessian, mlp_jacobian, parse_arch, save_model,
                      synth_quad_nodes)
 from .qp import OcpConfig, QpBuilder, QpData, QuadParams, build_qp, cycle_qp
@@ -15,7 +16,7 @@ from .taylor import TaylorApprox, eval_taylor, eval_taylor_jacobian, prepare_nod
 __all__ = [
     "BatchEval", "ConfigError", "DeviceError", "Engine", "EvalCounters", "EvalOrder", "InputDomainError",
     "MlpModel", "TaylorApprox", "UnsupportedError", "eval_taylor", "eval_taylor_jacobian", "flops_per_node",
-    "load_model", "make_mlp", "mlp_batched_eval", "mlp_forward", "mlp_hessian", "mlp_jacobian", "parse_arch",
+    "load_model", "make_mlp", "make_zero_network", "mlp_batched_eval", "mlp_forward", "mlp_hessian", "mlp_jacobian", "parse_arch",
     "prepare_nodes", "save_model", "synth_quad_nodes",
     "OcpConfig", "QpBuilder", "QpData", "QuadParams", "build_qp", "cycle_qp",
 ]

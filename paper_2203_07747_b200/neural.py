@@ -264,6 +264,19 @@ def make_mlp(layer_sizes, activation: str = "tanh", variant: str = "full", seed:
     return m
 
 
+def make_zero_network(depth: int, width: int, in_dim: int, out_dim: int, seed: int) -> MlpModel:
+    """MakeZeroNetwork (proj/src/bench.cpp:25-36): MakeMlp tanh hidden layers
+    with the last layer zeroed — the paper's §V timing trick:
+    full network cost, zero residual, so the controller's behaviour is the
+    nominal one. Outputs (f, J, H) are exactly zero."""
+    if depth < 1 or width < 1 or in_dim < 1 or out_dim < 1:
+        raise ConfigError("zero network: dimensions must be positive")
+    m = make_mlp([in_dim] + [width] * depth + [out_dim], "tanh", "full", seed)
+    m.weights[-1][:] = 0.0
+    m.biases[-1][:] = 0.0
+    return m
+
+
 def synth_quad_nodes(seed: int, k: int) -> np.ndarray:
     """Quadrotor node rows z=[p q v ω u] (SURVEY §8d synthetic inputs)."""
     z = np.empty((k, 17))

@@ -114,3 +114,18 @@ def test_taylor_consumers_match_oracle(oracle_lib):
     assert np.allclose(y, ref, rtol=0, atol=1e-14)
     with pytest.raises(ConfigError):
         TaylorApprox(0, 2, z0[0], f[0], j[0], []).validate()
+
+
+def test_make_zero_network():
+    """proj/src/bench.cpp:25-36: MakeMlp (tanh) hidden layers, last layer zeroed;
+    positive dimensions required."""
+    from paper_2203_07747_b200 import ConfigError, make_mlp, make_zero_network
+    z = make_zero_network(3, 32, 17, 6, 3032)
+    m = make_mlp([17, 32, 32, 32, 6], "tanh", "full", 3032)
+    assert z.layer_sizes == [17, 32, 32, 32, 6] and z.activation == "tanh"
+    for l in range(3):
+        assert np.array_equal(z.weights[l], m.weights[l]) and np.array_equal(z.biases[l], m.biases[l])
+    assert not z.weights[-1].any() and not z.biases[-1].any()
+    for bad in ((0, 32, 17, 6), (3, 0, 17, 6), (3, 32, 0, 6), (3, 32, 17, 0)):
+        with pytest.raises(ConfigError):
+            make_zero_network(*bad, 1)
