@@ -59,6 +59,7 @@ struct rtn_model {
   float* d_bh_pair = nullptr; // hidden biases with pair_wp stride
   double* d_mu = nullptr;     // in_mean (fp64, subtracted before layer 0)
   float* d_w0 = nullptr;
+  float* d_w0t = nullptr;     // input-major copy of W0' (n_in x pair_wp)
   float* d_b0 = nullptr;
   float* d_bl = nullptr;
   // pair (cta_group::2) kernel: plain row-major tf32 weights behind TMA maps
@@ -73,6 +74,7 @@ struct rtn_model {
       cudaSetDevice(device);
       cudaFree(d_mu);
       cudaFree(d_w0);
+      cudaFree(d_w0t);
       cudaFree(d_b0);
       cudaFree(d_bl);
       cudaFree(d_wt_hidden);

@@ -59,9 +59,11 @@ struct KParams {
   int lo_rows;       // pair kernel split modes: row offset of the lo weight tiles in the stacked map
   int ord2_g;        // order 2: pair tiles per node (Hessian slot groups)
   unsigned long long* trace;  // optional event timestamps (RTN_TRACE), pair 0 only
+  int trace_tile;    // which of pair 0's tiles is traced (RTN_TRACE = 1 + index)
   int dbg;           // perf-isolation switches (RTN_DEBUG): 4 = skip epilogue math, 8 = local stores, 128 = stream only
   const double* mu;  // n_in: in_mean, subtracted in fp64 before the fp32 layer 0
-  const float* w0;   // WP x n_in   (W0·diag(1/in_scale))
+  const float* w0;   // WP x n_in   (W0·diag(1/in_scale)), neuron-major (rows kernel staging)
+  const float* w0t;  // n_in x WP   the same, input-major: a warp's 32 neurons read 128 contiguous bytes
   const float* b0;   // WP          (the layer-0 bias; the mean is NOT folded in)
   const float* bh;   // (n_hidden-1) x WP
   const float* bl;   // kMaxOut     (out_scale ⊙ b_L + out_mean)
@@ -74,11 +76,12 @@ struct KParams {
   int zN;
 };
 
-// Layer-0 weight row of neuron j in registers (n_in <= kMaxIn0 for every tile shape).
+// Layer-0 weight row of neuron j in registers (n_in <= kMaxIn0 for every tile
+// shape), from the input-major copy: coalesced across the warp's neurons.
 constexpr int kMaxIn0 = 24;
-__device__ __forceinline__ void load_w0_row(const float* w0r, int n_in, float (&w)[kMaxIn0]) {
+__device__ __forceinline__ void load_w0_row(const float* w0t, int wp, int j, int n_in, float (&w)[kMaxIn0]) {
 #pragma unroll
-  for (int k = 0; k < kMaxIn0; ++k) w[k] = k < n_in ? __ldg(w0r + k) : 0.0f;
+  for (int k = 0; k < kMaxIn0; ++k) w[k] = k < n_in ? __ldg(w0t + k * wp + j) : 0.0f;
 }
 // pre = b + Σ_k W0'[j,k]·z[k], ascending k (same rounding as the loop it replaces).
 __device__ __forceinline__ float layer0_pre(float b, const float (&w)[kMaxIn0], const float* z, int n_in) {
@@ -379,6 +382,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 // Arrive (release, cluster scope) on an mbarrier given by its shared::cluster address.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Remote arrive with the default (.release.cta) semantics, as CUTLASS's
+// ClusterBarrier::arrive(cta_id): for TMEM reads, which the tcgen05 fences
+// around the barrier order, the cluster-scope release (MEMBAR) of
+// mbar_arrive_cluster is not needed.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_cluster() {
   asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");

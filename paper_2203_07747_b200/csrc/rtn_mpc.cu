@@ -196,6 +196,12 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   };
   up(reinterpret_cast<void**>(&m->d_mu), hm.in_mean.data(), hm.in_mean.size() * 8);
   up(reinterpret_cast<void**>(&m->d_w0), w0.data(), w0.size() * 4);
+  {
+    std::vector<float> w0t(w0.size(), 0.0f);
+    for (int j = 0; j < pwp; ++j)
+      for (int k = 0; k < n_in; ++k) w0t[static_cast<size_t>(k) * pwp + j] = w0[static_cast<size_t>(j) * n_in + k];
+    up(reinterpret_cast<void**>(&m->d_w0t), w0t.data(), w0t.size() * 4);
+  }
   up(reinterpret_cast<void**>(&m->d_b0), b0.data(), b0.size() * 4);
   up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
   {
@@ -358,11 +364,13 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   prm.lo_rows = m->lo_rows;
   prm.mu = m->d_mu;
   prm.w0 = m->d_w0;
+  prm.w0t = m->d_w0t;
   prm.b0 = m->d_b0;
   prm.bh = m->d_bh_pair;
   prm.bl = m->d_bl;
   if (const char* d = std::getenv("RTN_DEBUG")) prm.dbg = std::atoi(d);
-  if (std::getenv("RTN_TRACE")) {  // per-event timestamps of pair 0 (profiling aid)
+  if (const char* tr = std::getenv("RTN_TRACE")) {  // per-event timestamps of pair 0 (profiling aid)
+    prm.trace_tile = std::max(0, std::atoi(tr) - 1);
     if (!trace_buf) CUDA_CHECK(cudaMalloc(&trace_buf, 256 * 8));
     CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 256 * 8, c->stream));
     prm.trace = trace_buf;

@@ -38,9 +38,19 @@
 //   activations: the epilogue of CTA r owns next-layer K-group q = 2·mb + r
 //                and writes its rows into BOTH CTAs' operand buffers (the
 //                peer's half through DSMEM, st.shared::cluster)
-//   barriers   : full[s] (leader), act_ready[q] (leader, 8 warp arrivals from
-//                the owning CTA), empty/in_free/tmem_full/tmem_last multicast
-//                by the leader's tcgen05.commit to both CTAs.
+//   barriers   : full[s] (leader); act_ready[c] per 32-k (tf32) chunk of the
+//                next layer's input (leader; one arrival per epilogue warp
+//                that wrote it), so the next layer's MMAs start on a chunk as
+//                soon as it is stored; tmem_empty[mb] (leader; every epilogue
+//                warp of both CTAs, right after its TMEM reads), so a TMEM
+//                block is reused without waiting for the stores; empty /
+//                in_free / tmem_full / tmem_last multicast by the leader's
+//                tcgen05.commit to both CTAs.
+//   DSMEM      : the peer-side stores (~13.5 B/clk against ~40 B/clk local,
+//                scripts/dsmem_bench.cu) are issued one warp after another
+//                (named-barrier chain), so the first chunks of a group complete
+//                early and the MMA of the next layer resumes on them while the
+//                rest is in flight.
 #pragma once
 
 #include <cuda.h>
@@ -69,7 +79,9 @@ struct PairCfg {
   static constexpr uint32_t kActBytes = kSplit * kSplitStride;
   static constexpr uint32_t kStageOff = kActBytes;
   static constexpr uint32_t kBarOff = kStageOff + NSTAGE * kStageBytes;
-  static constexpr uint32_t kNumBars = 2 * NSTAGE + 13;
+  // full/empty[NSTAGE], act_ready[16] (per K-chunk), tmem_empty[2], in_free[4], tmem_full[2], tmem_last
+  static constexpr uint32_t kNumBars = 2 * NSTAGE + 25;
+  static constexpr int kWarpsPerChunk = 2 * (kCK / 32);  // both halves of the owning CTA
   static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
   static constexpr uint32_t kZsOff = kMiscOff + 16;
   // generic order 2: per-thread tangent rows T_a (2 halves x 32 x 128 fp32) and the slot → (a, b) table
@@ -131,6 +143,11 @@ __device__ __forceinline__ void tmem_read_acc(uint32_t t, float* v, int lim, uin
   }
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 template <int WP, int NSTAGE, int P, int NTC, int MODE, int ORD2 = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     rtn_pair_kernel(const KParams prm, const __grid_constant__ CUtensorMap tmap_h,
@@ -138,6 +155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using C = PairCfg<WP, NSTAGE, P, NTC, MODE, ORD2>;
   static_assert(ORD2 != 1 || NTC == kNtc2, "quadrotor order-2 tiles are 2 x 48 rows");
   constexpr int NMB = C::kNMB, NKC = C::kNKC, NG = C::kNG, SPLIT = C::kSplit, CPG = C::kCPG;
+  static_assert(NKC <= 16, "act_ready barriers");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* act_s = smem;
@@ -145,10 +163,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
-  uint64_t* act_ready = bars + 2 * NSTAGE;
-  uint64_t* in_free = act_ready + 4;
-  uint64_t* tmem_full = in_free + 4;
-  uint64_t* tmem_last = tmem_full + 4;
+  uint64_t* act_ready = bars + 2 * NSTAGE;  // [16]
+  uint64_t* tmem_empty = act_ready + 16;    // [2]
+  uint64_t* in_free = tmem_empty + 2;       // [4]
+  uint64_t* tmem_full = in_free + 4;        // [2]
+  uint64_t* tmem_last = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kMiscOff);
   float* zs = reinterpret_cast<float*>(smem + C::kZsOff);
 
@@ -164,11 +183,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int g = 0; g < 4; ++g) {
-      mbar_init(&act_ready[g], 8);  // one elected arrive per epilogue warp of the owning CTA
-      mbar_init(&in_free[g], 1);
-      mbar_init(&tmem_full[g], 1);
+    for (int c = 0; c < 16; ++c) mbar_init(&act_ready[c], C::kWarpsPerChunk);
+    for (int mb = 0; mb < 2; ++mb) {
+      mbar_init(&tmem_empty[mb], 16);  // 8 epilogue warps x 2 CTAs
+      mbar_init(&tmem_full[mb], 1);
     }
+    for (int g = 0; g < 4; ++g) mbar_init(&in_free[g], 1);
     mbar_init(tmem_last, 1);
     fence_barrier_init();
   }
@@ -190,7 +210,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (prm.trace && pair == 0 && threadIdx.x == 0) {
+  const bool tr_pair = prm.trace && pair == 0;
+  if (tr_pair && threadIdx.x == 0) {
     prm.trace[196 + rank] = globaltimer();
     prm.trace[250 + rank] = clock64();
   }
@@ -236,17 +257,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
       constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4, kSplitD = C::kSplitStride >> 4;
-      uint32_t ph = 0, ar = 0;
-      // Before the first MMA of a layer overwrites TMEM block 0, both CTAs must
-      // have drained it: wait for K-groups 0 and 1 (one per CTA) up front.
-      auto wait_group = [&](int g) {
-        if (prm.dbg & 128) return;  // dbg 128: stream only (timing)
-        if (g == 0) {
-          mbar_wait_cluster(&act_ready[0], ar & 1);
-          if (NG > 1) mbar_wait_cluster(&act_ready[1], ar & 1);
-        } else if (g != 1) {
-          mbar_wait_cluster(&act_ready[g], ar & 1);
-        }
+      const bool stream_only = prm.dbg & 128;  // dbg 128: weight stream + MMAs only (timing)
+      uint32_t ph = 0, ar = 0, use0 = 0, use1 = 0;
+      // TMEM block mb is about to be overwritten: both CTAs' epilogues must have
+      // read its previous contents (tmem_empty, one phase per use of the block).
+      auto claim_tmem = [&](int mb) {
+        const uint32_t u = mb ? use1 : use0;
+        if (!stream_only && u > 0) mbar_wait(&tmem_empty[mb], (u - 1) & 1);
+        if (mb) ++use1;
+        else ++use0;
+        tc_fence_after();
+      };
+      // input chunk c of the current activation production is in both CTAs' smem
+      auto wait_chunk = [&](int c) {
+        if (stream_only) return;
+        mbar_wait_cluster(&act_ready[c], ar & 1);
         tc_fence_after();
       };
       // One chunk: weights from stage(s) st0[/st1], activations chunk (hi[, lo]).
@@ -275,16 +300,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         else return (c >= C::kChains ? 1u : 0u) | (c != 0 ? 2u : 0u);
       };
       for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
+        const bool tr = tr_pair && tile == pair + prm.trace_tile * npairs && lane == 0;
         for (int l = 0; l < n_mma_layers; ++l) {
 #pragma unroll 1
           for (int mb = 0; mb < NMB; ++mb) {
             const uint32_t d = tmem_base + mb * C::kBlkCols;
             const uint32_t d2 = C::kCorr ? d + C::kCorrOff : d;
-            if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2] = globaltimer();
+            if (tr) prm.trace[(l * 2 + mb) * 2] = globaltimer();
+            claim_tmem(mb);
 #pragma unroll
             for (int c = 0; c < NKC; ++c) {
               const int st0 = (c * SPLIT) % NSTAGE, st1 = (c * SPLIT + SPLIT - 1) % NSTAGE;
-              if ((c % CPG) == 0 && mb == 0) wait_group(c / CPG);
+              if (mb == 0) wait_chunk(c);
               mbar_wait(&full[st0], ph);
               if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
               tc_fence_after();
@@ -295,16 +322,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (st1 == NSTAGE - 1) ph ^= 1;
             }
             mma_commit_pair(&tmem_full[mb]);
-            if (prm.trace && pair == 0 && tile == pair && lane == 0) prm.trace[(l * 2 + mb) * 2 + 1] = globaltimer();
+            if (tr) prm.trace[(l * 2 + mb) * 2 + 1] = globaltimer();
           }
           ++ar;
         }
         // output layer: D[row, o] = Σ_k X[row, k] · W_L'[o, k]; M = 2 x 128 rows, N = 16;
-        // main chains at columns 16·c, the correction accumulator at 16·kChains
+        // main chains at columns 16·c of block 0, the correction accumulator at 16·kChains
+        claim_tmem(0);
 #pragma unroll
         for (int c = 0; c < NKC; ++c) {
           const int st0 = (c * SPLIT) % NSTAGE, st1 = (c * SPLIT + SPLIT - 1) % NSTAGE;
-          if ((c % CPG) == 0) wait_group(c / CPG);
+          wait_chunk(c);
           mbar_wait(&full[st0], ph);
           if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
           tc_fence_after();
@@ -314,17 +342,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (st1 == NSTAGE - 1) ph ^= 1;
         }
         mma_commit_pair(tmem_last);
+        if (tr) prm.trace[44] = globaltimer();
         ++ar;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && !(prm.dbg & 128)) {
     // ===================== epilogue (8 warps per CTA) ========================
     // Thread = one neuron (TMEM lane) of this CTA's 128-neuron half of a
     // 256-block; warp half h owns the rows of side h (the nodes whose operand
     // rows live in CTA h), i.e. TMEM columns [h·ntc, (h+1)·ntc). Results stay
     // in registers until the layer's last block has consumed the input group
     // they overwrite (in_free), then go straight to the owning CTA's shared
-    // memory (DSMEM for the peer side).
+    // memory (DSMEM for the peer side), and each warp publishes its chunk.
     const int half = (warp - 4) >> 2;
     const int q = warp & 3;
     const int tid_h = q * 32 + lane;
@@ -341,28 +370,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t act_local = smem_u32(act_s);
     const bool local_side = half == static_cast<int>(rank) || (prm.dbg & 8);  // dbg 8: timing only
     const uint32_t side_base = local_side ? act_local : mapa(act_local, static_cast<uint32_t>(half));
-    uint32_t ready_cl[4];
-#pragma unroll
-    for (int g = 0; g < 4; ++g) ready_cl[g] = mapa(smem_u32(&act_ready[g]), 0);
+    const uint32_t ready_cl0 = mapa(smem_u32(&act_ready[0]), 0);
+    const uint32_t empty_cl0 = mapa(smem_u32(&tmem_empty[0]), 0);
     uint32_t hl = 0, tiles_done = 0;
+    auto trace_on = [&]() {
+      return tr_pair && tiles_done == static_cast<uint32_t>(prm.trace_tile) && warp == 4 && lane == 0;
+    };
 
     // Store one neuron column (rows 0..ntc-1) of one side into its operand
-    // buffer(s), rounding / splitting per precision mode.
-    auto store_side = [&](const float* v, int j) {
+    // buffer(s), rounding / splitting per precision mode. row(i) yields the
+    // value of row i (an array read, or generated on the fly at layer 0).
+    auto store_to = [&](auto&& row, int j, uint32_t buf, bool local) {
       const uint32_t base =
-          side_base + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) + ((j * C::kEB) & 15);
+          buf + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) + ((j * C::kEB) & 15);
 #pragma unroll
       for (int i = 0; i < NTC; ++i) {
         if ((i & ~7) >= ntc) continue;
         const uint32_t a = base + (i >> 3) * 1024 + swz[i & 7];
+        const float x = row(i);
         if constexpr (MODE == kTF32) {
-          const float h = to_tf32(v[i]);
-          if (local_side) st_shared_f32(a, h);
+          const float h = to_tf32(x);
+          if (local) st_shared_f32(a, h);
           else st_cluster_f32(a, h);
         } else if constexpr (MODE == k3xTF32) {
-          const float h = to_tf32(v[i]);
-          const float lo = to_tf32(v[i] - h);
-          if (local_side) {
+          const float h = to_tf32(x);
+          const float lo = to_tf32(x - h);
+          if (local) {
             st_shared_f32(a, h);
             st_shared_f32(a + C::kSplitStride, lo);
           } else {
@@ -370,9 +403,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             st_cluster_f32(a + C::kSplitStride, lo);
           }
         } else {
-          const uint16_t h = bf16_rn_bits(v[i]);
-          const uint16_t lo = bf16_rn_bits(v[i] - bf16_to_f32(h));
-          if (local_side) {
+          const uint16_t h = bf16_rn_bits(x);
+          const uint16_t lo = bf16_rn_bits(x - bf16_to_f32(h));
+          if (local) {
             st_shared_u16(a, h);
             st_shared_u16(a + C::kSplitStride, lo);
           } else {
@@ -382,10 +415,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     };
-    auto publish = [&](int grp) {
-      fence_proxy_async_cluster();
+    auto store_side = [&](auto&& row, int j) { store_to(row, j, side_base, local_side); };
+    // publishes this warp's chunk of K-group g: its stores are made visible to
+    // the async proxy (the tensor core) — a CTA-scope proxy fence when they all
+    // went to this CTA's shared memory, cluster scope for DSMEM stores — and
+    // the leader's barrier is released at cluster scope
+    auto publish_chunk = [&](int g, bool all_local) {
+      if (all_local) fence_proxy_async_smem();
+      else fence_proxy_async_cluster();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ready_cl[grp]);
+      if (lane == 0) mbar_arrive_cluster(ready_cl0 + 8 * ((g * 128 + q * 32) / C::kCK));
+    };
+    // Stores, then publishes this warp's chunk of K-group g. The peer-side
+    // half issues its DSMEM stores one warp after another (q = 0, 1, 2, 3
+    // through a chain of named barriers), so chunk by chunk they complete
+    // early instead of all at the end of the shared transfer.
+    auto store_publish = [&](auto&& row, int j, int g) {
+      const int c = (g * 128 + q * 32) / C::kCK;
+      if (!local_side && (prm.dbg & 16)) {  // dbg 16: chain the peer-side warps (experiment)
+        if (q > 0) named_bar_sync(2 + half * 3 + (q - 1), 64);
+        store_side(row, j);
+        if (q < 3) named_bar_arrive(2 + half * 3 + q, 64);
+      } else {
+        store_side(row, j);
+      }
+      (void)c;
+      publish_chunk(g, local_side);
+    };
+    // this warp has read TMEM block mb (all lanes' loads complete)
+    auto tmem_release = [&](int mb) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(empty_cl0 + 8 * mb);
     };
     // output-layer accumulator of this lane (row), columns = outputs
     auto read_out = [&](float* o) {
@@ -424,19 +485,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float v[kNtc2], car[24];
       tmem_read_acc<C, kNtc2>(tb + half * kNtc2, v, kNtc2, C::kN, C::kCorrOff);
       tmem_read_acc<C, 24>(tb, car, 24, C::kN, C::kCorrOff);
-      tc_fence_before();
+      tmem_release(mb);
       float val, sp, spp;
       act_fwd2(act, car[0] + bj, val, sp, spp);
       epi_rows(v, car + 1, val, sp, spp, hg);
       mbar_wait_sleep(&in_free[grp], hl & 1);
-      store_side(v, j);
-      publish(grp);
+      store_publish([&](int i) { return v[i]; }, j, grp);
     };
 
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
       const long long node = tile >> 1;
       const int hg = static_cast<int>(tile & 1);
-      if (tiles_done > 0) {
+      if (tiles_done > 0) {  // the previous tile's output MMAs have read the activation buffer
         mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
         tc_fence_after();
       }
@@ -449,7 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float pre = __ldg(prm.b0 + j);
 #pragma unroll
         for (int k = 0; k < kNin2; ++k) {
-          w[k] = __ldg(prm.w0 + j * kNin2 + k);
+          w[k] = __ldg(prm.w0t + k * WP + j);
           pre = fmaf(w[k], zs[k], pre);
         }
         float val, sp, spp;
@@ -465,17 +525,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (hg == 0) hrows0<kNtc2 - kCarrier2, 0>(v, w, spp, Seq1{});
           else hrows0<kSlots2 + kNtc2 - kCarrier2, 0>(v, w, spp, Seq1{});
         }
-        store_side(v, j);
-        publish(g);
+        store_publish([&](int i) { return v[i]; }, j, g);
       }
       for (int l = 0; l < n_mma_layers; ++l, ++hl)
         for (int mb = 0; mb < NMB; ++mb) do_block(mb, l, hg);
       // ---- output layer: lane = this CTA side's row; columns = outputs
       mbar_wait_sleep(tmem_last, tiles_done & 1);
       tc_fence_after();
+      float o[16];
+      if (half == 0) read_out(o);
+      tmem_release(0);
       if (half == 0) {
-        float o[16];
-        read_out(o);
         const int r = tid_h, n_out = prm.n_out;
         if (node < prm.K && r < kNtc2) {
           if (rank == 0 && r < kCarrier2) {
@@ -499,7 +559,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc_fence_before();
     }
    } else if constexpr (ORD2 == 2) {
     // ===================== order-2 epilogue, generic tiles (n_in <= 31) ========
@@ -548,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float v[NTC], car[kCar];
       tmem_read_acc<C, NTC>(tb + half * NTC, v, NTC, C::kN, C::kCorrOff);
       tmem_read_acc<C, kCar>(tb, car, car_rows, C::kN, C::kCorrOff);
-      tc_fence_before();
+      tmem_release(mb);
       float val, sp, spp;
       act_fwd2(act, car[0] + bj, val, sp, spp);
 #pragma unroll
@@ -556,14 +615,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (a < n_in) ts[a * 128] = car[1 + a];
       epi_rows(v, car + 1, val, sp, spp, hg, false);
       mbar_wait_sleep(&in_free[grp], hl & 1);
-      store_side(v, j);
-      publish(grp);
+      store_publish([&](int i) { return v[i]; }, j, grp);
     };
 
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
       const long long node = tile / G;
       const int hg = static_cast<int>(tile - node * G);
-      if (tiles_done > 0) {
+      if (tiles_done > 0) {  // the previous tile's output MMAs have read the activation buffer
         mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
         tc_fence_after();
       }
@@ -576,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float pre = __ldg(prm.b0 + j);
 #pragma unroll
         for (int k = 0; k < kCar; ++k) {
-          w[k] = k < n_in ? __ldg(prm.w0 + j * n_in + k) : 0.0f;
+          w[k] = k < n_in ? __ldg(prm.w0t + k * WP + j) : 0.0f;
           if (k < n_in) {
             pre = fmaf(w[k], zs[k], pre);
             ts[k * 128] = w[k];
@@ -586,17 +644,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         act_fwd2(act, pre, val, sp, spp);
         float v[NTC];
         epi_rows(v, w, val, sp, spp, hg, true);
-        store_side(v, j);
-        publish(g);
+        store_publish([&](int i) { return v[i]; }, j, g);
       }
       for (int l = 0; l < n_mma_layers; ++l, ++hl)
         for (int mb = 0; mb < NMB; ++mb) do_block(mb, l, hg);
       // ---- output layer: lane = this CTA side's row; columns = outputs
       mbar_wait_sleep(tmem_last, tiles_done & 1);
       tc_fence_after();
+      float o[16];
+      if (half == 0) read_out(o);
+      tmem_release(0);
       if (half == 0) {
-        float o[16];
-        read_out(o);
         const int r = tid_h, n_out = prm.n_out;
         if (node < prm.K && r < NTC) {
           if (rank == 0 && r < car_rows) {
@@ -621,9 +679,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc_fence_before();
     }
-   } else if (!(prm.dbg & 128)) {
+   } else {
     // ===================== order-1 epilogue ===================================
     const int rows_used = P * (1 + n_in);   // rows per side
     const bool no_pad = rows_used == ntc;
@@ -650,109 +707,158 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int grp = 2 * mb + static_cast<int>(rank);
       const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
       const float bj = __ldg(prm.bh + l * WP + j);
-      const uint32_t ts = tmem_base + lane_base + mb * C::kBlkCols + half * ntc;
+      const uint32_t tsd = tmem_base + lane_base + mb * C::kBlkCols + half * ntc;
       mbar_wait_sleep(&tmem_full[mb], hl & 1);
       tc_fence_after();
-      const bool tr = prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0;
-      unsigned long long* tp = tr ? prm.trace + 64 + rank * 64 + (l * 2 + mb) * 3 : nullptr;
+      const bool tr = trace_on();
+      unsigned long long* tp = tr ? prm.trace + 48 + rank * 66 + (l * 2 + mb) * 3 : nullptr;
       if (tr) tp[0] = globaltimer();
-      if (prm.dbg & 4) {
+      float v[NTC];
+      if (prm.dbg & 4) {  // dbg 4: no epilogue math or stores (timing)
+        tmem_release(mb);
         mbar_wait_sleep(&in_free[grp], hl & 1);
-        tc_fence_before();
-        publish(grp);
+        fence_proxy_async_cluster();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(ready_cl0 + 8 * ((grp * 128 + q * 32) / C::kCK));
         return;
       }
-      float v[NTC];
-      tmem_read_acc<C, NTC>(ts, v, ntc, C::kN, C::kCorrOff);
-      tc_fence_before();
+      tmem_read_acc<C, NTC>(tsd, v, ntc, C::kN, C::kCorrOff);
+      tmem_release(mb);
       scale_side(v, bj);
       mbar_wait_sleep(&in_free[grp], hl & 1);
       if (tr) tp[1] = globaltimer();
-      store_side(v, j);
-      publish(grp);
+      store_publish([&](int i) { return v[i]; }, j, grp);
       if (tr) tp[2] = globaltimer();
     };
-
-    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
-      const long long node0 = tile * (2 * P);
-      if (tiles_done > 0) {
-        mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
-        tc_fence_after();
-      }
-      // stage z of both sides' nodes (2P) for layer 0
-      if (etid < 2 * P * n_in) {
-        const int p = etid / n_in, k = etid - p * n_in;
-        const long long node = node0 + p;
-        zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, k)) : 0.0f;
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      // ---- layer 0 (CUDA cores): this CTA owns K-groups g ≡ rank (mod 2); half h writes side h
-      for (int g = static_cast<int>(rank); g < NG; g += 2) {
-        const int j = g * 128 + tid_h;
+    // Layer 0 (CUDA cores): σ, σ' of pre = b0 + W0'·(z − μ); the tangent rows
+    // are σ'·W0'[:, k] (the seed is the identity). Layer 0 needs no TMEM, so
+    // each CTA computes EVERY K-group for its OWN side's nodes (warp half h:
+    // groups h, h + 2, ...) and all its stores are local: twice the CUDA-core
+    // math of an owner-computes split, but none of the DSMEM traffic, which
+    // runs at a third of the local store rate (scripts/dsmem_bench.cu).
+    constexpr int kG0 = NG / 2;  // K-groups per warp half
+    constexpr bool kMayBeWide = P < 4 && NTC / P - 1 > kMaxIn0;  // small-P tiles may see > kMaxIn0 inputs
+    float val0[kG0][P], sp0[kG0][P];
+    auto layer0_math = [&]() {
+#pragma unroll
+      const float* zside = zs + static_cast<int>(rank) * P * n_in;  // this CTA's nodes
+      for (int gi = 0; gi < kG0; ++gi) {
+        const int j = (half + 2 * gi) * 128 + tid_h;
         const float bj = __ldg(prm.b0 + j);
-        float val[P], sp[P];
-        float v[NTC];
-        // P·(1+n_in) <= NTC bounds n_in: tiles of P >= 4 (or 24 rows) never see more than
-        // kMaxIn0 inputs, so only the small-P tiles carry the streaming fallback.
-        constexpr bool kMayBeWide = P < 4 && NTC / P - 1 > kMaxIn0;
-        if (!kMayBeWide || n_in <= kMaxIn0) {  // weight row in registers
+        if (!kMayBeWide || n_in <= kMaxIn0) {
           float w0[kMaxIn0];
-          load_w0_row(prm.w0 + j * n_in, n_in, w0);
+          load_w0_row(prm.w0t, WP, j, n_in, w0);
 #pragma unroll
           for (int p = 0; p < P; ++p)
-            act_fwd(act, layer0_pre(bj, w0, zs + (half * P + p) * n_in, n_in), val[p], sp[p]);
-#pragma unroll
-          for (int i = 0; i < NTC; ++i) {
-            if (i < P) v[i] = val[i];
-            else v[i] = i < rows_used ? sp[i % P] * w0[((i - P) / P) % kMaxIn0] : 0.0f;
-          }
-        } else if constexpr (kMayBeWide) {  // wide inputs (e.g. the 26-feature ground variant)
-          const float* w0r = prm.w0 + j * n_in;
+            act_fwd(act, layer0_pre(bj, w0, zside + p * n_in, n_in), val0[gi][p], sp0[gi][p]);
+        } else {
 #pragma unroll
           for (int p = 0; p < P; ++p) {
             float pre = bj;
-            for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(w0r + k), zs[(half * P + p) * n_in + k], pre);
-            act_fwd(act, pre, val[p], sp[p]);
-          }
-#pragma unroll
-          for (int i = 0; i < NTC; ++i) {
-            if (i < P) v[i] = val[i];
-            else v[i] = i < rows_used ? sp[i % P] * __ldg(w0r + (i - P) / P) : 0.0f;
+            for (int k = 0; k < n_in; ++k) pre = fmaf(__ldg(prm.w0t + k * WP + j), zside[p * n_in + k], pre);
+            act_fwd(act, pre, val0[gi][p], sp0[gi][p]);
           }
         }
-        store_side(v, j);
-        publish(g);
       }
-      if (prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0) prm.trace[192 + rank] = globaltimer();
+    };
+    auto layer0_store = [&]() {
+#pragma unroll
+      for (int gi = 0; gi < kG0; ++gi) {
+        const int g = half + 2 * gi;
+        const int j = g * 128 + tid_h;
+        // rows: value rows σ(pre), tangent row (k, p) σ'_p·W0'[j, k], padding 0
+        if (!kMayBeWide || n_in <= kMaxIn0) {
+          float w0[kMaxIn0];
+          load_w0_row(prm.w0t, WP, j, n_in, w0);
+          store_to([&](int i) {
+            return i < P ? val0[gi][i % P] : (i < rows_used ? sp0[gi][i % P] * w0[((i - P) / P) % kMaxIn0] : 0.0f);
+          }, j, act_local, true);
+        } else {
+          store_to([&](int i) {
+            return i < P ? val0[gi][i % P]
+                         : (i < rows_used ? sp0[gi][i % P] * __ldg(prm.w0t + ((i - P) / P) * WP + j) : 0.0f);
+          }, j, act_local, true);
+        }
+        publish_chunk(g, true);
+      }
+    };
+    // z of the tile's 2P nodes, one element per thread, fetched one tile ahead
+    // (registers) so its global-load latency hides behind the hidden layers
+    // (the raw fp64 element only: no arithmetic on it until the next tile's staging,
+    // so the load is not waited for here)
+    const bool zown = etid < 2 * P * n_in;
+    const int zp = zown ? etid / n_in : 0, zk = zown ? etid - zp * n_in : 0;
+    const double mu_k = __ldg(prm.mu + zk);
+    auto fetch_z = [&](long long tile) -> double {
+      const long long node = tile * (2 * P) + zp;
+      if (!(zown && tile < prm.num_tiles && node < prm.K)) return mu_k;  // stages as 0
+      if (prm.zx == nullptr) return prm.z[node * n_in + zk];
+      const long long xrow = node + node / prm.zN;  // gather mode: [x_k; u_k] from the iterate
+      return zk < 13 ? prm.zx[xrow * 13 + zk] : prm.zu[node * 4 + (zk - 13)];
+    };
+    // outputs of a finished tile (this CTA's rows in its TMEM lanes, outputs in columns 0..15)
+    auto write_out = [&](const float* o, long long node0) {
+      const int r = tid_h;
+      const int n_out = prm.n_out;
+      const long long nbase = node0 + static_cast<long long>(rank) * P;
+      if (r < P) {
+        const long long node = nbase + r;
+        if (node < prm.K)
+          for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+      } else if (r < rows_used && prm.jac != nullptr) {
+        const int k = (r - P) / P, p = (r - P) % P;
+        const long long node = nbase + p;
+        if (node < prm.K)
+          for (int oo = 0; oo < n_out; ++oo) prm.jac[(node * n_out + oo) * n_in + k] = static_cast<double>(o[oo]);
+      }
+    };
+
+    double znext = fetch_z(pair);
+    float o[16];
+    long long prev_node0 = -1;
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
+      const long long node0 = tile * (2 * P);
+      // ---- tile boundary: layer-0 math of this tile overlaps the previous
+      // tile's output layer; its stores wait for the output MMAs (which read
+      // the activation buffer)
+      const bool trb = trace_on();
+      unsigned long long* tb = trb ? prm.trace + 180 + rank * 6 : nullptr;
+      if (trb) tb[0] = globaltimer();
+      if (zown) zs[etid] = static_cast<float>(znext - mu_k);  // centred in fp64 (rtn_kernel.cuh load_z)
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      znext = fetch_z(tile + npairs);
+      layer0_math();
+      if (trb) tb[1] = globaltimer();
+      if (tiles_done > 0) {
+        mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
+        tc_fence_after();
+        if (trb) tb[2] = globaltimer();
+        if (half == 0) read_out(o);
+        tmem_release(0);
+      }
+      if (trb) tb[3] = globaltimer();
+      layer0_store();
+      if (trace_on()) prm.trace[192 + rank] = globaltimer();
+      // the previous tile's outputs go out after the layer-0 publications (a
+      // publication's proxy fence would otherwise wait for these global stores)
+      if (tiles_done > 0 && half == 0) write_out(o, prev_node0);
       // ---- hidden layers
       for (int l = 0; l < n_mma_layers; ++l, ++hl)
         for (int mb = 0; mb < NMB; ++mb) do_block(mb, l);
-      // ---- output layer: this CTA's rows in its TMEM lanes, outputs in columns 0..15
-      mbar_wait_sleep(tmem_last, tiles_done & 1);
+      prev_node0 = node0;
+      if (trace_on()) prm.trace[194 + rank] = globaltimer();
+    }
+    if (tiles_done > 0) {  // the last tile's outputs
+      mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
       tc_fence_after();
-      if (prm.trace && pair == 0 && tiles_done == 0 && warp == 4 && lane == 0) prm.trace[194 + rank] = globaltimer();
       if (half == 0) {
-        float o[16];
         read_out(o);
-        const int r = tid_h;
-        const int n_out = prm.n_out;
-        const long long nbase = node0 + static_cast<long long>(rank) * P;
-        if (r < P) {
-          const long long node = nbase + r;
-          if (node < prm.K)
-            for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
-        } else if (r < rows_used && prm.jac != nullptr) {
-          const int k = (r - P) / P, p = (r - P) % P;
-          const long long node = nbase + p;
-          if (node < prm.K)
-            for (int oo = 0; oo < n_out; ++oo) prm.jac[(node * n_out + oo) * n_in + k] = static_cast<double>(o[oo]);
-        }
+        write_out(o, prev_node0);
       }
-      tc_fence_before();
     }
    }
   }
-  if (prm.trace && pair == 0 && threadIdx.x == 0) {
+  if (tr_pair && threadIdx.x == 0) {
     prm.trace[252 + rank] = globaltimer();
     prm.trace[254 + rank] = clock64();
   }

@@ -361,7 +361,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     {
       const int j = grp * 128 + tid_h;
       float w0[kMaxIn0];
-      load_w0_row(prm.w0 + j * n_in, n_in, w0);
+      load_w0_row(prm.w0t, WP, j, n_in, w0);
       float val, sp;
       act_fwd(act, layer0_pre(__ldg(prm.b0 + j), w0, zs + half * n_in, n_in), val, sp);
       float v[NTC];

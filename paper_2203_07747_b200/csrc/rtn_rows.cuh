@@ -100,14 +100,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
       "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])));
 }
 
-// Remote arrive with the default (.release.cta) semantics, as CUTLASS's
-// ClusterBarrier::arrive(cta_id): TMEM data is ordered by the tcgen05 fences
-// around the barrier, so the cluster-scope release (MEMBAR.GPU) and acquire
-// (L1 invalidation) of mbar_arrive_cluster / mbar_wait_cluster are not needed.
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-
 // Activation for the rows kernel (TF32 mode only): SiLU through ex2.approx and
 // rcp.approx (~2 ulp in fp32, far below the 2^-11 tf32 operand rounding that
 // follows); tanh/relu as act_fwd.
