@@ -262,7 +262,7 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0, ac
     ach = fl / (d50 * 1e-6) / 1e12
     return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)], "device_p50_us": d50,
             "device_p99_us": dev[int(len(dev) * 0.99)], "steps": steps, "nodes": k, "order": order,
-            "precision": ["tf32", "3xtf32", "bf16x3"][precision],
+            "precision": ["tf32", "3xtf32", "bf16x3", "bf16"][precision],
             "roofline": {"bound": "tensor (serial layer chain)", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                          "frac": ach / tf32_peak if tf32_peak else None, "flop_per_step": fl,
                          "time": "device p50 (CUDA events)"}}
@@ -278,7 +278,7 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
     L = _lib.lib()
     out, runs = {}, {}
     fl = flops_per_node(sizes, 1)
-    for name in ("bf16x3", "3xtf32"):
+    for name in ("bf16x3", "3xtf32", "bf16"):
         m = make_mlp(sizes, "silu", "full", SEED)
         eng = m.engine(precision=_lib.PRECISIONS[name])
         eng._ensure(k, 1)
@@ -299,9 +299,11 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
         ach = k * fl / (ms * 1e-3) / 1e12
         out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": ach,
                      "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
-                     "hardware_frac": 3 * ach / tf32_peak if tf32_peak else None,
-                     "kernel": ("rtn_pair_kernel<512,8,1,24,3xTF32> (four main accumulators)" if name == "3xtf32"
-                                else "rtn_pair_kernel<512,4,4,80,bf16x3>")}
+                     "hardware_frac": ((3 if name != "bf16" else 0.5) * ach / tf32_peak) if tf32_peak else None,
+                     "hardware_frac_basis": "MMA passes x algorithmic FLOPs vs the TF32 peak (bf16 MMAs run at 2x tf32)",
+                     "kernel": {"3xtf32": "rtn_pair_kernel<512,8,1,24,3xTF32> (four main accumulators)",
+                                "bf16x3": "rtn_pair_kernel<512,4,4,80,bf16x3>",
+                                "bf16": "rtn_pair_kernel<512,8,4,80,bf16> (one kind::f16 pass)"}[name]}
         eng.close()
         runs[name] = (lambda f_, j_: (lambda idx: (f_[idx].cpu().numpy(), j_[idx].cpu().numpy())))(f, j)
     return out, runs
@@ -718,7 +720,7 @@ def run_ours(args, rank, world, local_rank):
                    "value_1thread": v_one, "sample_1thread": sample1, "cpu_model": cpu_model(),
                    "algorithm": "oracle/ restatement of proj/src/neural.cpp BatchedCore (reverse mode, fp64)"}
             if modes is not None:
-                order_ = {"tf32": mode_runs["tf32"], "3xtf32": mode_runs["3xtf32"], "bf16x3": mode_runs["bf16x3"]}
+                order_ = {k_: mode_runs[k_] for k_ in ("tf32", "3xtf32", "bf16x3", "bf16")}
                 parity = parity_leg(torch, eng, z, k, order_, threads)
         cfg4 = cfg4_bench(torch, tf32_peak, not args.no_cpu) if world == 1 and not args.no_modes else None
         blocks = None
@@ -784,6 +786,7 @@ def latency_suite(torch, tf32_peak, with_cpu):
              ("cfg3_12x512_N20_order2", SIZES, SEED, 20, 2, 0, "silu", 300),
              ("cfg3_12x512_N20_bf16x3", SIZES, SEED, 20, 1, 2, "silu", 300),
              ("cfg3_12x512_N20_3xtf32", SIZES, SEED, 20, 1, 1, "silu", 300),
+             ("cfg3_12x512_N20_bf16", SIZES, SEED, 20, 1, 3, "silu", 300),
              ("cfg2_5x256_N20", [17] + [256] * 5 + [6], 5256, 20, 1, 0, "silu", 1000),
              ("cfg1_2x64_N10", [17, 64, 64, 6], 2064, 10, 1, 0, "tanh", 1000)]
     out = {}

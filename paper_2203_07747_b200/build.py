@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-ccbin", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++",
 ]
 
-SOURCES = ["rtn_mpc.cu", "rtn_comm.cu", "rtn_pair_tf32.cu", "rtn_pair_3xtf32.cu", "rtn_pair_bf16x3.cu", "rtn_pair_order2.cu",
+SOURCES = ["rtn_mpc.cu", "rtn_comm.cu", "rtn_pair_tf32.cu", "rtn_pair_3xtf32.cu", "rtn_pair_bf16x3.cu", "rtn_pair_bf16.cu", "rtn_pair_order2.cu",
            "rtn_blocks.cu", "rtn_qpsolve.cu", "rtn_synth.cpp"]
 HEADERS = ["rtn_kernel.cuh", "rtn_pair.cuh", "rtn_pair_launch.cuh", "rtn_launch.h", "rtn_blocks.h", "rtn_quad.cuh",
            "rtn_qpsolve.h", "rtn_rows.cuh", "rtn_internal.h"]

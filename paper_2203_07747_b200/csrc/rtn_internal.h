@@ -66,7 +66,7 @@ struct rtn_model {
   void* d_wt_hidden = nullptr;  // split x (n_hidden-1)·wp rows x wp cols (fp32 or bf16)
   void* d_wt_last = nullptr;    // split x 16 rows x wp cols
   CUtensorMap tmap_h{}, tmap_l{};
-  int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3
+  int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3 / kBF16
   int lo_rows = 0;     // row offset of the lo tiles in the stacked hidden map
   ~rtn_model() {
     int prev;

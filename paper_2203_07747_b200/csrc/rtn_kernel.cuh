@@ -43,8 +43,10 @@ constexpr int kStageBytes = 16384;  // one weight stage: 128 neurons x 128 bytes
 constexpr int kThreads = 384;       // 4 control warps + 8 epilogue warps
 constexpr int kMaxOut = 16;
 
-// Precision modes of the pair kernel (rtn_pair.cuh): tf32, 3xtf32, bf16x3.
-enum : int { kTF32 = 0, k3xTF32 = 1, kBF16x3 = 2 };
+// Precision modes (rtn_pair.cuh): tf32, 3xtf32, bf16x3 and single-pass bf16.
+enum : int { kTF32 = 0, k3xTF32 = 1, kBF16x3 = 2, kBF16 = 3 };
+__host__ __device__ constexpr bool IsBf16Mode(int mode) { return mode == kBF16x3 || mode == kBF16; }
+__host__ __device__ constexpr bool IsSplitMode(int mode) { return mode == k3xTF32 || mode == kBF16x3; }
 
 struct KParams {
   const double* z;   // K x n_in
@@ -485,6 +487,31 @@ __device__ __forceinline__ void mma4_tf32_pair_commit(uint32_t d_tmem, uint64_t 
 }  // namespace rtn
 
 namespace rtn {
+// mma4_tf32_pair_commit for kind::f16 (bf16 operands, K = 16 per MMA = the
+// same 32 bytes of each operand row, so the descriptor steps are identical).
+__device__ __forceinline__ void mma4_bf16_pair_commit(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                      uint32_t accumulate, uint32_t bar, uint32_t bar2) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b16 m;\n\t"
+      "mov.b16 m, 3;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], m;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], m;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2)
+      : "memory");
+}
+
 // Split-operand pair MMA step (3xTF32 / BF16x3): with A = A_hi + A_lo and
 // B = B_hi + B_lo, D += A_hi·B_hi and D2 += A_hi·B_lo + A_lo·B_hi (the lo·lo
 // term is below the representation error). 3 passes x 4 K-steps of 32 bytes,

@@ -45,6 +45,8 @@ cudaError_t LaunchPair3xTF32(const KParams& prm, const CUtensorMap& th, const CU
                              int grid, cudaStream_t st);
 cudaError_t LaunchPairBF16x3(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
                              int grid, cudaStream_t st);
+cudaError_t LaunchPairBF16(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int wp, bool latency,
+                           int grid, cudaStream_t st);
 
 // Latency kernel on 4-CTA clusters (rtn_quad.cuh): width 512, order <= 1,
 // one node per CTA side, grid = 4 x ceil(K / 2).
@@ -53,6 +55,7 @@ cudaError_t LaunchQuadBF16x3(const KParams& prm, const CUtensorMap& th, const CU
                              cudaStream_t st);
 cudaError_t LaunchQuad3xTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
                              cudaStream_t st);
+cudaError_t LaunchQuadBF16(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 
 // Width-256 throughput kernel with the activations as the A operand in TMEM
 // (rtn_rows.cuh): TF32, order <= 1, 7 <= n_in <= 31, prm.P = 128 / (1 + n_in)

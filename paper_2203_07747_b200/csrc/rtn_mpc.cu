@@ -153,8 +153,12 @@ CUtensorMap MakeTmap(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows
 // TMA tensor maps (hi/lo stacked in the split precision modes).
 rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   Validate(hm);
-  if (prec != RTN_TF32 && prec != RTN_3XTF32 && prec != RTN_BF16X3) throw Error(RTN_ECONFIG, "unknown precision mode");
-  const int mode = prec == RTN_TF32 ? rtn::kTF32 : (prec == RTN_3XTF32 ? rtn::k3xTF32 : rtn::kBF16x3);
+  if (prec != RTN_TF32 && prec != RTN_3XTF32 && prec != RTN_BF16X3 && prec != RTN_BF16)
+    throw Error(RTN_ECONFIG, "unknown precision mode");
+  const int mode = prec == RTN_TF32     ? rtn::kTF32
+                   : prec == RTN_3XTF32 ? rtn::k3xTF32
+                   : prec == RTN_BF16X3 ? rtn::kBF16x3
+                                        : rtn::kBF16;
   const int L = static_cast<int>(hm.sizes.size()) - 1;
   const int n_in = hm.sizes.front(), n_out = hm.sizes.back();
   if (L < 2) throw Error(RTN_EUNSUPPORTED, "device path needs at least one hidden layer");
@@ -215,8 +219,8 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
     const int wp = pwp;  // pair packs use the pair width
     // Row-major operand copies for the pair kernel's TMA maps: [hi; lo] stacked
     // (split modes) in tf32-rounded fp32 or bf16.
-    const int split = mode == rtn::kTF32 ? 1 : 2;
-    const bool bf16 = mode == rtn::kBF16x3;
+    const int split = rtn::IsSplitMode(mode) ? 2 : 1;
+    const bool bf16 = rtn::IsBf16Mode(mode);
     const size_t hid_rows = static_cast<size_t>(std::max(H - 1, 1)) * wp;
     std::vector<float> th(split * hid_rows * wp, 0.0f), tl(static_cast<size_t>(split) * 16 * wp, 0.0f);
     auto put = [&](std::vector<float>& dst, size_t row, size_t col, double w) {
@@ -396,6 +400,7 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     prm.num_tiles = (K + 1) / 2;
     const int g4 = static_cast<int>(4 * prm.num_tiles);
     e = m->pair_mode == rtn::kBF16x3  ? rtn::LaunchQuadBF16x3(prm, m->tmap_h, m->tmap_l, g4, c->stream)
+        : m->pair_mode == rtn::kBF16   ? rtn::LaunchQuadBF16(prm, m->tmap_h, m->tmap_l, g4, c->stream)
         : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
                                        : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
@@ -424,6 +429,8 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     e = rtn::LaunchPairTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
   else if (m->pair_mode == rtn::k3xTF32)
     e = rtn::LaunchPair3xTF32(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
+  else if (m->pair_mode == rtn::kBF16)
+    e = rtn::LaunchPairBF16(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
   else
     e = rtn::LaunchPairBF16x3(prm, m->tmap_h, m->tmap_l, m->pair_wp, lat, grid, c->stream);
   if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));

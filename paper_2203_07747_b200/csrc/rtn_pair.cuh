@@ -15,6 +15,8 @@
 //             passes hi·hi + hi·lo + lo·hi; fp32-grade (1e-5 class).
 //   kBF16x3 : same split in bf16 (8+8 mantissa bits), three kind::f16 passes
 //             at twice the tf32 rate; operand bytes equal to tf32 mode.
+//   kBF16   : one kind::f16 pass on bf16 operands (8-bit mantissa): half the
+//             operand bytes and twice the MMA rate of tf32, ~8x its error.
 //
 // 3xTF32 accumulation (PairCfg::kChains): the tensor core adds each K = 8 MMA
 // into its fp32 accumulator with an error proportional to the running sum's
@@ -66,10 +68,10 @@ constexpr int kLastHalfBytes = 1024;  // output layer: 8 of the 16 output rows x
 // for 3xTF32 at width 512, 48 / 24 / 40 for order-2 tiles.
 template <int WP, int NSTAGE, int P, int NTC, int MODE, int ORD2 = 0>
 struct PairCfg {
-  static constexpr int kEB = MODE == kBF16x3 ? 2 : 4;  // operand element bytes
+  static constexpr int kEB = IsBf16Mode(MODE) ? 2 : 4;  // operand element bytes
   static constexpr int kCK = 128 / kEB;                // k per 128-byte chunk row
   static constexpr int kNKC = WP / kCK;                // chunks per layer input
-  static constexpr int kSplit = MODE == kTF32 ? 1 : 2; // operand buffers (hi[, lo])
+  static constexpr int kSplit = IsSplitMode(MODE) ? 2 : 1;  // operand buffers (hi[, lo])
   static constexpr int kCPG = 128 / kCK;               // chunks per 128-neuron K-group
   static constexpr int kNMB = WP / 256;                // 256-neuron blocks (pair M)
   static constexpr int kNG = WP / 128;                 // 128-neuron K-groups
@@ -251,8 +253,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== pair MMA issuer (leader CTA) ======================
     if (leader) {
-      const uint32_t idesc_h = MODE == kBF16x3 ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
-      const uint32_t idesc_o = MODE == kBF16x3 ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
+      const uint32_t idesc_h = IsBf16Mode(MODE) ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_o = IsBf16Mode(MODE) ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
       // descriptors advance by (bytes >> 4) in the start-address field
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
@@ -282,6 +284,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mma4_tf32_pair_commit(d, wa, xa, idesc, acc, smem_u32(&empty[st0]), bar2);
           else
             mma4_tf32_pair_commit(d, xa, wa, idesc, acc, smem_u32(&empty[st0]), bar2);
+        } else if constexpr (MODE == kBF16) {
+          if (weights_are_a)
+            mma4_bf16_pair_commit(d, wa, xa, idesc, acc, smem_u32(&empty[st0]), bar2);
+          else
+            mma4_bf16_pair_commit(d, xa, wa, idesc, acc, smem_u32(&empty[st0]), bar2);
         } else {
           const uint64_t ah = weights_are_a ? wa : xa, al = weights_are_a ? wb : xb;
           const uint64_t bh = weights_are_a ? xa : wa, bl = weights_are_a ? xb : wb;
@@ -296,7 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // main-pass accumulator of chunk c (rotating over kChains), and the
       // accumulate flags (TF32: a bool; split modes: bit 0 main, bit 1 correction)
       auto chain_acc = [&](int c) -> uint32_t {
-        if constexpr (MODE == kTF32) return c != 0;
+        if constexpr (!IsSplitMode(MODE)) return c != 0;
         else return (c >= C::kChains ? 1u : 0u) | (c != 0 ? 2u : 0u);
       };
       for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
@@ -392,6 +399,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const float h = to_tf32(x);
           if (local) st_shared_f32(a, h);
           else st_cluster_f32(a, h);
+        } else if constexpr (MODE == kBF16) {
+          const uint16_t h = bf16_rn_bits(x);
+          if (local) st_shared_u16(a, h);
+          else st_cluster_u16(a, h);
         } else if constexpr (MODE == k3xTF32) {
           const float h = to_tf32(x);
           const float lo = to_tf32(x - h);

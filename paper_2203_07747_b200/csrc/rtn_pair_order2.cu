@@ -16,15 +16,18 @@ template <int WP>
 static cudaError_t LaunchOrder2W(int mode, const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
                                  cudaStream_t st) {
   if (prm.nt == kNtc2) {
-    return mode == kTF32 ? LaunchPairT<WP, 8, 1, kNtc2, kTF32, 1>(prm, th, tl, grid, st)
-                         : LaunchPairT<WP, 8, 1, kNtc2, kBF16x3, 1>(prm, th, tl, grid, st);
+    if (mode == kTF32) return LaunchPairT<WP, 8, 1, kNtc2, kTF32, 1>(prm, th, tl, grid, st);
+    if (mode == kBF16) return LaunchPairT<WP, (WP == 256 ? 4 : 8), 1, kNtc2, kBF16, 1>(prm, th, tl, grid, st);
+    return LaunchPairT<WP, 8, 1, kNtc2, kBF16x3, 1>(prm, th, tl, grid, st);
   }
   if (prm.nt == 24) {
     if (mode == kTF32) return LaunchPairT<WP, 8, 1, 24, kTF32, 2>(prm, th, tl, grid, st);
+    if (mode == kBF16) return LaunchPairT<WP, (WP == 256 ? 4 : 8), 1, 24, kBF16, 2>(prm, th, tl, grid, st);
     if (mode == kBF16x3) return LaunchPairT<WP, 8, 1, 24, kBF16x3, 2>(prm, th, tl, grid, st);
     return LaunchPairT<WP, 4, 1, 24, k3xTF32, 2>(prm, th, tl, grid, st);
   }
   if (mode == kTF32) return LaunchPairT<WP, 4, 1, 40, kTF32, 2>(prm, th, tl, grid, st);
+  if (mode == kBF16) return LaunchPairT<WP, 4, 1, 40, kBF16, 2>(prm, th, tl, grid, st);
   if (mode == kBF16x3) return LaunchPairT<WP, 4, 1, 40, kBF16x3, 2>(prm, th, tl, grid, st);
   return LaunchPairT<WP, 2, 1, 40, k3xTF32, 2>(prm, th, tl, grid, st);
 }

@@ -49,7 +49,7 @@ cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUte
 PairGeom PairGeometry(int mode, int wp, bool latency, int n_in) {
   if (latency || (mode == k3xTF32 && wp == 512)) return {1, 24};
   const int ntc = 80;
-  int p = mode == kTF32 ? 16 : 4;
+  int p = (mode == kTF32 || mode == kBF16) ? 16 : 4;
   while (p > 1 && p * (1 + n_in) > ntc) p >>= 1;
   return {p, ntc};
 }

@@ -55,6 +55,30 @@ __device__ __forceinline__ void mma4_tf32_pair_commit_m(uint32_t d_tmem, uint64_
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2), "r"(mask), "r"(mask2)
       : "memory");
 }
+// The same for kind::f16 (single-pass bf16; K = 16 per MMA, same descriptor steps).
+__device__ __forceinline__ void mma4_bf16_pair_commit_m(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                        uint32_t accumulate, uint32_t bar, uint32_t mask,
+                                                        uint32_t bar2, uint32_t mask2) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b16 m, m2;\n\t"
+      "cvt.u16.u32 m, %7;\n\tcvt.u16.u32 m2, %8;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], m;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], m2;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(bar), "r"(bar2), "r"(mask), "r"(mask2)
+      : "memory");
+}
 // bf16x3 chunk (rtn_pair.cuh RTN_MMA12 with D2 == D) with masked multicast commits:
 // the two weight stages' empty barriers to `mask`, and `bar2` (if non-zero) to `mask2`.
 __device__ __forceinline__ void mma12_bf16_pair_commit_m(uint32_t d, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
@@ -219,8 +243,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== pair MMA issuer (pair leaders: ranks 0 and 2) ======
     if (leader) {
-      const uint32_t idesc_h = MODE == kBF16x3 ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);  // tf32: TF32, 3xTF32
-      const uint32_t idesc_o = MODE == kBF16x3 ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
+      const uint32_t idesc_h = IsBf16Mode(MODE) ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
+      const uint32_t idesc_o = IsBf16Mode(MODE) ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
       constexpr uint32_t kStageD = kStageBytes >> 4, kChunkD = C::kChunkStride >> 4, kSplitD = C::kSplitStride >> 4;
@@ -248,6 +272,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
             mma4_tf32_pair_commit_m(tmem_base, wa, xa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
           else
             mma4_tf32_pair_commit_m(tmem_base, xa, wa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
+        } else if constexpr (MODE == kBF16) {
+          if (weights_are_a)
+            mma4_bf16_pair_commit_m(tmem_base, wa, xa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
+          else
+            mma4_bf16_pair_commit_m(tmem_base, xa, wa, idesc, acc, smem_u32(&empty[st0]), pair_mask, bar2, mask2);
         } else {
           const uint64_t wb = wa + kStageD, xb = xa + kSplitD;
           if (weights_are_a)
@@ -327,6 +356,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
           const float h = to_tf32(v[i]);
           st_cluster_f32(dst0 + a, h);
           st_cluster_f32(dst1 + a, h);
+        } else if constexpr (MODE == kBF16) {
+          const uint16_t h = bf16_rn_bits(v[i]);
+          st_cluster_u16(dst0 + a, h);
+          st_cluster_u16(dst1 + a, h);
         } else if constexpr (MODE == k3xTF32) {  // tf32 hi and lo
           const float h = to_tf32(v[i]), lo = to_tf32(v[i] - h);
           st_cluster_f32(dst0 + a, h);

@@ -181,3 +181,15 @@ def test_order2_unsupported_shapes():
     r = make_mlp([6, 32, 4], "relu", "full", 3)        # proj/src/neural.cpp:176-177
     with pytest.raises(UnsupportedError):
         mlp_batched_eval(r, np.zeros((2, 6)), EvalOrder.HESSIAN)
+
+
+def test_order2_bf16_single_pass_documented_bounds():
+    """Order 2 in single-pass BF16 (8-bit mantissa operands): ~2e-3 on the
+    reference's small nets, 2.3e-3 at 12x512 gain 2.5 — the mode's measured
+    limit, asserted with margin."""
+    for sizes, act, gain, bound in (([6, 32, 32, 4], "tanh", 1.0, 5e-3), ([3, 16, 16, 2], "tanh", 1.0, 5e-3),
+                                    ([17] + [512] * 12 + [6], "silu", 2.0, 1e-3),
+                                    ([17] + [256] * 5 + [6], "silu", 1.5, 2e-3)):
+        ef, ej, eh, got = _errs(_net(sizes, act, gain), "bf16")
+        assert max(ef, ej, eh) < bound, (sizes, ef, ej, eh)
+        assert np.array_equal(got.hessians, np.swapaxes(got.hessians, 2, 3))

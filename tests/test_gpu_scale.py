@@ -81,3 +81,9 @@ def test_latency_tiles_forced_on_a_large_batch(monkeypatch):
     pair; forced here onto 3,000 nodes so every pair walks ~20 tiles."""
     err = _sampled(_net([17] + [512] * 6 + [6], "silu", 2.0), "tf32", 3000, "latency", monkeypatch, every=50)
     assert err < 1e-3, err
+
+
+def test_cfg5_shape_bf16_single_pass_many_tiles(monkeypatch):
+    """Single-pass BF16 on the throughput tiles (P = 4), 100k nodes, gain 2.0."""
+    err = _sampled(_net([17] + [512] * 12 + [6], "silu", 2.0), "bf16", 100352, None, monkeypatch)
+    assert err < 1e-3, err
