@@ -62,8 +62,18 @@ typedef enum { RTN_ACT_TANH = 0, RTN_ACT_RELU = 1, RTN_ACT_SILU = 2 } rtn_activa
 
 /* Loads an RMLP v1 (proj/src/neural.cpp:685-755) or v2 (SiLU tag 2) file,
  * folds the normalisation into the first/last layer and packs the weights
- * into the device layout. Replaces resmpc::LoadModel (neural.hpp:117). */
+ * into the device layout. Replaces resmpc::LoadModel (neural.hpp:117).
+ * Digest-keyed (FNV-1a 64 of the file bytes, proj/src/io.cpp:10-26): loading
+ * identical bytes again on the same device and precision returns the same
+ * shared, reference-counted handle (free each one with rtn_model_free); with
+ * RTN_PACK_CACHE=<dir> the packed device layout is also kept on disk as
+ * <dir>/<digest>-p<precision>.rtnp and reused by later processes. */
 rtn_status rtn_model_load_rmlp(const char* path, int device, rtn_precision p, rtn_model** out);
+
+/* The FNV-1a 64 digest (16 hex digits + NUL) of the RMLP file a model was
+ * loaded from ("" for rtn_model_from_arrays), and whether its packed layout
+ * came from the RTN_PACK_CACHE file. */
+rtn_status rtn_model_digest(const rtn_model* m, char out[17], int* from_pack_cache);
 
 /* Same from in-memory arrays (resmpc::MlpModel fields, neural.hpp:19-34).
  * W[l] is row-major sizes[l+1] x sizes[l]; b[l] has sizes[l+1] entries. */

@@ -20,7 +20,7 @@ VARIANTS = {"full": (0, 17, 6), "a": (1, 3, 3), "a_u": (2, 7, 3), "ground": (3, 
 
 # Every symbol include/rtn_mpc.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info",
+    "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info", "rtn_model_digest",
     "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
     "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_last_error",
     "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp", "rtn_solve_feedback",
@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
     L.rtn_model_free.argtypes = [_vp]
     L.rtn_model_free.restype = None
     L.rtn_model_info.argtypes = [_vp, _ip, _ip, _ip, _ip, _ip]
+    L.rtn_model_digest.argtypes = [_vp, C.c_char_p, _ip]
     L.rtn_ctx_create.argtypes = [_vp, C.c_longlong, C.c_int, C.c_int, C.POINTER(_vp)]
     L.rtn_ctx_free.argtypes = [_vp]
     L.rtn_ctx_free.restype = None

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -67,6 +68,11 @@ struct rtn_model {
   void* d_wt_last = nullptr;    // split x 16 rows x wp cols
   CUtensorMap tmap_h{}, tmap_l{};
   int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3 / kBF16
+  // rtn_model_load_rmlp's digest-keyed cache: shared handles are reference counted
+  int refs = 1;
+  uint64_t digest = 0;     // FNV-1a 64 of the RMLP file bytes
+  bool cached = false;     // registered in the in-process cache
+  bool from_pack = false;  // packed layout read from RTN_PACK_CACHE
   int lo_rows = 0;     // row offset of the lo tiles in the stacked hidden map
   ~rtn_model() {
     int prev;

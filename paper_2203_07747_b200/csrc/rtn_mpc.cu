@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -145,20 +148,30 @@ CUtensorMap MakeTmap(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows
   return m;
 }
 
+// The device layout of a model as host arrays: everything BuildModel uploads.
+// Written to / read from the packed-layout cache file (PackCache) unchanged.
+struct Packed {
+  int32_t mode = 0, n_in = 0, n_out = 0, n_layers = 0, act = 0, pwp = 0, split = 1, bf16 = 0;
+  std::vector<double> mu;                  // in_mean (fp64)
+  std::vector<float> w0, w0t, b0, bl, bh;  // layer 0 (neuron- and input-major), biases
+  std::vector<uint8_t> th, tl;             // hidden / output operand copies (fp32 or bf16 bytes)
+};
+
 // Folds the normalisation into the first/last layer in fp64
 // (proj/include/resmpc/neural.hpp:14-18: y = out_scale ⊙ net((z−μ)⊘s) + out_mean):
 //   W0' = W0·diag(1/s)   (μ is subtracted from z in fp64 by the kernels, load_z),
 //   WL' = diag(out_scale)·WL,  bL' = out_scale ⊙ bL + out_mean,
-// then packs the hidden and output layers as row-major operand copies behind
+// and packs the hidden and output layers as row-major operand copies for the
 // TMA tensor maps (hi/lo stacked in the split precision modes).
-rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
+Packed PackModel(const HostModel& hm, rtn_precision prec) {
   Validate(hm);
   if (prec != RTN_TF32 && prec != RTN_3XTF32 && prec != RTN_BF16X3 && prec != RTN_BF16)
     throw Error(RTN_ECONFIG, "unknown precision mode");
-  const int mode = prec == RTN_TF32     ? rtn::kTF32
-                   : prec == RTN_3XTF32 ? rtn::k3xTF32
-                   : prec == RTN_BF16X3 ? rtn::kBF16x3
-                                        : rtn::kBF16;
+  Packed pk;
+  pk.mode = prec == RTN_TF32     ? rtn::kTF32
+            : prec == RTN_3XTF32 ? rtn::k3xTF32
+            : prec == RTN_BF16X3 ? rtn::kBF16x3
+                                 : rtn::kBF16;
   const int L = static_cast<int>(hm.sizes.size()) - 1;
   const int n_in = hm.sizes.front(), n_out = hm.sizes.back();
   if (L < 2) throw Error(RTN_EUNSUPPORTED, "device path needs at least one hidden layer");
@@ -167,17 +180,78 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   if (n_out > rtn::kMaxOut) throw Error(RTN_EUNSUPPORTED, "n_out > 16 not supported");
   if (n_in > 79) throw Error(RTN_EUNSUPPORTED, "n_in > 79 not supported");
   const int H = L - 1;  // hidden layers (each followed by the activation)
-
+  pk.n_in = n_in;
+  pk.n_out = n_out;
+  pk.n_layers = L;
+  pk.act = hm.act;
+  pk.pwp = pwp;
+  pk.mu = hm.in_mean;
   // layer 0 (CUDA cores, fp32): W0' = W0·diag(1/in_scale); the bias stays b0
-  std::vector<float> w0(static_cast<size_t>(pwp) * n_in, 0.0f), b0(pwp, 0.0f);
+  pk.w0.assign(static_cast<size_t>(pwp) * n_in, 0.0f);
+  pk.w0t.assign(static_cast<size_t>(pwp) * n_in, 0.0f);
+  pk.b0.assign(pwp, 0.0f);
   for (int j = 0; j < hm.sizes[1]; ++j) {
-    for (int k = 0; k < n_in; ++k)
-      w0[static_cast<size_t>(j) * n_in + k] = static_cast<float>(hm.W[0][static_cast<size_t>(j) * n_in + k] / hm.in_scale[k]);
-    b0[j] = static_cast<float>(hm.b[0][j]);
+    for (int k = 0; k < n_in; ++k) {
+      const float w = static_cast<float>(hm.W[0][static_cast<size_t>(j) * n_in + k] / hm.in_scale[k]);
+      pk.w0[static_cast<size_t>(j) * n_in + k] = w;
+      pk.w0t[static_cast<size_t>(k) * pwp + j] = w;
+    }
+    pk.b0[j] = static_cast<float>(hm.b[0][j]);
   }
-  std::vector<float> bl(rtn::kMaxOut, 0.0f);
-  for (int o = 0; o < n_out; ++o) bl[o] = static_cast<float>(hm.out_scale[o] * hm.b[L - 1][o] + hm.out_mean[o]);
+  pk.bl.assign(rtn::kMaxOut, 0.0f);
+  for (int o = 0; o < n_out; ++o) pk.bl[o] = static_cast<float>(hm.out_scale[o] * hm.b[L - 1][o] + hm.out_mean[o]);
+  pk.bh.assign(static_cast<size_t>(std::max(H - 1, 1)) * pwp, 0.0f);
+  for (int l = 1; l < H; ++l)
+    for (int j = 0; j < hm.sizes[l + 1]; ++j) pk.bh[static_cast<size_t>(l - 1) * pwp + j] = static_cast<float>(hm.b[l][j]);
+  // Row-major operand copies for the TMA maps: [hi; lo] stacked (split modes),
+  // tf32-rounded fp32 or bf16.
+  const int wp = pwp;
+  pk.split = rtn::IsSplitMode(pk.mode) ? 2 : 1;
+  pk.bf16 = rtn::IsBf16Mode(pk.mode);
+  const int split = pk.split;
+  const bool bf16 = pk.bf16;
+  const size_t hid_rows = static_cast<size_t>(std::max(H - 1, 1)) * wp;
+  std::vector<float> th(split * hid_rows * wp, 0.0f), tl(static_cast<size_t>(split) * 16 * wp, 0.0f);
+  auto put = [&](std::vector<float>& dst, size_t row, size_t col, double w) {
+    // hi part, then the residual in the second half of the stack
+    if (bf16) {
+      const float h = RoundBf16(static_cast<float>(w));
+      dst[row * wp + col] = h;
+      if (split == 2) dst[(row + dst.size() / (2 * wp)) * wp + col] = RoundBf16(static_cast<float>(w - h));
+    } else {
+      const float h = RoundTf32(static_cast<float>(w));
+      dst[row * wp + col] = h;
+      if (split == 2) dst[(row + dst.size() / (2 * wp)) * wp + col] = RoundTf32(static_cast<float>(w - h));
+    }
+  };
+  for (int l = 1; l < H; ++l) {
+    const int rows = hm.sizes[l + 1], cols = hm.sizes[l];
+    for (int j = 0; j < rows; ++j)
+      for (int k = 0; k < cols; ++k) put(th, static_cast<size_t>(l - 1) * wp + j, k, hm.W[l][static_cast<size_t>(j) * cols + k]);
+  }
+  {
+    const int cols = hm.sizes[L - 1];
+    for (int o = 0; o < n_out; ++o)
+      for (int k = 0; k < cols; ++k) put(tl, o, k, hm.out_scale[o] * hm.W[L - 1][static_cast<size_t>(o) * cols + k]);
+  }
+  auto bytes = [&](const std::vector<float>& v, std::vector<uint8_t>& out) {
+    if (bf16) {
+      out.resize(v.size() * 2);
+      for (size_t i = 0; i < v.size(); ++i) {
+        const uint16_t h = Bf16Bits(v[i]);
+        std::memcpy(out.data() + 2 * i, &h, 2);
+      }
+    } else {
+      out.resize(v.size() * 4);
+      std::memcpy(out.data(), v.data(), out.size());
+    }
+  };
+  bytes(th, pk.th);
+  bytes(tl, pk.tl);
+  return pk;
+}
 
+rtn_model* UploadModel(const Packed& pk, int device) {
   int ndev = 0;
   CUDA_CHECK(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) throw Error(RTN_ECUDA, "invalid device ordinal");
@@ -187,90 +261,138 @@ rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
   CUDA_CHECK(cudaSetDevice(device));
   std::unique_ptr<rtn_model> m(new rtn_model());
   m->device = device;
-  m->prec = prec;
-  m->n_in = n_in;
-  m->n_out = n_out;
-  m->n_layers = L;
-  m->n_hidden = H;
-  m->act = hm.act;
-  m->wp = pwp;
+  m->prec = pk.mode == rtn::kTF32 ? RTN_TF32 : pk.mode == rtn::k3xTF32 ? RTN_3XTF32 : pk.mode == rtn::kBF16x3 ? RTN_BF16X3 : RTN_BF16;
+  m->n_in = pk.n_in;
+  m->n_out = pk.n_out;
+  m->n_layers = pk.n_layers;
+  m->n_hidden = pk.n_layers - 1;
+  m->act = pk.act;
+  m->wp = pk.pwp;
+  m->pair_wp = pk.pwp;
+  m->pair_mode = pk.mode;
   auto up = [](void** d, const void* h, size_t n) {
     CUDA_CHECK(cudaMalloc(d, std::max<size_t>(n, 16)));
     if (n) CUDA_CHECK(cudaMemcpy(*d, h, n, cudaMemcpyHostToDevice));
   };
-  up(reinterpret_cast<void**>(&m->d_mu), hm.in_mean.data(), hm.in_mean.size() * 8);
-  up(reinterpret_cast<void**>(&m->d_w0), w0.data(), w0.size() * 4);
-  {
-    std::vector<float> w0t(w0.size(), 0.0f);
-    for (int j = 0; j < pwp; ++j)
-      for (int k = 0; k < n_in; ++k) w0t[static_cast<size_t>(k) * pwp + j] = w0[static_cast<size_t>(j) * n_in + k];
-    up(reinterpret_cast<void**>(&m->d_w0t), w0t.data(), w0t.size() * 4);
-  }
-  up(reinterpret_cast<void**>(&m->d_b0), b0.data(), b0.size() * 4);
-  up(reinterpret_cast<void**>(&m->d_bl), bl.data(), bl.size() * 4);
-  {
-    std::vector<float> bh2(static_cast<size_t>(std::max(H - 1, 1)) * pwp, 0.0f);
-    for (int l = 1; l < H; ++l)
-      for (int j = 0; j < hm.sizes[l + 1]; ++j) bh2[static_cast<size_t>(l - 1) * pwp + j] = static_cast<float>(hm.b[l][j]);
-    up(reinterpret_cast<void**>(&m->d_bh_pair), bh2.data(), bh2.size() * 4);
-  }
-  m->pair_wp = pwp;
-  {
-    const int wp = pwp;  // pair packs use the pair width
-    // Row-major operand copies for the pair kernel's TMA maps: [hi; lo] stacked
-    // (split modes) in tf32-rounded fp32 or bf16.
-    const int split = rtn::IsSplitMode(mode) ? 2 : 1;
-    const bool bf16 = rtn::IsBf16Mode(mode);
-    const size_t hid_rows = static_cast<size_t>(std::max(H - 1, 1)) * wp;
-    std::vector<float> th(split * hid_rows * wp, 0.0f), tl(static_cast<size_t>(split) * 16 * wp, 0.0f);
-    auto put = [&](std::vector<float>& dst, size_t row, size_t col, double w) {
-      // hi part, then the residual in the second half of the stack
-      if (bf16) {
-        const float h = RoundBf16(static_cast<float>(w));
-        dst[row * wp + col] = h;
-        if (split == 2) dst[(row + dst.size() / (2 * wp)) * wp + col] = RoundBf16(static_cast<float>(w - h));
-      } else {
-        const float h = RoundTf32(static_cast<float>(w));
-        dst[row * wp + col] = h;
-        if (split == 2) dst[(row + dst.size() / (2 * wp)) * wp + col] = RoundTf32(static_cast<float>(w - h));
-      }
-    };
-    for (int l = 1; l < H; ++l) {
-      const int rows = hm.sizes[l + 1], cols = hm.sizes[l];
-      for (int j = 0; j < rows; ++j)
-        for (int k = 0; k < cols; ++k)
-          put(th, static_cast<size_t>(l - 1) * wp + j, k, hm.W[l][static_cast<size_t>(j) * cols + k]);
-    }
-    {
-      const int cols = hm.sizes[L - 1];
-      for (int o = 0; o < n_out; ++o)
-        for (int k = 0; k < cols; ++k) put(tl, o, k, hm.out_scale[o] * hm.W[L - 1][static_cast<size_t>(o) * cols + k]);
-    }
-    if (bf16) {
-      std::vector<uint16_t> bh16(th.size()), bl16(tl.size());
-      for (size_t i = 0; i < th.size(); ++i) bh16[i] = Bf16Bits(th[i]);
-      for (size_t i = 0; i < tl.size(); ++i) bl16[i] = Bf16Bits(tl[i]);
-      up(&m->d_wt_hidden, bh16.data(), bh16.size() * 2);
-      up(&m->d_wt_last, bl16.data(), bl16.size() * 2);
-    } else {
-      up(&m->d_wt_hidden, th.data(), th.size() * 4);
-      up(&m->d_wt_last, tl.data(), tl.size() * 4);
-    }
-    m->tmap_h = MakeTmap(m->d_wt_hidden, split * hid_rows, wp, 128, bf16);
-    m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(split) * 16, wp, 8, bf16);
-    m->pair_mode = mode;
-    m->lo_rows = static_cast<int>(hid_rows);
-  }
+  up(reinterpret_cast<void**>(&m->d_mu), pk.mu.data(), pk.mu.size() * 8);
+  up(reinterpret_cast<void**>(&m->d_w0), pk.w0.data(), pk.w0.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_w0t), pk.w0t.data(), pk.w0t.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_b0), pk.b0.data(), pk.b0.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_bl), pk.bl.data(), pk.bl.size() * 4);
+  up(reinterpret_cast<void**>(&m->d_bh_pair), pk.bh.data(), pk.bh.size() * 4);
+  up(&m->d_wt_hidden, pk.th.data(), pk.th.size());
+  up(&m->d_wt_last, pk.tl.data(), pk.tl.size());
+  const size_t hid_rows = static_cast<size_t>(std::max(pk.n_layers - 2, 1)) * pk.pwp;
+  m->tmap_h = MakeTmap(m->d_wt_hidden, pk.split * hid_rows, pk.pwp, 128, pk.bf16);
+  m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(pk.split) * 16, pk.pwp, 8, pk.bf16);
+  m->lo_rows = static_cast<int>(hid_rows);
   return m.release();
 }
 
-// RMLP v1/v2 reader (proj/src/neural.cpp:720-755; v2 adds activation tag 2).
-HostModel ReadRmlp(const char* path) {
+rtn_model* BuildModel(const HostModel& hm, int device, rtn_precision prec) {
+  return UploadModel(PackModel(hm, prec), device);
+}
+
+// ---- digest-keyed packed-layout cache -------------------
+// FNV-1a 64 of the RMLP file bytes, the reference's manifest digest
+// (/root/reference/proj/src/io.cpp:10-26, Fnv1a64File).
+uint64_t Fnv1a64(const std::vector<char>& bytes) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (char c : bytes) {
+    h ^= static_cast<unsigned char>(c);
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+std::string Hex16(uint64_t v) {
+  char buf[17];
+  std::snprintf(buf, sizeof(buf), "%016llx", static_cast<unsigned long long>(v));
+  return buf;
+}
+
+// On-disk copy of a Packed layout ("RTNP" v1): header, then the arrays. Keyed by
+// the source file's digest and the precision, so a changed model never matches.
+constexpr uint32_t kPackVersion = 1;
+bool WritePacked(const std::string& path, uint64_t digest, const Packed& pk) {
+  std::ofstream out(path + ".tmp", std::ios::binary);
+  if (!out) return false;
+  auto w = [&](const void* p, size_t n) { out.write(static_cast<const char*>(p), static_cast<std::streamsize>(n)); };
+  auto wv = [&](const auto& v) {
+    const uint64_t n = v.size();
+    w(&n, 8);
+    w(v.data(), n * sizeof(v[0]));
+  };
+  w("RTNP", 4);
+  w(&kPackVersion, 4);
+  w(&digest, 8);
+  const int32_t hdr[8] = {pk.mode, pk.n_in, pk.n_out, pk.n_layers, pk.act, pk.pwp, pk.split, pk.bf16};
+  w(hdr, sizeof(hdr));
+  wv(pk.mu);
+  wv(pk.w0);
+  wv(pk.w0t);
+  wv(pk.b0);
+  wv(pk.bl);
+  wv(pk.bh);
+  wv(pk.th);
+  wv(pk.tl);
+  out.close();
+  if (!out) return false;
+  return std::rename((path + ".tmp").c_str(), path.c_str()) == 0;
+}
+
+bool ReadPacked(const std::string& path, uint64_t digest, int mode, Packed* pk) {
   std::ifstream in(path, std::ios::binary);
-  if (!in) throw Error(RTN_ECONFIG, std::string("model: cannot open '") + path + "'");
+  if (!in) return false;
+  auto r = [&](void* p, size_t n) {
+    in.read(static_cast<char*>(p), static_cast<std::streamsize>(n));
+    return static_cast<bool>(in);
+  };
+  auto rv = [&](auto& v) {
+    uint64_t n = 0;
+    if (!r(&n, 8) || n > (1ull << 32)) return false;
+    v.resize(n);
+    return r(v.data(), n * sizeof(v[0]));
+  };
+  char magic[4];
+  uint32_t ver = 0;
+  uint64_t dg = 0;
+  int32_t hdr[8];
+  if (!r(magic, 4) || std::memcmp(magic, "RTNP", 4) != 0 || !r(&ver, 4) || ver != kPackVersion || !r(&dg, 8) ||
+      dg != digest || !r(hdr, sizeof(hdr)) || hdr[0] != mode)
+    return false;
+  pk->mode = hdr[0];
+  pk->n_in = hdr[1];
+  pk->n_out = hdr[2];
+  pk->n_layers = hdr[3];
+  pk->act = hdr[4];
+  pk->pwp = hdr[5];
+  pk->split = hdr[6];
+  pk->bf16 = hdr[7];
+  return rv(pk->mu) && rv(pk->w0) && rv(pk->w0t) && rv(pk->b0) && rv(pk->bl) && rv(pk->bh) && rv(pk->th) &&
+         rv(pk->tl);
+}
+
+// In-process cache: one packed device model per (file digest, device,
+// precision), shared by every rtn_model_load_rmlp of identical bytes and freed
+// with its last handle.
+struct CacheKey {
+  uint64_t digest;
+  int device, prec;
+  bool operator<(const CacheKey& o) const {
+    return std::tie(digest, device, prec) < std::tie(o.digest, o.device, o.prec);
+  }
+};
+std::mutex g_cache_mu;
+std::map<CacheKey, rtn_model*> g_cache;
+
+// RMLP v1/v2 parser of a file's bytes (proj/src/neural.cpp:720-755; v2 adds activation tag 2).
+HostModel ParseRmlp(const std::vector<char>& bytes) {
+  size_t pos = 0;
   auto rd = [&](void* p, size_t n) {
-    in.read(reinterpret_cast<char*>(p), static_cast<std::streamsize>(n));
-    if (!in) throw Error(RTN_ECONFIG, "unexpected end of file");
+    if (n > bytes.size() - pos) throw Error(RTN_ECONFIG, "unexpected end of file");
+    std::memcpy(p, bytes.data() + pos, n);
+    pos += n;
   };
   char magic[4];
   rd(magic, 4);
@@ -454,7 +576,61 @@ int rtn_debug_trace(unsigned long long* out, int n) {
 rtn_status rtn_model_load_rmlp(const char* path, int device, rtn_precision p, rtn_model** out) {
   return Guard([&] {
     if (!path || !out) throw Error(RTN_ECONFIG, "null argument");
-    *out = BuildModel(ReadRmlp(path), device, p);
+    std::vector<char> bytes;
+    {
+      std::ifstream in(path, std::ios::binary);
+      if (!in) throw Error(RTN_ECONFIG, std::string("model: cannot open '") + path + "'");
+      bytes.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+    }
+    const uint64_t digest = Fnv1a64(bytes);
+    const CacheKey key{digest, device, static_cast<int>(p)};
+    {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      auto it = g_cache.find(key);
+      if (it != g_cache.end()) {  // identical bytes already on this device in this precision
+        ++it->second->refs;
+        *out = it->second;
+        return;
+      }
+    }
+    // RTN_PACK_CACHE=<dir>: the packed device layout on disk, keyed by the digest
+    const char* dir = std::getenv("RTN_PACK_CACHE");
+    const int mode = p == RTN_TF32 ? rtn::kTF32 : p == RTN_3XTF32 ? rtn::k3xTF32 : p == RTN_BF16X3 ? rtn::kBF16x3 : rtn::kBF16;
+    const std::string pack_path = dir ? std::string(dir) + "/" + Hex16(digest) + "-p" + std::to_string(p) + ".rtnp" : "";
+    Packed pk;
+    bool from_pack = !pack_path.empty() && ReadPacked(pack_path, digest, mode, &pk);
+    if (!from_pack) {
+      pk = PackModel(ParseRmlp(bytes), p);
+      if (!pack_path.empty()) WritePacked(pack_path, digest, pk);
+    }
+    rtn_model* m = UploadModel(pk, device);
+    m->digest = digest;
+    m->from_pack = from_pack;
+    m->cached = true;
+    {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      auto it = g_cache.find(key);
+      if (it != g_cache.end()) {  // another thread loaded it meanwhile
+        ++it->second->refs;
+        *out = it->second;
+        m->cached = false;
+        delete m;
+        return;
+      }
+      g_cache[key] = m;
+    }
+    *out = m;
+  });
+}
+
+// FNV-1a 64 digest (hex) of the RMLP file a model was loaded from ("" for models
+// built from arrays) and whether its packed layout came from the on-disk cache.
+rtn_status rtn_model_digest(const rtn_model* m, char out[17], int* from_pack_cache) {
+  return Guard([&] {
+    if (!m || !out) throw Error(RTN_ECONFIG, "null argument");
+    const std::string h = m->cached || m->digest ? Hex16(m->digest) : std::string();
+    std::memcpy(out, h.c_str(), h.size() + 1);
+    if (from_pack_cache) *from_pack_cache = m->from_pack ? 1 : 0;
   });
 }
 
@@ -483,7 +659,17 @@ rtn_status rtn_model_from_arrays(const int* sizes, int n_sizes, int activation, 
   });
 }
 
-void rtn_model_free(rtn_model* m) { delete m; }
+void rtn_model_free(rtn_model* m) {
+  if (!m) return;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (m->cached) {
+      if (--m->refs > 0) return;
+      g_cache.erase(CacheKey{m->digest, m->device, static_cast<int>(m->prec)});
+    }
+  }
+  delete m;
+}
 
 rtn_status rtn_model_info(const rtn_model* m, int* n_in, int* n_out, int* n_layers, int* activation,
                           int* padded_width) {

@@ -751,8 +751,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr bool kMayBeWide = P < 4 && NTC / P - 1 > kMaxIn0;  // small-P tiles may see > kMaxIn0 inputs
     float val0[kG0][P], sp0[kG0][P];
     auto layer0_math = [&]() {
-#pragma unroll
       const float* zside = zs + static_cast<int>(rank) * P * n_in;  // this CTA's nodes
+#pragma unroll
       for (int gi = 0; gi < kG0; ++gi) {
         const int j = (half + 2 * gi) * 128 + tid_h;
         const float bj = __ldg(prm.b0 + j);

