@@ -110,6 +110,14 @@ rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int or
 rtn_status rtn_ctx_set_stream(rtn_ctx* c, void* cuda_stream);
 rtn_status rtn_ctx_synchronize(rtn_ctx* c);
 
+/* NaN/Inf flag (failure detection): 1 if an output value written by
+ * the context's kernels since the last reset is not finite. Every blocking
+ * call (rtn_prepare, rtn_cycle_qp) resets it first, so after one it describes
+ * that call; after device-pointer calls it accumulates until reset. The
+ * reference's controller policy on a bad cycle (reuse the last command,
+ * sqp_rti.cpp:233-267) stays with the caller. Synchronises the context stream. */
+rtn_status rtn_ctx_nonfinite(rtn_ctx* c, int* flag, int reset);
+
 /* Counters (EvalCounters::batched_calls / batched_points, neural.hpp:38-44)
  * and the number of device kernel launches this context has issued. */
 rtn_status rtn_ctx_counters(const rtn_ctx* c, unsigned long long* batched_calls,

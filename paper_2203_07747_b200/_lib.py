@@ -22,7 +22,7 @@ VARIANTS = {"full": (0, 17, 6), "a": (1, 3, 3), "a_u": (2, 7, 3), "ground": (3, 
 EXPORTS = (
     "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info", "rtn_model_digest",
     "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
-    "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_last_error",
+    "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_ctx_nonfinite", "rtn_last_error",
     "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp", "rtn_solve_feedback",
     "rtn_comm_unique_id", "rtn_comm_create", "rtn_comm_free", "rtn_prepare_partitioned",
     "rtn_prepare_partitioned_device",
@@ -92,6 +92,7 @@ def lib() -> C.CDLL:
                                      C.c_void_p]
     L.rtn_ctx_set_stream.argtypes = [_vp, _vp]
     L.rtn_ctx_synchronize.argtypes = [_vp]
+    L.rtn_ctx_nonfinite.argtypes = [_vp, _ip, C.c_int]
     L.rtn_ctx_counters.argtypes = [_vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong),
                                    C.POINTER(C.c_ulonglong)]
     L.rtn_build_qp.argtypes = [_vp, C.POINTER(QuadParamsC), C.POINTER(OcpConfigC), C.c_longlong,

@@ -251,6 +251,7 @@ void rtn_comm_free(rtn_comm* cm) {
 rtn_status rtn_prepare_partitioned_device(rtn_ctx* c, rtn_comm* cm, const double* d_z, long long K_local, int order,
                                           double* d_f, double* d_jac, int root, double* d_f_all, double* d_jac_all,
                                           int chunks) {
+  NvtxRange nvtx("rtn_prepare_partitioned_device");
   return Guard([&] {
     CheckPartitioned(c, cm, K_local, order, root);
     if (K_local > 0 && (!d_z || !d_f || (order >= 1 && !d_jac))) throw Error(RTN_ECONFIG, "null buffer");
@@ -264,6 +265,7 @@ rtn_status rtn_prepare_partitioned_device(rtn_ctx* c, rtn_comm* cm, const double
 
 rtn_status rtn_prepare_partitioned(rtn_ctx* c, rtn_comm* cm, const double* z_local, long long K_local, int n_cols,
                                    int order, int root, double* f_all, double* jac_all) {
+  NvtxRange nvtx("rtn_prepare_partitioned");
   return Guard([&] {
     CheckPartitioned(c, cm, K_local, order, root);
     const rtn_model* m = c->model;

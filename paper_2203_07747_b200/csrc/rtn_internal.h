@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rtn_mpc.h"
 #include "rtn_blocks.h"
 #include "rtn_launch.h"
@@ -108,6 +110,7 @@ struct rtn_ctx {
   double* h_jac = nullptr;
   int num_sms = 148;
   unsigned long long calls = 0, points = 0, launches = 0;
+  unsigned int* h_nonfinite = nullptr;  // host-mapped NaN/Inf flag the output epilogues raise
   // end-to-end pipeline: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_k;
@@ -177,12 +180,21 @@ struct rtn_ctx {
       cudaFree(d_fb);
       cudaFree(d_fb_small);
       cudaFreeHost(h_status);
+      cudaFreeHost(h_nonfinite);
       cudaSetDevice(prev);
     }
   }
 };
 
 namespace rtn_host {
+
+// NVTX range over one C-ABI call (visible in Nsight Systems / ncu --nvtx).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kMaxChunks = 8;  // end-to-end pipeline depth (chunks per call)
 

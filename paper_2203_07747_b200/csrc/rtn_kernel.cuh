@@ -64,6 +64,7 @@ struct KParams {
   int trace_tile;    // which of pair 0's tiles is traced (RTN_TRACE = 1 + index)
   int dbg;           // perf-isolation switches (RTN_DEBUG): 4 = skip epilogue math, 8 = local stores, 128 = stream only
   const double* mu;  // n_in: in_mean, subtracted in fp64 before the fp32 layer 0
+  unsigned int* nonfinite;  // host-mapped flag: set when a written f/J/H value is NaN or Inf
   const float* w0;   // WP x n_in   (W0·diag(1/in_scale)), neuron-major (rows kernel staging)
   const float* w0t;  // n_in x WP   the same, input-major: a warp's 32 neurons read 128 contiguous bytes
   const float* b0;   // WP          (the layer-0 bias; the mean is NOT folded in)
@@ -108,6 +109,16 @@ __device__ __forceinline__ double load_z(const KParams& prm, long long node, int
     v = k < 13 ? prm.zx[xrow * 13 + k] : prm.zu[node * 4 + (k - 13)];
   }
   return v - __ldg(prm.mu + k);
+}
+
+// Per-call NaN/Inf flag: a thread about to write the outputs o[0..n)
+// of one row raises the context's flag if any of them is not finite.
+__device__ __forceinline__ void note_nonfinite(const KParams& prm, const float* o, int n) {
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kMaxOut; ++i)
+    if (i < n) bad |= !isfinite(o[i]);
+  if (bad && prm.nonfinite != nullptr) atomicOr(prm.nonfinite, 1u);
 }
 
 // ----------------------------------------------------------------------------

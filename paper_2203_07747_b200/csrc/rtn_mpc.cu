@@ -489,6 +489,7 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   prm.order = order;
   prm.lo_rows = m->lo_rows;
   prm.mu = m->d_mu;
+  prm.nonfinite = c->h_nonfinite;
   prm.w0 = m->d_w0;
   prm.w0t = m->d_w0t;
   prm.b0 = m->d_b0;
@@ -711,6 +712,8 @@ rtn_status rtn_ctx_create(const rtn_model* m, long long max_rows, int max_order,
       CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
     }
     c->stream = c->own_stream;
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_nonfinite), sizeof(unsigned int), cudaHostAllocMapped));
+    *c->h_nonfinite = 0;
     const size_t zb = sizeof(double) * max_rows * m->n_in, fb = sizeof(double) * max_rows * m->n_out,
                  jb = fb * m->n_in;
     CUDA_CHECK(cudaMalloc(&c->d_z, zb));
@@ -735,6 +738,15 @@ rtn_status rtn_ctx_synchronize(rtn_ctx* c) {
   return Guard([&] {
     if (!c) throw Error(RTN_ECONFIG, "null context");
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+rtn_status rtn_ctx_nonfinite(rtn_ctx* c, int* flag, int reset) {
+  return Guard([&] {
+    if (!c || !flag) throw Error(RTN_ECONFIG, "null argument");
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    *flag = *c->h_nonfinite ? 1 : 0;
+    if (reset) *c->h_nonfinite = 0;
   });
 }
 
@@ -784,8 +796,10 @@ extern "C" {
 
 rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int order, double* f, double* jac,
                        double* hess) {
+  NvtxRange nvtx("rtn_prepare");
   return Guard([&] {
     CheckCall(c, K, order);
+    *c->h_nonfinite = 0;  // per-call flag (the call is blocking: no kernel of this context is in flight)
     const rtn_model* m = c->model;
     if (n_cols != m->n_in)
       throw Error(RTN_EDOMAIN, "mlp eval: feature dim " + std::to_string(n_cols) + " does not match model input " +
@@ -917,6 +931,7 @@ rtn_status rtn_prepare(rtn_ctx* c, const double* z, long long K, int n_cols, int
 
 rtn_status rtn_prepare_device(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac,
                               double* d_hess) {
+  NvtxRange nvtx("rtn_prepare_device");
   return Guard([&] {
     CheckCall(c, K, order);
     if (d_hess != nullptr && order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless order == 2");
@@ -1313,6 +1328,7 @@ extern "C" {
 
 rtn_status rtn_build_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
                         const rtn_iterate* it, const rtn_approx* ap, rtn_qp_blocks* out, unsigned long long* fevals) {
+  NvtxRange nvtx("rtn_build_qp");
   return Guard([&] {
     RunQp(c, p, cfg, n_inst, it, ap, out, false, nullptr, nullptr, nullptr);
     if (fevals) {  // FevalCounter: 4 values + 4 Jacobians per node (integrator.cpp:79-82)
@@ -1324,6 +1340,7 @@ rtn_status rtn_build_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_conf
 
 rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
                                const rtn_iterate* it, const rtn_approx* ap, rtn_qp_blocks* out) {
+  NvtxRange nvtx("rtn_build_qp_device");
   return Guard([&] {
     if (!c || !p || !cfg || !it || !ap || !out) throw Error(RTN_ECONFIG, "null argument");
     ValidateQuad(*p);
@@ -1370,8 +1387,10 @@ rtn_status rtn_build_qp_device(rtn_ctx* c, const rtn_quad_params* p, const rtn_o
 
 rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long long n_inst,
                         const rtn_iterate* it, rtn_qp_blocks* out, double* f, double* jac, double* hess) {
+  NvtxRange nvtx("rtn_cycle_qp");
   return Guard([&] {
     if (hess && cfg && cfg->taylor_order != 2) throw Error(RTN_ECONFIG, "hess must be NULL unless taylor_order == 2");
+    if (c) *c->h_nonfinite = 0;
     RunQp(c, p, cfg, n_inst, it, nullptr, out, true, f, jac, hess);
   });
 }
@@ -1383,6 +1402,7 @@ rtn_status rtn_cycle_qp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_conf
 extern "C" rtn_status rtn_solve_feedback(rtn_ctx* c, const rtn_ocp_config* cfg, long long n_inst,
                                          const rtn_qp_blocks* qp, const double* x_measured, const rtn_iterate* it,
                                          rtn_feedback* out) {
+  NvtxRange nvtx("rtn_solve_feedback");
   return Guard([&] {
     if (!cfg) throw Error(RTN_ECONFIG, "null argument");
     if (cfg->horizon < 1) throw Error(RTN_ECONFIG, "qp data: bad dimensions");

@@ -549,6 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (half == 0) {
         const int r = tid_h, n_out = prm.n_out;
         if (node < prm.K && r < kNtc2) {
+          note_nonfinite(prm, o, n_out);
           if (rank == 0 && r < kCarrier2) {
             if (hg == 0) {
               if (r == 0)
@@ -668,6 +669,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (half == 0) {
         const int r = tid_h, n_out = prm.n_out;
         if (node < prm.K && r < NTC) {
+          note_nonfinite(prm, o, n_out);
           if (rank == 0 && r < car_rows) {
             if (hg == 0) {
               if (r == 0)
@@ -814,13 +816,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const long long nbase = node0 + static_cast<long long>(rank) * P;
       if (r < P) {
         const long long node = nbase + r;
-        if (node < prm.K)
+        if (node < prm.K) {
+          note_nonfinite(prm, o, n_out);
           for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+        }
       } else if (r < rows_used && prm.jac != nullptr) {
         const int k = (r - P) / P, p = (r - P) % P;
         const long long node = nbase + p;
-        if (node < prm.K)
+        if (node < prm.K) {
+          note_nonfinite(prm, o, n_out);
           for (int oo = 0; oo < n_out; ++oo) prm.jac[(node * n_out + oo) * n_in + k] = static_cast<double>(o[oo]);
+        }
       }
     };
 

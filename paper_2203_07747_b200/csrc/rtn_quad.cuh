@@ -430,6 +430,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
       const int r = tid_h, n_out = prm.n_out;
       const long long nd = node0 + sub;
       if (nd < prm.K) {
+        note_nonfinite(prm, o, n_out);
         if (r == 0) {
           for (int oo = 0; oo < n_out; ++oo) prm.f[nd * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
         } else if (r < rows_used && prm.jac != nullptr) {

@@ -506,6 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long node = node0 + p;
         const int n_out = prm.n_out;
         if (valid && node < prm.K) {
+          note_nonfinite(prm, o, n_out);
           if (j == 0) {
             for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
           } else if (prm.jac != nullptr) {

@@ -179,6 +179,13 @@ class Engine:
         raise_for_status(st)
         return BatchEval(f, jac, hess)
 
+    def nonfinite(self, reset: bool = True) -> bool:
+        """True when the last blocking call (or the device calls since the last
+        reset) wrote a NaN/Inf output (rtn_ctx_nonfinite)."""
+        flag = C.c_int()
+        raise_for_status(_lib.lib().rtn_ctx_nonfinite(self.ctx_ptr, C.byref(flag), int(reset)))
+        return bool(flag.value)
+
     def counters(self) -> tuple[int, int, int]:
         a, b, c = C.c_ulonglong(), C.c_ulonglong(), C.c_ulonglong()
         raise_for_status(_lib.lib().rtn_ctx_counters(self.ctx_ptr, C.byref(a), C.byref(b), C.byref(c)))

@@ -181,3 +181,23 @@ def test_digest_keyed_model_cache(tmp_path, monkeypatch):
     L.rtn_model_free(d)
     f_ref, j_ref, _ = om.batched_eval(z, 1)
     assert oracle.max_node_rel_error(f3, f_ref) < 1e-3 and oracle.max_node_rel_error(j3, j_ref) < 1e-3
+
+
+def test_nonfinite_flag_per_call():
+    """SURVEY §5 failure detection: a NaN/Inf written by the output epilogue raises
+    the context's flag (rtn_ctx_nonfinite); each blocking call starts clean."""
+    om = oracle.OracleModel.random_net([17, 64, 64, 6], "tanh", 3, True)
+    good = oracle.to_product_model(om)
+    bad = oracle.to_product_model(om)
+    bad.weights[-1] = bad.weights[-1].copy()
+    bad.weights[-1][2, 5] = np.nan
+    z = oracle.quad_nodes(1, 40)
+    eb = bad.engine()
+    out = eb.prepare(z, 1)
+    assert np.isnan(out.values[:, 2]).all()
+    assert eb.nonfinite(reset=False) and eb.nonfinite(reset=True) and not eb.nonfinite()
+    eg = good.engine()
+    eg.prepare(z, 1)
+    assert not eg.nonfinite()
+    eb.prepare(z, 1)
+    assert eb.nonfinite()
