@@ -6,6 +6,7 @@
 //   1: st.shared::cluster.v4.f32 (32 lanes -> 512 contiguous bytes)
 //   2: st.shared.f32 into local staging, then one cp.async.bulk.shared::cluster.shared::cta
 //   3: st.shared.f32 local only (reference)
+//   4/5: st.async(.v4).b32 to the peer, completion counted on the peer's mbarrier
 // and report cycles per KB (max over the two CTAs, median over clusters).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o dsmem_bench dsmem_bench.cu
 #include <cstdio>
@@ -30,7 +31,7 @@ __device__ __forceinline__ void cluster_sync() {
 
 constexpr int kBytes = 36 * 1024;  // one 4-chunk group of 72 rows (the pair kernel's remote share per block)
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int mode, int reps, long long* out) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024, 1) bench(int mode, int reps, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* dst = smem;               // the peer writes here
   uint8_t* stage = smem + kBytes;    // local staging (mode 2)
@@ -46,15 +47,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int mo
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     if (mode == 0) {
-      for (int off = threadIdx.x * 4; off < kBytes; off += 256 * 4)
+      for (int off = threadIdx.x * 4; off < kBytes; off += blockDim.x * 4)
         asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rdst + off), "f"(v) : "memory");
       asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
     } else if (mode == 1) {
-      for (int off = threadIdx.x * 16; off < kBytes; off += 256 * 16)
+      for (int off = threadIdx.x * 16; off < kBytes; off += blockDim.x * 16)
         asm volatile("st.shared::cluster.v4.f32 [%0], {%1,%1,%1,%1};" ::"r"(rdst + off), "f"(v) : "memory");
       asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
     } else if (mode == 2) {
-      for (int off = threadIdx.x * 4; off < kBytes; off += 256 * 4)
+      for (int off = threadIdx.x * 4; off < kBytes; off += blockDim.x * 4)
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(stage) + off), "f"(v) : "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
@@ -74,10 +75,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int mo
             : "memory");
       }
       __syncthreads();
-    } else {
-      for (int off = threadIdx.x * 4; off < kBytes; off += 256 * 4)
+    } else if (mode == 3) {
+      for (int off = threadIdx.x * 4; off < kBytes; off += blockDim.x * 4)
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(dst) + off), "f"(v) : "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    } else {
+      // st.async: remote stores completing on the PEER's mbarrier (complete_tx)
+      const uint32_t rbar = mapa(smem_u32(bar), peer);
+      if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(kBytes)
+                     : "memory");
+      if (mode == 4) {
+        for (int off = threadIdx.x * 4; off < kBytes; off += blockDim.x * 4)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(rdst + off),
+                       "r"(__float_as_uint(v)), "r"(rbar)
+                       : "memory");
+      } else {
+        for (int off = threadIdx.x * 16; off < kBytes; off += blockDim.x * 16)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%1,%1,%1}, [%2];" ::"r"(
+                           rdst + off),
+                       "r"(__float_as_uint(v)), "r"(rbar)
+                       : "memory");
+      }
+      if (threadIdx.x == 0)
+        asm volatile(
+            "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
+                smem_u32(bar)),
+            "r"(r & 1)
+            : "memory");
+      __syncthreads();
     }
     cluster_sync();
   }
@@ -92,9 +118,10 @@ int main() {
   const int smem = 2 * kBytes + 1024;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"st.shared::cluster.f32", "st.shared::cluster.v4.f32", "local st + cp.async.bulk to peer",
-                         "st.shared.f32 local only"};
-  for (int mode = 0; mode < 4; ++mode) {
-    bench<<<2 * clusters, 256, smem>>>(mode, reps, d);
+                         "st.shared.f32 local only", "st.async.b32 (complete_tx)", "st.async.v4.b32 (complete_tx)"};
+  for (int threads : {256, 512})
+  for (int mode = 0; mode < 6; ++mode) {
+    bench<<<2 * clusters, threads, smem>>>(mode, reps, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       std::printf("mode %d: %s\n", mode, cudaGetErrorString(e));
@@ -106,8 +133,8 @@ int main() {
     for (int c = 0; c < clusters; ++c) mx[c] = std::max(h[2 * c], h[2 * c + 1]);
     std::sort(mx.begin(), mx.end());
     const double cyc = static_cast<double>(mx[clusters / 2]);
-    std::printf("%-36s %8.0f cycles per %d KB (incl. cluster barrier)  %6.1f B/clk\n", names[mode], cyc, kBytes / 1024,
-                kBytes / cyc);
+    std::printf("%4d threads %-36s %8.0f cycles per %d KB (incl. cluster barrier)  %6.1f B/clk\n", threads, names[mode], cyc,
+                kBytes / 1024, kBytes / cyc);
   }
   return 0;
 }
