@@ -63,11 +63,6 @@ cudaError_t LaunchQuadBF16(const KParams& prm, const CUtensorMap& th, const CUte
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 11;
 
-// Width-512 throughput kernel with the activations as the A operand in shared
-// memory, M = 128 pair MMAs, no DSMEM (rtn_rowsa.cuh): TF32, order <= 1,
-// 7 <= n_in <= 31, n_out <= 8, prm.P = 64 / (1 + n_in) nodes per CTA.
-cudaError_t LaunchRowsATF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
-                            cudaStream_t st);
 
 // Order 2 (value + Jacobian + Hessian), n_in <= kMaxIn2. Order2Ntc picks the
 // tile (rows per CTA side): 48 for the quadrotor's 17 inputs in TF32/bf16x3

@@ -446,18 +446,15 @@ HostModel ParseRmlp(const std::vector<char>& bytes) {
 //   rows    : TF32 width-256 throughput batches, activations as the A operand
 //             in TMEM (rtn_rows.cuh);
 //   pair    : pair-kernel throughput tiles (rtn_pair.cuh).
-enum class Kern { kPair, kLatency, kQuad, kRows, kRowsA };
+enum class Kern { kPair, kLatency, kQuad, kRows };
 Kern Choose(const rtn_model* m, long long K, int num_sms) {
   const bool lat_ok = m->n_in + 1 <= 24;
   const bool quad_ok = lat_ok && m->pair_wp == 512 && m->n_in <= rtn::kMaxIn0 && K <= 2 * (num_sms / 4);
   const bool rows_ok = m->pair_mode == rtn::kTF32 && m->pair_wp == 256 && m->n_in >= rtn::kRowsMinIn &&
                        m->n_in <= rtn::kRowsMaxInHost && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
-  const bool rowsa_ok = m->pair_mode == rtn::kTF32 && m->pair_wp == 512 && m->n_in >= rtn::kRowsMinIn &&
-                        m->n_in <= rtn::kRowsMaxInHost && m->n_out <= 8;
   if (const char* e = std::getenv("RTN_KERNEL")) {
     if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
     if (std::strcmp(e, "rows") == 0 && rows_ok) return Kern::kRows;
-    if (std::strcmp(e, "rowsa") == 0 && rowsa_ok) return Kern::kRowsA;
     if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
     if (std::strcmp(e, "pair") == 0) return Kern::kPair;
     // a kernel that does not apply to this model: the default choice below
@@ -530,17 +527,6 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
         : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
                                        : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
-    c->launches += 1;
-    return;
-  }
-  if (kern == Kern::kRowsA) {
-    // width 512: activations as the A operand in shared memory, 64 rows per CTA (rtn_rowsa.cuh)
-    prm.P = 64 / (1 + m->n_in);
-    prm.nt = 64;
-    prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);
-    const int g = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
-    e = rtn::LaunchRowsATF32(prm, m->tmap_h, m->tmap_l, g, c->stream);
-    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("rowsa kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }

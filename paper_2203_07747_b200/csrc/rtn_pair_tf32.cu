@@ -3,7 +3,6 @@
 #include "rtn_pair_launch.cuh"
 #include "rtn_quad.cuh"
 #include "rtn_rows.cuh"
-#include "rtn_rowsa.cuh"
 
 namespace rtn {
 
@@ -38,16 +37,6 @@ cudaError_t LaunchQuadTF32(const KParams& prm, const CUtensorMap& th, const CUte
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st) {
   using Cfg = RowsCfg<6>;
   auto kern = prm.act == 0 ? rtn_rows_kernel<6, 0> : (prm.act == 1 ? rtn_rows_kernel<6, 1> : rtn_rows_kernel<6, 2>);
-  const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
-  return cudaGetLastError();
-}
-
-cudaError_t LaunchRowsATF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid,
-                            cudaStream_t st) {
-  using Cfg = RowsACfg<4>;
-  auto kern = prm.act == 0 ? rtn_rowsa_kernel<4, 0> : (prm.act == 1 ? rtn_rowsa_kernel<4, 1> : rtn_rowsa_kernel<4, 2>);
   const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(prm, th, tl);
