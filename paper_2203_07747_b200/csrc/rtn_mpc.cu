@@ -507,6 +507,10 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     // pair tiles of the node's carrier (value + tangents) plus Hessian slots
     prm.P = 1;
     prm.nt = rtn::Order2Ntc(m->pair_mode, m->n_in);
+    if (const char* o2 = std::getenv("RTN_ORD2_NTC")) {  // A/B aid: the generic tiles' heights
+      const int v = std::atoi(o2);
+      if ((v == 24 || v == 40) && 1 + m->n_in <= v) prm.nt = v;
+    }
     prm.ord2_g = rtn::ord2_tiles(m->n_in, prm.nt);
     prm.hess = d_hess;
     prm.num_tiles = static_cast<long long>(prm.ord2_g) * K;

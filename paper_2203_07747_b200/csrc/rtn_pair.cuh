@@ -493,6 +493,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t tb = tmem_base + lane_base + mb * C::kBlkCols;
       mbar_wait_sleep(&tmem_full[mb], hl & 1);
       tc_fence_after();
+      const bool tr = trace_on();
+      unsigned long long* tp = tr ? prm.trace + 48 + rank * 66 + (l * 2 + mb) * 3 : nullptr;
+      if (tr) tp[0] = globaltimer();
       float v[kNtc2], car[24];
       tmem_read_acc<C, kNtc2>(tb + half * kNtc2, v, kNtc2, C::kN, C::kCorrOff);
       tmem_read_acc<C, 24>(tb, car, 24, C::kN, C::kCorrOff);
@@ -501,7 +504,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       act_fwd2(act, car[0] + bj, val, sp, spp);
       epi_rows(v, car + 1, val, sp, spp, hg);
       mbar_wait_sleep(&in_free[grp], hl & 1);
+      if (tr) tp[1] = globaltimer();
       store_publish([&](int i) { return v[i]; }, j, grp);
+      if (tr) tp[2] = globaltimer();
     };
 
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {

@@ -1,7 +1,7 @@
 """Event timeline of one tile of CTA pair 0 in the throughput kernel (RTN_TRACE
 = 1 + tile index): per (layer, block) the MMA warp's issue window and each
 CTA's epilogue (accumulator seen, input group free, published).
-Usage: RTN_TRACE=3 [RTN_DEBUG=n] python scripts/trace_tput.py [K]"""
+Usage: RTN_TRACE=3 [RTN_DEBUG=n] [ORDER=2] python scripts/trace_tput.py [K]"""
 import ctypes as C
 import os
 import sys
@@ -16,8 +16,9 @@ sizes = [17] + [512] * 12 + [6]
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 409600
 m = make_mlp(sizes, "silu", "full", 12512)
 z = synth_quad_nodes(7, k)
+order = EvalOrder.HESSIAN if os.environ.get("ORDER") == "2" else EvalOrder.JACOBIAN
 for _ in range(3):
-    mlp_batched_eval(m, z, EvalOrder.JACOBIAN)
+    mlp_batched_eval(m, z, order)
 buf = (C.c_ulonglong * 256)()
 _lib.lib().rtn_debug_trace(buf, 256)
 t = np.array(buf, dtype=np.float64)
