@@ -408,6 +408,41 @@ def _quad_iterate(np, n_inst, n, seed):
     return xs, us, xs + rng.normal(0, 0.1, xs.shape), us + rng.normal(0, 0.1, us.shape)
 
 
+def cycle_latency(torch, order, steps=None):
+    """Fused phase 1+2 latency at cfg3 (12x512, N=20, one instance), host -> host
+    through the C-ABI (rtn_cycle_qp, structs built once like a controller would)."""
+    import numpy as np
+    from paper_2203_07747_b200 import _lib, make_mlp, qp
+    from paper_2203_07747_b200.errors import raise_for_status
+    L = _lib.lib()
+    p = qp.QuadParams()
+    big = make_mlp(SIZES, "silu", "full", SEED)
+    b = qp.QpBuilder(big, latency_mode=1)
+    b.engine._ensure(20, order)
+    cfg3 = qp.OcpConfig(horizon=20, dt=0.02, q_diag=np.ones(13), r_diag=np.full(4, 0.1), taylor_order=order)
+    x3, u3, rx3, ru3 = (np.ascontiguousarray(a[0]) for a in _quad_iterate(np, 1, 20, 3))
+    outs = {nm: np.empty(sh) for nm, sh in {"a": (20, 13, 13), "b": (20, 13, 4), "phi_res": (20, 13),
+                                             "q": (21, 13), "r": (20, 4), "hx_diag": (21, 13), "hu_diag": (20, 4),
+                                             "du_lb": (20, 4), "du_ub": (20, 4)}.items()}
+    it3 = _lib.IterateC(x3.ctypes.data, u3.ctypes.data, rx3.ctypes.data, ru3.ctypes.data)
+    oc3 = _lib.QpBlocksC(*[outs[nm].ctypes.data for nm in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag",
+                                                            "du_lb", "du_ub")])
+    pc3, cc3 = p.to_c(), cfg3.to_c()
+    args = (b.engine.ctx_ptr, C.byref(pc3), C.byref(cc3), 1, C.byref(it3), C.byref(oc3), None, None, None)
+    for _ in range(50):
+        raise_for_status(L.rtn_cycle_qp(*args))
+    ts = []
+    for _ in range(steps or (300 if order == 2 else 1000)):
+        t0 = time.perf_counter()
+        L.rtn_cycle_qp(*args)
+        ts.append((time.perf_counter() - t0) * 1e6)
+    ts.sort()
+    big.invalidate()
+    return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)], "steps": len(ts),
+            "path": "rtn_cycle_qp (C-ABI): H2D iterate -> [x;u] features -> MLP (f,A,B" + (",H" if order == 2 else "") +
+                    ") -> RK4 blocks -> D2H QpData, one CUDA graph"}
+
+
 def blocks_bench(torch, hbm_peak, steps=5):
     """§8f rank 1: the continuity-block builder (csrc/rtn_blocks.cu) on the
     cfg5 shape (65,536 instances x N=50), fp64. Device-resident throughput
@@ -478,35 +513,7 @@ def blocks_bench(torch, hbm_peak, steps=5):
     eng.close()
     # fused phase 1+2 latency at cfg3 (12x512, N=20, one instance), host -> host through the
     # C-ABI (rtn_cycle_qp, structs built once like a controller would), and device-only
-    lat = {}
-    big = make_mlp(SIZES, "silu", "full", SEED)
-    for order in (1, 2):
-        b = qp.QpBuilder(big, latency_mode=1)
-        b.engine._ensure(20, order)
-        cfg3 = qp.OcpConfig(horizon=20, dt=0.02, q_diag=np.ones(13), r_diag=np.full(4, 0.1), taylor_order=order)
-        x3, u3, rx3, ru3 = (np.ascontiguousarray(a[0]) for a in _quad_iterate(np, 1, 20, 3))
-        outs = {nm: np.empty(sh) for nm, sh in {"a": (20, 13, 13), "b": (20, 13, 4), "phi_res": (20, 13),
-                                                 "q": (21, 13), "r": (20, 4), "hx_diag": (21, 13), "hu_diag": (20, 4),
-                                                 "du_lb": (20, 4), "du_ub": (20, 4)}.items()}
-        it3 = _lib.IterateC(x3.ctypes.data, u3.ctypes.data, rx3.ctypes.data, ru3.ctypes.data)
-        oc3 = _lib.QpBlocksC(*[outs[nm].ctypes.data for nm in ("a", "b", "phi_res", "q", "r", "hx_diag", "hu_diag",
-                                                                "du_lb", "du_ub")])
-        pc3, cc3 = p.to_c(), cfg3.to_c()
-        args = (b.engine.ctx_ptr, C.byref(pc3), C.byref(cc3), 1, C.byref(it3), C.byref(oc3), None, None, None)
-        for _ in range(50):
-            raise_for_status(L.rtn_cycle_qp(*args))
-        ts = []
-        for _ in range(300 if order == 2 else 1000):
-            t0 = time.perf_counter()
-            L.rtn_cycle_qp(*args)
-            ts.append((time.perf_counter() - t0) * 1e6)
-        ts.sort()
-        lat[f"cfg3_cycle_order{order}"] = {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)],
-                                           "steps": len(ts),
-                                           "path": "rtn_cycle_qp (C-ABI): H2D iterate -> [x;u] features -> MLP (f,A,B" +
-                                                   (",H" if order == 2 else "") + ") -> RK4 blocks -> D2H QpData, "
-                                                   "one CUDA graph"}
-    big.invalidate()
+    lat = {f"cfg3_cycle_order{order}": cycle_latency(torch, order) for order in (1, 2)}
     # CPU baseline: the oracle's serial BuildQp (like the reference's per-instance loop)
     ns = 64
     t0 = time.perf_counter()

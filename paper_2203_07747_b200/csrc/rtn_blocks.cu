@@ -15,8 +15,10 @@
 // coalesced stores. Roofline: HBM — ≈3.5 KB of fp64 in + out per node at
 // order 1; the fp64 arithmetic is ~8 kFLOP per node.
 #include <cmath>
+#include <cstdlib>
 
 #include "rtn_blocks.h"
+#include "rtn_launch.h"
 
 namespace rtn {
 namespace {
@@ -26,6 +28,7 @@ constexpr int kDkStride = 18;      // dk row stride (doubles): 16-byte aligned p
 constexpr int kDk = kQNx * kDkStride;
 
 constexpr int kMaxNf = 26;
+constexpr long long kLatencyMaxNodes = 4096;  // batches up to this size take the HS variant
 
 // Per-node scratch, ≡ 64 (mod 128) bytes: the two nodes of a warp sit in
 // disjoint banks, so their broadcast loads do not conflict.
@@ -223,10 +226,17 @@ __device__ __forceinline__ double NominalRowAndJacobian(int i, const double* X, 
   return f;
 }
 
-template <int ORDER, int VAR>
-__global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams p) {
-  constexpr int NF = VarNf(VAR), NR = VarNr(VAR);
+// HS (latency-sized batches): one CTA per SM, so no register cap (the 4-CTA
+// variant spills 56-184 bytes per thread at 128 registers), and at order 2 the
+// node's Hessian rows are copied into shared memory once (cp.async, all issued
+// up front) instead of being re-read from L2 at every RK4 stage in 7 dependent
+// rounds per lane. Costs 8·n_r·n_f² doubles of dynamic shared memory per CTA
+// (111-130 KB), so large batches keep the L2 variant and its 4 CTAs per SM.
+template <int ORDER, int VAR, bool HS>
+__global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const BlkParams p) {
+  constexpr int NF = VarNf(VAR), NR = VarNr(VAR), NH = NR * NF * NF;
   __shared__ __align__(128) NodeSmem smem[kWarps * 2];
+  extern __shared__ __align__(16) double hsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, r = lane & 15;
   const unsigned half_mask = half ? 0xffff0000u : 0x0000ffffu;
@@ -246,12 +256,30 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
   if (row) S.x[r] = p.xs[xrow * kQNx + r];
   if (r < kQNu) S.u[r] = p.us[node * kQNu + r];
   if (VAR == kVarGround && r < 9) S.aux[r] = p.aux[node * 9 + r];
+  // Programmatic dependent launch (fused cycle): everything above reads only
+  // the caller's iterate; the MLP kernel's outputs (and a feature kernel's z0)
+  // are read after its grid has completed. A no-op without the launch attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const double* hn = ORDER == 2 ? p.hess + node * NH : nullptr;
+  if (ORDER == 2 && HS) {
+    double* hs = hsm + (warp * 2 + half) * NH;
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(hs));
+    for (int i = r; i < NH; i += 16)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * i), "l"(hn + i) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    hn = hs;
+  }
   __syncwarp();
   for (int c = r; c < NF; c += 16) S.z0[c] = p.z0 ? p.z0[node * NF + c] : Feature<VAR>(c, S.x, S.u, S.aux);
   // Taylor rows: lane 7+o evaluates residual row o (TaylorApprox, taylor.hpp:13-24)
   const int o = res_row ? r - 7 : 0;
   const double* jrow_g = p.jac + (node * NR + o) * NF;
   const double fbo = res_row ? p.fbar[node * NR + o] : 0.0;
+  double jn0[NF];  // HS: this lane's Jacobian row, loaded once instead of at every stage
+  if (HS) {
+#pragma unroll
+    for (int c = 0; c < NF; ++c) jn0[c] = res_row ? __ldg(jrow_g + c) : 0.0;
+  }
   // body wrench = mix · u (MixThrustTorque, dynamics.cpp:57-62)
   double tb[3], tau[3];
 #pragma unroll
@@ -274,13 +302,24 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
     for (int c = r; c < NF; c += 16) S.dz[c] = Feature<VAR>(c, S.xs, S.u, S.aux) - S.z0[c];
     __syncwarp();
     if (ORDER == 2) {  // G[o][a] = Σ_b H_o(a,b)·dz_b, n_r·n_f rows spread over the half-warp
-      const double* hn = p.hess + node * (NR * NF * NF);
-      for (int e = r; e < NR * NF; e += 16) {
+      if (HS && s == 0) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+      }
+      auto g_row = [&](int e) {
         const double* h = hn + e * NF;
         double g = 0.0;
 #pragma unroll
-        for (int b = 0; b < NF; ++b) g += __ldg(h + b) * S.dz[b];
+        for (int b = 0; b < NF; ++b) g += (HS ? h[b] : __ldg(h + b)) * S.dz[b];
         S.g[e] = g;
+      };
+      if constexpr (HS) {  // shared-memory rows, unrolled: the lane's FMA chains interleave
+        constexpr int kRowsPerLane = (NR * NF + 15) / 16;
+#pragma unroll
+        for (int i = 0; i < kRowsPerLane; ++i)
+          if (r + 16 * i < NR * NF) g_row(r + 16 * i);
+      } else {
+        for (int e = r; e < NR * NF; e += 16) g_row(e);
       }
       __syncwarp();
     }
@@ -290,7 +329,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) QpBlocksKernel(const BlkParams
     {
       double jn[NF], jc[kQNf];
 #pragma unroll
-      for (int c = 0; c < NF; ++c) jn[c] = res_row ? __ldg(jrow_g + c) : 0.0;
+      for (int c = 0; c < NF; ++c) jn[c] = HS ? jn0[c] : (res_row ? __ldg(jrow_g + c) : 0.0);
       if (res_row) {  // EvalTaylor row o: f_bar + jac·dz (+ ½ dzᵀ H_o dz) (taylor.cpp:57-64)
         double a1 = 0.0;
 #pragma unroll
@@ -428,25 +467,46 @@ cudaError_t LaunchFeatures(int variant, const double* xs, const double* us, cons
   return cudaGetLastError();
 }
 
-cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s) {
+template <int ORDER, int VAR, bool HS>
+static cudaError_t LaunchBlk(const BlkParams& p, unsigned g, cudaStream_t s, bool pdl) {
+  const int dyn = HS && ORDER == 2 ? 2 * kWarps * VarNr(VAR) * VarNf(VAR) * VarNf(VAR) * static_cast<int>(sizeof(double)) : 0;
+  if (dyn > 0) {
+    const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(QpBlocksKernel<ORDER, VAR, HS>), dyn);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(kWarps * 32);
+  cfg.dynamicSmemBytes = static_cast<size_t>(dyn);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, QpBlocksKernel<ORDER, VAR, HS>, p);
+}
+
+cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s, bool pdl) {
   const long long K = p.n_inst * p.N;
   if (K <= 0) return cudaSuccess;
   const long long per_cta = 2 * kWarps;
   const long long grid = (K + per_cta - 1) / per_cta;
   const unsigned g = static_cast<unsigned>(grid);
-#define RTN_BLK_LAUNCH(O, V) QpBlocksKernel<O, V><<<g, kWarps * 32, 0, s>>>(p)
+  const char* e = std::getenv("RTN_BLK_HS");  // A/B aid: 0 forces the 4-CTA variant
+  const bool hs = K <= kLatencyMaxNodes && !(e && e[0] == '0');  // latency-sized batches
+#define RTN_BLK(O, V) return hs ? LaunchBlk<O, V, true>(p, g, s, pdl) : LaunchBlk<O, V, false>(p, g, s, pdl)
   switch (p.variant * 2 + (p.order == 2 ? 1 : 0)) {
-    case kVarFull * 2: RTN_BLK_LAUNCH(1, kVarFull); break;
-    case kVarFull * 2 + 1: RTN_BLK_LAUNCH(2, kVarFull); break;
-    case kVarA * 2: RTN_BLK_LAUNCH(1, kVarA); break;
-    case kVarA * 2 + 1: RTN_BLK_LAUNCH(2, kVarA); break;
-    case kVarAU * 2: RTN_BLK_LAUNCH(1, kVarAU); break;
-    case kVarAU * 2 + 1: RTN_BLK_LAUNCH(2, kVarAU); break;
-    case kVarGround * 2: RTN_BLK_LAUNCH(1, kVarGround); break;
-    default: RTN_BLK_LAUNCH(2, kVarGround); break;
+    case kVarFull * 2: RTN_BLK(1, kVarFull);
+    case kVarFull * 2 + 1: RTN_BLK(2, kVarFull);
+    case kVarA * 2: RTN_BLK(1, kVarA);
+    case kVarA * 2 + 1: RTN_BLK(2, kVarA);
+    case kVarAU * 2: RTN_BLK(1, kVarAU);
+    case kVarAU * 2 + 1: RTN_BLK(2, kVarAU);
+    case kVarGround * 2: RTN_BLK(1, kVarGround);
+    default: RTN_BLK(2, kVarGround);
   }
-#undef RTN_BLK_LAUNCH
-  return cudaGetLastError();
+#undef RTN_BLK
 }
 
 }  // namespace rtn

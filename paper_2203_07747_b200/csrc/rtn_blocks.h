@@ -46,7 +46,9 @@ struct BlkParams {
   double qd[13], rd[4], qf[13], umin[4], umax[4];
 };
 
-cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s);
+// pdl: launch as a programmatic dependent of the preceding kernel on `s` (the
+// fused cycle's MLP kernel): the prologue overlaps that kernel's tail.
+cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s, bool pdl = false);
 // z_k = features(x_k, u_k, aux_k) (K x n_f) for the non-'full' variants of the fused cycle.
 cudaError_t LaunchFeatures(int variant, const double* xs, const double* us, const double* aux, long long n_inst,
                            int N, double* z, cudaStream_t s);

@@ -130,6 +130,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Lets a programmatic dependent launch (the fused cycle's blocks kernel) be
+// scheduled now; it still waits for this grid's completion before reading its
+// outputs (griddepcontrol.wait). A no-op when nothing was launched that way.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

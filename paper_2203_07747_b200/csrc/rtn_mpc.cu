@@ -107,6 +107,16 @@ bool ZeroCopy() {
   return on;
 }
 
+// Fused cycle: the blocks kernel is a programmatic dependent of the MLP kernel
+// (launch + prologue overlap its tail; RTN_PDL=0 disables).
+bool PdlEnabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Hidden widths are zero-padded to the kernels' 256- or 512-neuron layouts
 // (any width in (256, 512] pads to 512; > 512 is rejected by the caller).
 int PaddedWidth(const std::vector<int>& sizes) {
@@ -1183,7 +1193,7 @@ void RunQp(rtn_ctx* c, const rtn_quad_params* p, const rtn_ocp_config* cfg, long
       c->launches += 1;
       Enqueue(c, c->d_z, K, order, c->d_f, c->d_jac, order == 2 ? c->d_hess : nullptr);
     }
-    CUDA_CHECK(rtn::LaunchQpBlocks(b, s));
+    CUDA_CHECK(rtn::LaunchQpBlocks(b, s, cycle && PdlEnabled()));
     c->launches += 1;
   };
   const unsigned mask = (out->a ? 1u : 0) | (out->b ? 2u : 0) | (out->phi_res ? 4u : 0) | (out->q ? 8u : 0) |

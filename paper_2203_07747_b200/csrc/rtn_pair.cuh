@@ -199,6 +199,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_l);
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  pdl_launch_dependents();
   if constexpr (ORD2 == 2) {  // slot → (a, b) table of the packed upper triangle
     uint16_t* ab = reinterpret_cast<uint16_t*>(smem + C::kAbOff);
     const int np = n_in * (n_in + 1) / 2;

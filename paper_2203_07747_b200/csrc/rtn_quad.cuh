@@ -209,6 +209,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_l);
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 256);
+  pdl_launch_dependents();
   tc_fence_before();
   cluster_sync();
   tc_fence_after();

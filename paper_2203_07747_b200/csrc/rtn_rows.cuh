@@ -183,6 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_l);
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  pdl_launch_dependents();
   // layer-0 weights (normalisation folded) stay in shared memory for the whole kernel
   for (int i = threadIdx.x; i < 256 * n_in; i += blockDim.x) w0s[i] = __ldg(prm.w0 + i);
   for (int i = threadIdx.x; i < 256 * n_mma; i += blockDim.x) bhs[i] = __ldg(prm.bh + i);
