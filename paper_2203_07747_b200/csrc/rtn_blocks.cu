@@ -226,12 +226,15 @@ __device__ __forceinline__ double NominalRowAndJacobian(int i, const double* X, 
   return f;
 }
 
-// HS (latency-sized batches): one CTA per SM, so no register cap (the 4-CTA
-// variant spills 56-184 bytes per thread at 128 registers), and at order 2 the
-// node's Hessian rows are copied into shared memory once (cp.async, all issued
-// up front) instead of being re-read from L2 at every RK4 stage in 7 dependent
-// rounds per lane. Costs 8·n_r·n_f² doubles of dynamic shared memory per CTA
-// (111-130 KB), so large batches keep the L2 variant and its 4 CTAs per SM.
+// HS (latency-sized batches): the kernel is a chain of dependent fp64 steps
+// (~6,000 warp-instructions per node at order 2, ~9 cycles each), so a node
+// gets a whole warp: both halves run the same rows, half h computes the
+// sensitivity columns [8h, 8h + 10) (selects, no divergence), and the order-2
+// H·dz rows and the feature/Hessian loads spread over 32 lanes. One CTA per SM
+// (no register cap; the 4-CTA variant spills 56-184 bytes per thread at 128
+// registers), and at order 2 the node's Hessian rows are copied into shared
+// memory once (cp.async, all issued up front) instead of being re-read from L2
+// at every RK4 stage. Large batches keep the half-warp L2 variant, 4 CTAs per SM.
 template <int ORDER, int VAR, bool HS>
 __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const BlkParams p) {
   constexpr int NF = VarNf(VAR), NR = VarNr(VAR), NH = NR * NF * NF;
@@ -241,11 +244,16 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
   const int half = lane >> 4, r = lane & 15;
   const unsigned half_mask = half ? 0xffff0000u : 0x0000ffffu;
   const long long K = p.n_inst * p.N;
-  const long long raw = (static_cast<long long>(blockIdx.x) * kWarps + warp) * 2 + half;
-  if ((raw & ~1ll) >= K) return;     // both halves past the end: the whole warp leaves
-  const bool valid = raw < K;        // a past-the-end half shadows its partner's node
+  constexpr int kStep = HS ? 32 : 16;  // lanes per node
+  const int nl = HS ? lane : r;         // lane index inside the node's lanes
+  const int slot = HS ? warp : warp * 2 + half;
+  const long long raw = HS ? static_cast<long long>(blockIdx.x) * kWarps + warp
+                           : (static_cast<long long>(blockIdx.x) * kWarps + warp) * 2 + half;
+  if ((HS ? raw : (raw & ~1ll)) >= K) return;  // the whole warp is past the end
+  const bool valid = raw < K;                  // a past-the-end half shadows its partner's node
   const long long node = valid ? raw : raw - 1;
-  NodeSmem& S = smem[warp * 2 + half];
+  const bool writer = !HS || half == 0;        // HS: half 0 stores the row outputs
+  NodeSmem& S = smem[slot];
   const long long inst = node / p.N;
   const int n = static_cast<int>(node - inst * p.N);
   const long long xrow = inst * (p.N + 1) + n;
@@ -256,21 +264,30 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
   if (row) S.x[r] = p.xs[xrow * kQNx + r];
   if (r < kQNu) S.u[r] = p.us[node * kQNu + r];
   if (VAR == kVarGround && r < 9) S.aux[r] = p.aux[node * 9 + r];
+  // the tail's inputs from the iterate, loaded up front (host-mapped in latency
+  // mode: each is a PCIe round trip that would otherwise follow the RK4 stages)
+  double xn = 0.0, rx = 0.0, rxn = 0.0, ru = 0.0;
+  if (row) {
+    xn = p.xs[(xrow + 1) * kQNx + r];
+    if (p.q) rx = p.rxs[xrow * kQNx + r];
+    if (p.q && n == p.N - 1) rxn = p.rxs[(xrow + 1) * kQNx + r];
+  }
+  if (r < kQNu && p.r) ru = p.rus[node * kQNu + r];
   // Programmatic dependent launch (fused cycle): everything above reads only
   // the caller's iterate; the MLP kernel's outputs (and a feature kernel's z0)
   // are read after its grid has completed. A no-op without the launch attribute.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const double* hn = ORDER == 2 ? p.hess + node * NH : nullptr;
   if (ORDER == 2 && HS) {
-    double* hs = hsm + (warp * 2 + half) * NH;
+    double* hs = hsm + slot * NH;
     const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(hs));
-    for (int i = r; i < NH; i += 16)
+    for (int i = nl; i < NH; i += kStep)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * i), "l"(hn + i) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
     hn = hs;
   }
   __syncwarp();
-  for (int c = r; c < NF; c += 16) S.z0[c] = p.z0 ? p.z0[node * NF + c] : Feature<VAR>(c, S.x, S.u, S.aux);
+  for (int c = nl; c < NF; c += kStep) S.z0[c] = p.z0 ? p.z0[node * NF + c] : Feature<VAR>(c, S.x, S.u, S.aux);
   // Taylor rows: lane 7+o evaluates residual row o (TaylorApprox, taylor.hpp:13-24)
   const int o = res_row ? r - 7 : 0;
   const double* jrow_g = p.jac + (node * NR + o) * NF;
@@ -291,7 +308,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
   }
 
   int failed = 0;
-  double acc[kQNf];
+  // sensitivity columns of this lane: all kQNf (+1 pad), or (HS) 10 from jo
+  constexpr int kJ = HS ? 10 : kQNf + 1;
+  const int jo = HS ? 8 * half : 0;
+  double acc[kJ];
 #pragma unroll 1
   for (int s = 0; s < 4; ++s) {
     const double cs = s == 0 ? 0.0 : (s == 3 ? dt : 0.5 * dt);
@@ -299,7 +319,7 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
     if (row) S.xs[r] = s == 0 ? S.x[r] : S.x[r] + cs * S.k[s - 1][r];
     __syncwarp();
     // dz = features(x_s, u, aux) − z0 (the EvalTaylor argument, sqp_rti.cpp:96-99)
-    for (int c = r; c < NF; c += 16) S.dz[c] = Feature<VAR>(c, S.xs, S.u, S.aux) - S.z0[c];
+    for (int c = nl; c < NF; c += kStep) S.dz[c] = Feature<VAR>(c, S.xs, S.u, S.aux) - S.z0[c];
     __syncwarp();
     if (ORDER == 2) {  // G[o][a] = Σ_b H_o(a,b)·dz_b, n_r·n_f rows spread over the half-warp
       if (HS && s == 0) {
@@ -314,10 +334,10 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
         S.g[e] = g;
       };
       if constexpr (HS) {  // shared-memory rows, unrolled: the lane's FMA chains interleave
-        constexpr int kRowsPerLane = (NR * NF + 15) / 16;
+        constexpr int kRowsPerLane = (NR * NF + 31) / 32;
 #pragma unroll
         for (int i = 0; i < kRowsPerLane; ++i)
-          if (r + 16 * i < NR * NF) g_row(r + 16 * i);
+          if (lane + 32 * i < NR * NF) g_row(lane + 32 * i);
       } else {
         for (int e = r; e < NR * NF; e += 16) g_row(e);
       }
@@ -359,19 +379,17 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
     if (!failed && nonfinite) failed = 20 + s + 1;  // CheckFinite (integrator.cpp:12-15)
 
     // row r of dk_s: x columns jx[j] + Σ_m (c·jx[m]) dk[m][j]; u columns ju[j] + Σ_m (c·jx[m]) dk[m][j]
-    double nd[kQNf + 1];
+    auto jcol = [&](int c) { return c < kQNx ? fx[c] : (c < kQNf ? fu[c - kQNx] : 0.0); };  // c compile-time
+    double nd[kJ];
 #pragma unroll
-    for (int j = 0; j < kQNx; ++j) nd[j] = fx[j];
-#pragma unroll
-    for (int j = 0; j < kQNu; ++j) nd[kQNx + j] = fu[j];
-    nd[kQNf] = 0.0;
+    for (int j = 0; j < kJ; ++j) nd[j] = HS ? (half ? jcol(8 + j) : jcol(j)) : jcol(j);
     if (s > 0) {
-      const double* dkp = S.dk[(s - 1) & 1];
+      const double* dkp = S.dk[(s - 1) & 1] + jo;
 #pragma unroll
       for (int m = 0; m < kQNx; ++m) {
         const double a = cs * fx[m];
 #pragma unroll
-        for (int j = 0; j < kQNf + 1; j += 2) {
+        for (int j = 0; j < kJ; j += 2) {
           const double2 v = *reinterpret_cast<const double2*>(dkp + m * kDkStride + j);
           nd[j] += a * v.x;
           nd[j + 1] += a * v.y;
@@ -381,16 +399,16 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
     // dk1 + 2·dk2 + 2·dk3 + dk4, left to right (integrator.cpp:84-88)
     const double wgt = s == 3 ? 1.0 : 2.0;
 #pragma unroll
-    for (int j = 0; j < kQNf; ++j) acc[j] = s == 0 ? nd[j] : acc[j] + wgt * nd[j];
-    if (s < 3 && row) {
-      double* dkn = S.dk[s & 1] + r * kDkStride;
+    for (int j = 0; j < kJ; ++j) acc[j] = s == 0 ? nd[j] : acc[j] + wgt * nd[j];
+    if (s < 3 && row) {  // (HS: columns 8, 9 are written by both halves, with the same bits)
+      double* dkn = S.dk[s & 1] + r * kDkStride + jo;
 #pragma unroll
-      for (int j = 0; j < kQNf + 1; j += 2) *reinterpret_cast<double2*>(dkn + j) = make_double2(nd[j], nd[j + 1]);
+      for (int j = 0; j < kJ; j += 2) *reinterpret_cast<double2*>(dkn + j) = make_double2(nd[j], nd[j + 1]);
     }
     __syncwarp();
   }
   if (failed) {
-    if (valid && r == 0) {
+    if (valid && r == 0 && writer) {
       if (p.first_bad) Report(p.first_bad, node, failed);
       if (p.status) p.status[node] = static_cast<unsigned char>(failed);
     }
@@ -402,36 +420,37 @@ __global__ void __launch_bounds__(kWarps * 32, HS ? 1 : 4) QpBlocksKernel(const 
   double* stage = S.dk[1];
   if (row) {
 #pragma unroll
-    for (int j = 0; j < kQNx; ++j) stage[r * kQNx + j] = (r == j ? 1.0 : 0.0) + h6 * acc[j];
-#pragma unroll
-    for (int j = 0; j < kQNu; ++j) stage[kQNx * kQNx + r * kQNu + j] = h6 * acc[kQNx + j];
+    for (int j = 0; j < kJ; ++j) {
+      const int c = jo + j;
+      if (c < kQNx) stage[r * kQNx + c] = (r == c ? 1.0 : 0.0) + h6 * acc[j];
+      else if (c < kQNf) stage[kQNx * kQNx + r * kQNu + (c - kQNx)] = h6 * acc[j];
+    }
     // φ̄ = x + dt/6 (k1 + 2k2 + 2k3 + k4) (integrator.cpp:84-86)
     S.phi[r] = S.x[r] + h6 * (S.k[0][r] + 2.0 * S.k[1][r] + 2.0 * S.k[2][r] + S.k[3][r]);
   }
-  __syncwarp(half_mask);
+  __syncwarp(HS ? 0xffffffffu : half_mask);
   if (!valid) return;
-  if (p.status && r == 0) p.status[node] = 0;
+  if (p.status && r == 0 && writer) p.status[node] = 0;
   if (p.a)
-    for (int e = r; e < kQNx * kQNx; e += 16) p.a[node * (kQNx * kQNx) + e] = stage[e];
+    for (int e = nl; e < kQNx * kQNx; e += kStep) p.a[node * (kQNx * kQNx) + e] = stage[e];
   if (p.b)
-    for (int e = r; e < kQNx * kQNu; e += 16) p.b[node * (kQNx * kQNu) + e] = stage[kQNx * kQNx + e];
-  if (row) {
+    for (int e = nl; e < kQNx * kQNu; e += kStep) p.b[node * (kQNx * kQNu) + e] = stage[kQNx * kQNx + e];
+  if (row && writer) {
     double v = S.phi[r];
     if (r >= 3 && r < 7)  // quaternion renormalised (RenormalizeQuat, integrator.cpp:17-20)
       v /= sqrt(S.phi[3] * S.phi[3] + S.phi[4] * S.phi[4] + S.phi[5] * S.phi[5] + S.phi[6] * S.phi[6]);
-    const double xn = p.xs[(xrow + 1) * kQNx + r];
     if (p.phi) p.phi[node * kQNx + r] = v - xn;  // phi_res = φ̄ − x_{k+1} (sqp_rti.cpp:141)
     // cost terms (sqp_rti.cpp:143-148) and the terminal ones (:150-153)
-    if (p.q) p.q[xrow * kQNx + r] = 2.0 * (p.qd[r] * (S.x[r] - p.rxs[xrow * kQNx + r]));
+    if (p.q) p.q[xrow * kQNx + r] = 2.0 * (p.qd[r] * (S.x[r] - rx));
     if (p.hx) p.hx[xrow * kQNx + r] = 2.0 * p.qd[r];
     if (n == p.N - 1) {
-      if (p.q) p.q[(xrow + 1) * kQNx + r] = 2.0 * (p.qf[r] * (xn - p.rxs[(xrow + 1) * kQNx + r]));
+      if (p.q) p.q[(xrow + 1) * kQNx + r] = 2.0 * (p.qf[r] * (xn - rxn));
       if (p.hx) p.hx[(xrow + 1) * kQNx + r] = 2.0 * p.qf[r];
     }
   }
-  if (r < kQNu) {
+  if (r < kQNu && writer) {
     const double u = S.u[r];
-    if (p.r) p.r[node * kQNu + r] = 2.0 * (p.rd[r] * (u - p.rus[node * kQNu + r]));
+    if (p.r) p.r[node * kQNu + r] = 2.0 * (p.rd[r] * (u - ru));
     if (p.hu) p.hu[node * kQNu + r] = 2.0 * p.rd[r];
     if (p.lb) p.lb[node * kQNu + r] = p.umin[r] - u;
     if (p.ub) p.ub[node * kQNu + r] = p.umax[r] - u;
@@ -469,7 +488,7 @@ cudaError_t LaunchFeatures(int variant, const double* xs, const double* us, cons
 
 template <int ORDER, int VAR, bool HS>
 static cudaError_t LaunchBlk(const BlkParams& p, unsigned g, cudaStream_t s, bool pdl) {
-  const int dyn = HS && ORDER == 2 ? 2 * kWarps * VarNr(VAR) * VarNf(VAR) * VarNf(VAR) * static_cast<int>(sizeof(double)) : 0;
+  const int dyn = HS && ORDER == 2 ? kWarps * VarNr(VAR) * VarNf(VAR) * VarNf(VAR) * static_cast<int>(sizeof(double)) : 0;
   if (dyn > 0) {
     const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(QpBlocksKernel<ORDER, VAR, HS>), dyn);
     if (e != cudaSuccess) return e;
@@ -490,11 +509,10 @@ static cudaError_t LaunchBlk(const BlkParams& p, unsigned g, cudaStream_t s, boo
 cudaError_t LaunchQpBlocks(const BlkParams& p, cudaStream_t s, bool pdl) {
   const long long K = p.n_inst * p.N;
   if (K <= 0) return cudaSuccess;
-  const long long per_cta = 2 * kWarps;
-  const long long grid = (K + per_cta - 1) / per_cta;
-  const unsigned g = static_cast<unsigned>(grid);
   const char* e = std::getenv("RTN_BLK_HS");  // A/B aid: 0 forces the 4-CTA variant
   const bool hs = K <= kLatencyMaxNodes && !(e && e[0] == '0');  // latency-sized batches
+  const long long per_cta = hs ? kWarps : 2 * kWarps;            // nodes per CTA
+  const unsigned g = static_cast<unsigned>((K + per_cta - 1) / per_cta);
 #define RTN_BLK(O, V) return hs ? LaunchBlk<O, V, true>(p, g, s, pdl) : LaunchBlk<O, V, false>(p, g, s, pdl)
   switch (p.variant * 2 + (p.order == 2 ? 1 : 0)) {
     case kVarFull * 2: RTN_BLK(1, kVarFull);

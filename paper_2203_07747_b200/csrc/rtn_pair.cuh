@@ -180,6 +180,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_mma_layers = prm.n_hidden - 1;
   const long long pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
+  // This epilogue thread's element of the first tile's inputs, read before the
+  // setup below: with zero-copy latency calls it is a PCIe round trip, which
+  // then overlaps barrier init, TMEM allocation and the cluster barrier.
+  // Order 1: raw z (centred later); order 2: centred (load_z).
+  double z_first = 0.0;
+  if (threadIdx.x >= 128 && pair < prm.num_tiles) {
+    const int e = static_cast<int>(threadIdx.x) - 128;
+    if constexpr (ORD2 != 0) {
+      const long long node0 = pair / (ORD2 == 1 ? 2 : prm.ord2_g);
+      if (e < n_in && node0 < prm.K) z_first = load_z(prm, node0, e);
+    } else if (e < 2 * P * n_in) {
+      const int zp = e / n_in, zk = e - zp * n_in;
+      const long long node0 = pair * (2 * P) + zp;
+      if (node0 < prm.K)
+        z_first = prm.zx == nullptr ? prm.z[node0 * n_in + zk]
+                                    : (zk < 13 ? prm.zx[(node0 + node0 / prm.zN) * 13 + zk]
+                                               : prm.zu[node0 * 4 + (zk - 13)]);
+      else
+        z_first = __ldg(prm.mu + zk);
+    }
+  }
+
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
@@ -517,7 +539,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
         tc_fence_after();
       }
-      if (etid < kNin2) zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, etid)) : 0.0f;
+      if (etid < kNin2)
+        zs[etid] = node < prm.K ? static_cast<float>(tiles_done == 0 ? z_first : load_z(prm, node, etid)) : 0.0f;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       // ---- layer 0: v = σ(pre), t_a = σ'·W0'[:,a], h_ab = σ''·W0'[:,a]·W0'[:,b]
       for (int g = static_cast<int>(rank); g < NG; g += 2) {
@@ -643,7 +666,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
         tc_fence_after();
       }
-      if (etid < n_in) zs[etid] = node < prm.K ? static_cast<float>(load_z(prm, node, etid)) : 0.0f;
+      if (etid < n_in)
+        zs[etid] = node < prm.K ? static_cast<float>(tiles_done == 0 ? z_first : load_z(prm, node, etid)) : 0.0f;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       // ---- layer 0: v = σ(pre), t_a = σ'·W0'[:,a], h_ab = σ''·W0'[:,a]·W0'[:,b]
       for (int g = static_cast<int>(rank); g < NG; g += 2) {
@@ -836,7 +860,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     };
 
-    double znext = fetch_z(pair);
+    double znext = z_first;  // fetch_z(pair), issued before the setup
     float o[16];
     long long prev_node0 = -1;
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {

@@ -190,6 +190,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_in = prm.n_in, ntc = prm.nt;
   const int n_mma_layers = prm.n_hidden - 1;
   const long long node0 = static_cast<long long>(blockIdx.x >> 2) * 2;
+  // this epilogue thread's input element, read before the setup (a PCIe round
+  // trip with zero-copy latency calls; it overlaps barrier init, TMEM
+  // allocation and the cluster barrier)
+  double z_first = 0.0;
+  if (threadIdx.x >= 128 && static_cast<int>(threadIdx.x) - 128 < 2 * n_in) {
+    const int e = static_cast<int>(threadIdx.x) - 128, p = e / n_in;
+    if (node0 + p < prm.K) z_first = load_z(prm, node0 + p, e - p * n_in);
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -387,8 +395,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreads, 1)
     };
     const long long node = node0 + half;
     if (etid < 2 * n_in) {
-      const int p = etid / n_in, k = etid - p * n_in;
-      zs[etid] = node0 + p < prm.K ? static_cast<float>(load_z(prm, node0 + p, k)) : 0.0f;
+      const int p = etid / n_in;
+      zs[etid] = node0 + p < prm.K ? static_cast<float>(z_first) : 0.0f;
     }
     asm volatile("bar.sync 1, 256;" ::: "memory");
     // ---- layer 0 (CUDA cores): this CTA produces K-group `rank` for both nodes
