@@ -610,12 +610,42 @@ def run_ours(args, rank, world, local_rank):
 
     z_host = torch.from_numpy(synth_quad_nodes(2203 + rank, k))
     z = z_host.to(dev)
-    if world > 1:
+    gather = None
+    if world > 1 and args.gather == "p2p":
+        # peer-store gather through the C-ABI multi-GPU entry: rank 0's (f, J)
+        # buffers are mapped into every rank and each rank's kernel stores its
+        # rows straight into them over NVLink (rtn_comm_bind_root_outputs +
+        # rtn_prepare_partitioned_p2p); falls back to the NCCL gather below if
+        # the mapping is refused (no peer access)
+        try:
+            uid = C.create_string_buffer(128)
+            if rank == 0:
+                raise_for_status(L.rtn_comm_unique_id(uid))
+            obj = [uid.raw]
+            dist.broadcast_object_list(obj, src=0)
+            cm = C.c_void_p()
+            raise_for_status(L.rtn_comm_create(obj[0], world, rank, local_rank, C.byref(cm)))
+            total = sum(counts)
+            f_all = torch.empty((total, n_out), dtype=torch.float64, device=dev) if rank == 0 else None
+            j_all = torch.empty((total, n_out, n_in), dtype=torch.float64, device=dev) if rank == 0 else None
+            raise_for_status(L.rtn_comm_bind_root_outputs(cm, 0, f_all.data_ptr() if rank == 0 else None,
+                                                          j_all.data_ptr() if rank == 0 else None, total))
+            gather = "p2p"
+        except Exception as e:  # noqa: BLE001 - reported on stderr, the JSON line names the gather used
+            print(f"rank {rank}: p2p gather unavailable ({e}); using the NCCL gather", file=sys.stderr)
+        agree = torch.tensor([1 if gather == "p2p" else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if int(agree.item()) == 0:
+            gather = None
+    if world > 1 and gather is None:
         # the kernel writes straight into the gather send buffers (sharding.Gatherer),
         # and chunk i's NCCL gather overlaps chunk i+1's kernel (sharding.partitioned_step)
+        gather = "nccl"
         gf = Gatherer(counts, (n_out,), torch.float64, dev)
         gj = Gatherer(counts, (n_out, n_in), torch.float64, dev)
         f, jac = gf.local, gj.local
+    elif gather == "p2p":
+        f = jac = None  # outputs go straight to rank 0's f_all / j_all
     else:
         f = torch.empty((k, n_out), dtype=torch.float64, device=dev)
         jac = torch.empty((k, n_out, n_in), dtype=torch.float64, device=dev)
@@ -640,7 +670,16 @@ def run_ours(args, rank, world, local_rank):
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(stream)
                     ev.append((e0, e1))
-            if world > 1:
+            if gather == "p2p":
+                if ev is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                raise_for_status(L.rtn_prepare_partitioned_p2p(eng.ctx_ptr, cm, z.data_ptr(), k, 1))
+                if ev is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(stream)
+                    ev.append((e0, e1))
+            elif gather == "nccl":
                 partitioned_step(compute, [gf, gj], k, args.gather_chunks)
             else:
                 compute(0, k)
@@ -695,7 +734,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = total_nodes / float(e2e_s.item())
     # sanity: outputs finite and match the device-resident run
-    ok = bool(torch.isfinite(fp).all()) and bool(torch.allclose(fp, f.cpu(), rtol=0, atol=0))
+    ref_f = (f_all[:k] if rank == 0 else None) if gather == "p2p" else f
+    ok = bool(torch.isfinite(fp).all()) and (ref_f is None or bool(torch.allclose(fp, ref_f.cpu(), rtol=0, atol=0)))
 
     result = None
     if rank == 0:
@@ -742,6 +782,9 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "nodes": total_nodes, "nodes_per_rank": k,
                        "parallelism": f"instance partition x{world}" + (
+                           " + peer-store gather: each rank's kernel stores its (f,A,B) rows into rank 0's buffers "
+                           "over NVLink (rtn_prepare_partitioned_p2p), one-element all-reduce as completion"
+                           if gather == "p2p" else
                            f" + NCCL gather of (f,A,B) to rank 0 in {args.gather_chunks} chunks overlapping the kernel"
                            if world > 1 else ""),
                        "l2": "inputs larger than L2 (z 446 MB + outputs 2.8 GB per step); weights (11.6 MB) stay L2-resident by design",
@@ -778,6 +821,9 @@ def run_ours(args, rank, world, local_rank):
             result["latency"] = lat  # last: the driver's stdout tail keeps the per-step latency lines
     if world > 1:
         dist.barrier(device_ids=[local_rank])
+        if gather == "p2p":
+            L.rtn_comm_free(cm)  # unmaps rank 0's buffers on the other ranks
+            dist.barrier(device_ids=[local_rank])
         dist.destroy_process_group()
     if result is not None:
         print(json.dumps(result), flush=True)
@@ -823,7 +869,9 @@ def main():
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-modes", action="store_true")
     ap.add_argument("--no-blocks", action="store_true")
-    ap.add_argument("--gather-chunks", type=int, default=4, help="N>1: gather chunks overlapping the kernel")
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N>1, --gather nccl: chunks overlapping the kernel")
+    ap.add_argument("--gather", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1: peer stores into rank 0's buffers (one kernel per rank) or chunked NCCL gather")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = _env_int("RANK", 0)

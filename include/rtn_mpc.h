@@ -156,6 +156,27 @@ rtn_status rtn_prepare_partitioned_device(rtn_ctx* c, rtn_comm* comm, const doub
                                           double* d_f, double* d_jac, int root, double* d_f_all, double* d_jac_all,
                                           int chunks);
 
+/* Peer-store gather. The root's device output buffers (f_all: rows_total x n_out,
+ * jac_all: rows_total x n_out x n_in, NULL for order 0) are bound to the
+ * communicator once (collective; other ranks pass NULL): they are mapped into
+ * every rank by CUDA IPC (or used directly when the ranks are threads of one
+ * process). rtn_prepare_partitioned_p2p then runs one kernel per rank whose
+ * output stores go straight into the root's rows for that rank over NVLink --
+ * the gather is the kernel's own stores, overlapped tile by tile with the math --
+ * followed by a one-element all-reduce as the completion barrier. Enqueued on
+ * the context stream; on the root, the buffers are complete once it is done. */
+rtn_status rtn_comm_bind_root_outputs(rtn_comm* comm, int root, double* d_f_all, double* d_jac_all,
+                                      long long rows_total);
+rtn_status rtn_prepare_partitioned_p2p(rtn_ctx* c, rtn_comm* comm, const double* d_z, long long K_local, int order);
+
+/* CUDA IPC of a device buffer between processes (any pointer inside an
+ * allocation): 72 bytes = the allocation's cudaIpcMemHandle_t + the pointer's
+ * byte offset in it. rtn_ipc_import maps it on `device` (peer access enabled
+ * lazily); rtn_ipc_release unmaps a pointer rtn_ipc_import returned. */
+rtn_status rtn_ipc_export(const void* d_ptr, unsigned char out[72]);
+rtn_status rtn_ipc_import(const unsigned char handle[72], int device, void** d_ptr);
+rtn_status rtn_ipc_release(void* d_ptr);
+
 /* ---------------------------------------------------------------------------
  * Continuity-block builder (the step after PrepareNodes).
  * Replaces the node loop of

@@ -25,7 +25,8 @@ EXPORTS = (
     "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_ctx_nonfinite", "rtn_last_error",
     "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp", "rtn_solve_feedback",
     "rtn_comm_unique_id", "rtn_comm_create", "rtn_comm_free", "rtn_prepare_partitioned",
-    "rtn_prepare_partitioned_device",
+    "rtn_prepare_partitioned_device", "rtn_comm_bind_root_outputs", "rtn_prepare_partitioned_p2p",
+    "rtn_ipc_export", "rtn_ipc_import", "rtn_ipc_release",
 )
 
 
@@ -109,6 +110,11 @@ def lib() -> C.CDLL:
     L.rtn_comm_free.argtypes = [_vp]
     L.rtn_comm_free.restype = None
     L.rtn_prepare_partitioned.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp]
+    L.rtn_comm_bind_root_outputs.argtypes = [_vp, C.c_int, _vp, _vp, C.c_longlong]
+    L.rtn_prepare_partitioned_p2p.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int]
+    L.rtn_ipc_export.argtypes = [_vp, C.c_char_p]
+    L.rtn_ipc_import.argtypes = [C.c_char_p, C.c_int, C.POINTER(_vp)]
+    L.rtn_ipc_release.argtypes = [_vp]
     L.rtn_prepare_partitioned_device.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int, _vp, _vp, C.c_int, _vp, _vp,
                                                  C.c_int]
     L.rtn_make_mlp.argtypes = [_ip, C.c_int, C.c_ulonglong, C.POINTER(_dp), C.POINTER(_dp)]

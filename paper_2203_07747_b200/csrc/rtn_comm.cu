@@ -12,15 +12,27 @@
 // BatchedCore through ThreadPool::Global(), proj/src/neural.cpp:259-268),
 // which is the only parallelism the reference has.
 //
+// Peer-store gather (rtn_comm_bind_root_outputs + rtn_prepare_partitioned_p2p):
+// the root's output buffers are mapped into every rank (CUDA IPC, or the raw
+// pointer when the ranks are threads of one process), and each rank's kernel
+// stores its (f, A, B) rows straight into them over NVLink as its tiles
+// finish: the gather IS the kernel's output stores, overlapped tile by tile
+// with the math, with no staging copy and no NCCL data transfer. A one-element
+// NCCL all-reduce after the kernel is the completion barrier.
+//
 // NCCL is resolved at run time (dlopen "libnccl.so.2"): the library loads and
 // every single-GPU entry works without it; a missing NCCL or any NCCL failure
 // returns RTN_ENCCL with NCCL's message.
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -39,6 +51,8 @@ struct NcclApi {
   decltype(&ncclSend) Send = nullptr;
   decltype(&ncclRecv) Recv = nullptr;
   decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
   std::string why;  // empty when loaded
 };
@@ -66,6 +80,8 @@ const NcclApi& Nccl() {
     a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
     a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
     return a;
   }();
@@ -89,6 +105,68 @@ std::vector<std::pair<long long, long long>> ChunkBounds(long long rows, int chu
   return b;
 }
 
+// ---- CUDA IPC export / import of device buffers (any pointer inside an allocation)
+constexpr int kIpcBytes = 72;  // cudaIpcMemHandle_t (64) + byte offset of the pointer in its allocation (8)
+
+void* AllocationBase(const void* p, size_t* offset) {
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<GetRange>(f);
+  }();
+  if (!fn) throw Error(RTN_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+    throw Error(RTN_ECONFIG, "ipc export: not a device allocation");
+  *offset = static_cast<size_t>(reinterpret_cast<CUdeviceptr>(p) - base);
+  return reinterpret_cast<void*>(base);
+}
+
+void IpcExport(const void* p, unsigned char out[kIpcBytes]) {
+  size_t off = 0;
+  void* base = AllocationBase(p, &off);
+  cudaIpcMemHandle_t h;
+  CUDA_CHECK(cudaIpcGetMemHandle(&h, base));
+  std::memcpy(out, &h, sizeof(h));
+  const unsigned long long o = off;
+  std::memcpy(out + 64, &o, 8);
+}
+
+// imported pointer -> the mapping's base (cudaIpcCloseMemHandle takes the base)
+std::mutex g_ipc_mu;
+std::map<void*, void*> g_ipc_base;
+
+void* IpcImport(const unsigned char in[kIpcBytes], int device) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, in, sizeof(h));
+  unsigned long long off = 0;
+  std::memcpy(&off, in + 64, 8);
+  CUDA_CHECK(cudaSetDevice(device));
+  void* base = nullptr;
+  CUDA_CHECK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  void* p = static_cast<unsigned char*>(base) + off;
+  std::lock_guard<std::mutex> lock(g_ipc_mu);
+  g_ipc_base[p] = base;
+  return p;
+}
+
+void IpcRelease(void* p) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_ipc_mu);
+    auto it = g_ipc_base.find(p);
+    if (it == g_ipc_base.end()) throw Error(RTN_ECONFIG, "ipc release: pointer was not imported");
+    base = it->second;
+    g_ipc_base.erase(it);
+  }
+  CUDA_CHECK(cudaIpcCloseMemHandle(base));
+}
+
 }  // namespace
 
 struct rtn_comm {
@@ -103,10 +181,36 @@ struct rtn_comm {
   double* d_f_all = nullptr;
   double* d_jac_all = nullptr;
   long long all_cap = 0;  // rows
+  // peer-store gather: the root's outputs as addressable from this rank
+  int p2p_root = -1;
+  long long p2p_rows = 0;
+  double* p2p_f = nullptr;
+  double* p2p_jac = nullptr;
+  bool p2p_imported = false;      // p2p_f / p2p_jac are IPC mappings to release
+  unsigned char* d_bind = nullptr;  // handle exchange (device, pinned host)
+  unsigned char* h_bind = nullptr;
+  float* d_flag = nullptr;          // completion all-reduce
+  void Unbind() {
+    if (p2p_imported) {
+      try {
+        if (p2p_f) IpcRelease(p2p_f);
+        if (p2p_jac) IpcRelease(p2p_jac);
+      } catch (...) {
+      }
+    }
+    p2p_root = -1;
+    p2p_rows = 0;
+    p2p_f = p2p_jac = nullptr;
+    p2p_imported = false;
+  }
   ~rtn_comm() {
     int prev;
     if (cudaGetDevice(&prev) == cudaSuccess) {
       cudaSetDevice(device);
+      Unbind();
+      cudaFree(d_bind);
+      cudaFreeHost(h_bind);
+      cudaFree(d_flag);
       if (comm) Nccl().CommDestroy(comm);
       if (stream) cudaStreamDestroy(stream);
       cudaFree(d_counts);
@@ -260,6 +364,127 @@ rtn_status rtn_prepare_partitioned_device(rtn_ctx* c, rtn_comm* cm, const double
     c->points += static_cast<unsigned long long>(K_local);
     const std::vector<long long> counts = ExchangeCounts(cm, K_local);
     PartitionedEnqueue(c, cm, d_z, K_local, order, d_f, d_jac, root, d_f_all, d_jac_all, std::max(1, chunks), counts);
+  });
+}
+
+rtn_status rtn_ipc_export(const void* d_ptr, unsigned char out[72]) {
+  return Guard([&] {
+    if (!d_ptr || !out) throw Error(RTN_ECONFIG, "null argument");
+    IpcExport(d_ptr, out);
+  });
+}
+
+rtn_status rtn_ipc_import(const unsigned char handle[72], int device, void** d_ptr) {
+  return Guard([&] {
+    if (!handle || !d_ptr) throw Error(RTN_ECONFIG, "null argument");
+    *d_ptr = IpcImport(handle, device);
+  });
+}
+
+rtn_status rtn_ipc_release(void* d_ptr) {
+  return Guard([&] {
+    if (!d_ptr) throw Error(RTN_ECONFIG, "null argument");
+    IpcRelease(d_ptr);
+  });
+}
+
+// Packet broadcast by the root: [0,72) f handle, [72,144) jac handle, then
+// rows_total, the raw f / jac pointers, the root's pid and device.
+constexpr int kBindBytes = 192;
+
+rtn_status rtn_comm_bind_root_outputs(rtn_comm* cm, int root, double* d_f_all, double* d_jac_all,
+                                      long long rows_total) {
+  NvtxRange nvtx("rtn_comm_bind_root_outputs");
+  return Guard([&] {
+    if (!cm) throw Error(RTN_ECONFIG, "null argument");
+    if (root < 0 || root >= cm->nranks) throw Error(RTN_ECONFIG, "root outside [0, nranks)");
+    const bool is_root = cm->rank == root;
+    if (is_root && (!d_f_all || rows_total < 0)) throw Error(RTN_ECONFIG, "root needs f_all (and rows_total >= 0)");
+    const NcclApi& nc = Nccl();
+    CUDA_CHECK(cudaSetDevice(cm->device));
+    cm->Unbind();
+    if (!cm->d_bind) {
+      CUDA_CHECK(cudaMalloc(&cm->d_bind, kBindBytes));
+      CUDA_CHECK(cudaMallocHost(&cm->h_bind, kBindBytes));
+      CUDA_CHECK(cudaMalloc(&cm->d_flag, sizeof(float)));
+      CUDA_CHECK(cudaMemset(cm->d_flag, 0, sizeof(float)));
+    }
+    unsigned char* pk = cm->h_bind;
+    std::memset(pk, 0, kBindBytes);
+    if (is_root) {
+      IpcExport(d_f_all, pk);
+      if (d_jac_all) IpcExport(d_jac_all, pk + 72);
+      const long long pid = static_cast<long long>(getpid()), dev = cm->device;
+      const unsigned long long fp = reinterpret_cast<unsigned long long>(d_f_all),
+                               jp = reinterpret_cast<unsigned long long>(d_jac_all);
+      std::memcpy(pk + 144, &rows_total, 8);
+      std::memcpy(pk + 152, &fp, 8);
+      std::memcpy(pk + 160, &jp, 8);
+      std::memcpy(pk + 168, &pid, 8);
+      std::memcpy(pk + 176, &dev, 8);
+    }
+    CUDA_CHECK(cudaMemcpyAsync(cm->d_bind, pk, kBindBytes, cudaMemcpyHostToDevice, cm->stream));
+    NCCL_CHECK(nc.Broadcast(cm->d_bind, cm->d_bind, kBindBytes, ncclUint8, root, cm->comm, cm->stream));
+    CUDA_CHECK(cudaMemcpyAsync(pk, cm->d_bind, kBindBytes, cudaMemcpyDeviceToHost, cm->stream));
+    CUDA_CHECK(cudaStreamSynchronize(cm->stream));
+    long long rows = 0, pid = 0, rdev = 0;
+    unsigned long long fp = 0, jp = 0;
+    std::memcpy(&rows, pk + 144, 8);
+    std::memcpy(&fp, pk + 152, 8);
+    std::memcpy(&jp, pk + 160, 8);
+    std::memcpy(&pid, pk + 168, 8);
+    std::memcpy(&rdev, pk + 176, 8);
+    if (is_root) {
+      cm->p2p_f = d_f_all;
+      cm->p2p_jac = d_jac_all;
+    } else if (pid == static_cast<long long>(getpid())) {  // ranks are threads of one process: UVA pointers
+      if (rdev != cm->device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(static_cast<int>(rdev), 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_CHECK(e);
+        cudaGetLastError();
+      }
+      cm->p2p_f = reinterpret_cast<double*>(fp);
+      cm->p2p_jac = reinterpret_cast<double*>(jp);
+    } else {
+      cm->p2p_f = static_cast<double*>(IpcImport(pk, cm->device));
+      cm->p2p_imported = true;
+      if (jp) cm->p2p_jac = static_cast<double*>(IpcImport(pk + 72, cm->device));
+    }
+    cm->p2p_rows = rows;
+    cm->p2p_root = root;
+  });
+}
+
+rtn_status rtn_prepare_partitioned_p2p(rtn_ctx* c, rtn_comm* cm, const double* d_z, long long K_local, int order) {
+  NvtxRange nvtx("rtn_prepare_partitioned_p2p");
+  return Guard([&] {
+    if (!cm) throw Error(RTN_ECONFIG, "null argument");
+    if (cm->p2p_root < 0) throw Error(RTN_ECONFIG, "bind the root's outputs first (rtn_comm_bind_root_outputs)");
+    CheckPartitioned(c, cm, K_local, order, cm->p2p_root);
+    if (K_local > 0 && !d_z) throw Error(RTN_ECONFIG, "null buffer");
+    if (order >= 1 && !cm->p2p_jac) throw Error(RTN_ECONFIG, "order 1 needs the root's jac_all bound");
+    const NcclApi& nc = Nccl();
+    CUDA_CHECK(cudaSetDevice(cm->device));
+    c->calls += 1;
+    c->points += static_cast<unsigned long long>(K_local);
+    const std::vector<long long> counts = ExchangeCounts(cm, K_local);
+    long long off = 0, total = 0;
+    for (int r = 0; r < cm->nranks; ++r) {
+      if (r < cm->rank) off += counts[r];
+      total += counts[r];
+    }
+    if (total > cm->p2p_rows) throw Error(RTN_ECONFIG, "rows exceed the bound root outputs");
+    const rtn_model* m = c->model;
+    const long long jrow = static_cast<long long>(m->n_out) * m->n_in;
+    // one launch: every tile's output stores land in the root's buffers
+    Enqueue(c, d_z, K_local, order, cm->p2p_f + off * m->n_out, order >= 1 ? cm->p2p_jac + off * jrow : nullptr);
+    // completion barrier: each rank's all-reduce follows its kernel, so the
+    // root's completes after every rank's stores
+    CUDA_CHECK(cudaEventRecord(cm->ev_done, c->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(cm->stream, cm->ev_done, 0));
+    NCCL_CHECK(nc.AllReduce(cm->d_flag, cm->d_flag, 1, ncclFloat32, ncclSum, cm->comm, cm->stream));
+    CUDA_CHECK(cudaEventRecord(cm->ev_done, cm->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(c->stream, cm->ev_done, 0));
   });
 }
 
