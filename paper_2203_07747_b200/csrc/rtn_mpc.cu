@@ -95,6 +95,7 @@ uint16_t Bf16Bits(float x) {
 namespace rtn_host {
 
 unsigned long long* trace_buf = nullptr;  // RTN_TRACE device buffer
+void* trace_host = nullptr;               // RTN_TRACE_HOST: the same buffer, host-mapped
 constexpr long long kGraphMaxRows = 4096;     // latency mode: graph-captured steps up to this K
 constexpr long long kChunkMinRows = 1 << 17;  // chunk only batches this large
 
@@ -295,6 +296,7 @@ rtn_model* UploadModel(const Packed& pk, int device) {
   const size_t hid_rows = static_cast<size_t>(std::max(pk.n_layers - 2, 1)) * pk.pwp;
   m->tmap_h = MakeTmap(m->d_wt_hidden, pk.split * hid_rows, pk.pwp, 128, pk.bf16);
   m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(pk.split) * 16, pk.pwp, 8, pk.bf16);
+  if (pk.pwp == 512 && pk.split == 1 && !pk.bf16) m->tmap_h64 = MakeTmap(m->d_wt_hidden, hid_rows, pk.pwp, 64, false);
   m->lo_rows = static_cast<int>(hid_rows);
   return m.release();
 }
@@ -456,15 +458,17 @@ HostModel ParseRmlp(const std::vector<char>& bytes) {
 //   rows    : TF32 width-256 throughput batches, activations as the A operand
 //             in TMEM (rtn_rows.cuh);
 //   pair    : pair-kernel throughput tiles (rtn_pair.cuh).
-enum class Kern { kPair, kLatency, kQuad, kRows };
+enum class Kern { kPair, kLatency, kQuad, kRows, kSplit };
 Kern Choose(const rtn_model* m, long long K, int num_sms) {
   const bool lat_ok = m->n_in + 1 <= 24;
   const bool quad_ok = lat_ok && m->pair_wp == 512 && m->n_in <= rtn::kMaxIn0 && K <= 2 * (num_sms / 4);
-  const bool rows_ok = m->pair_mode == rtn::kTF32 && m->pair_wp == 256 && m->n_in >= rtn::kRowsMinIn &&
-                       m->n_in <= rtn::kRowsMaxInHost && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
+  const bool rows_geom = m->pair_mode == rtn::kTF32 && m->n_in >= rtn::kRowsMinIn && m->n_in <= rtn::kRowsMaxInHost;
+  const bool rows_ok = rows_geom && m->pair_wp == 256 && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
+  const bool split_ok = rows_geom && m->pair_wp == 512;
   if (const char* e = std::getenv("RTN_KERNEL")) {
     if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
     if (std::strcmp(e, "rows") == 0 && rows_ok) return Kern::kRows;
+    if (std::strcmp(e, "split") == 0 && split_ok) return Kern::kSplit;
     if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
     if (std::strcmp(e, "pair") == 0) return Kern::kPair;
     // a kernel that does not apply to this model: the default choice below
@@ -474,6 +478,8 @@ Kern Choose(const rtn_model* m, long long K, int num_sms) {
   if (lat_ok && K <= num_sms) return Kern::kLatency;
   const char* r = std::getenv("RTN_ROWS");
   if (rows_ok && !(r && r[0] == '0')) return Kern::kRows;
+  const char* sp = std::getenv("RTN_SPLIT");
+  if (split_ok && sp && sp[0] == '1') return Kern::kSplit;  // opt-in until measured faster than the pair kernel
   return Kern::kPair;
 }
 
@@ -508,7 +514,14 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
   if (const char* d = std::getenv("RTN_DEBUG")) prm.dbg = std::atoi(d);
   if (const char* tr = std::getenv("RTN_TRACE")) {  // per-event timestamps of pair 0 (profiling aid)
     prm.trace_tile = std::max(0, std::atoi(tr) - 1);
-    if (!trace_buf) CUDA_CHECK(cudaMalloc(&trace_buf, 256 * 8));
+    if (!trace_buf) {
+      if (std::getenv("RTN_TRACE_HOST")) {  // host-mapped: readable while a kernel hangs (debug aid)
+        CUDA_CHECK(cudaHostAlloc(&trace_host, 256 * 8, cudaHostAllocMapped));
+        CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&trace_buf), trace_host, 0));
+      } else {
+        CUDA_CHECK(cudaMalloc(&trace_buf, 256 * 8));
+      }
+    }
     CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, 256 * 8, c->stream));
     prm.trace = trace_buf;
   }
@@ -541,6 +554,17 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
         : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
                                        : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
+    c->launches += 1;
+    return;
+  }
+  if (kern == Kern::kSplit) {
+    // width 512: activations split between TMEM and shared memory (rtn_split.cuh), 128 rows per CTA
+    prm.P = 128 / (1 + m->n_in);
+    prm.nt = 128;
+    prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);
+    const int g5 = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+    e = rtn::LaunchSplitTF32(prm, m->tmap_h64, m->tmap_l, g5, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("split kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }
@@ -585,6 +609,10 @@ const char* rtn_last_error(void) { return g_err.c_str(); }
 // (256 globaltimer stamps of pair 0's first tile) after a synchronised call.
 int rtn_debug_trace(unsigned long long* out, int n) {
   if (!trace_buf || n > 256) return 1;
+  if (trace_host) {  // no CUDA call: works while the traced kernel is still running
+    std::memcpy(out, trace_host, sizeof(unsigned long long) * n);
+    return 0;
+  }
   return cudaMemcpy(out, trace_buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
 }
 

@@ -1,0 +1,25 @@
+// Split-kernel instantiations (TF32, width 512; rtn_split.cuh), one
+// translation unit so it compiles in parallel with the pair kernels.
+#include <cstdio>
+
+#include "rtn_launch.h"
+// #define RTN_SPLIT_DEBUG 1  // bounded waits + progress stamps (RTN_TRACE_HOST) for hang hunting
+#include "rtn_split.cuh"
+
+#ifndef SPLIT_NS
+#define SPLIT_NS 4
+#endif
+
+namespace rtn {
+
+cudaError_t LaunchSplitTF32(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,
+                            cudaStream_t st) {
+  using Cfg = SplitCfg<SPLIT_NS>;
+  auto kern = prm.act == 0 ? rtn_split_kernel<SPLIT_NS, 0> : (prm.act == 1 ? rtn_split_kernel<SPLIT_NS, 1> : rtn_split_kernel<SPLIT_NS, 2>);
+  const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kSplitThreads, Cfg::kSmemBytes, st>>>(prm, th64, tl);
+  return cudaGetLastError();
+}
+
+}  // namespace rtn
