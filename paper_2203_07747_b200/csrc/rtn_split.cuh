@@ -49,6 +49,8 @@ constexpr int kSplitThreads = 320;
 constexpr int kSplitStage = 8192;  // one weight stage per CTA: 64 neurons x 32 k fp32
 constexpr int kSplitTab = 132;     // floats per node row of the σ/σ' tables (bank spread)
 constexpr int kSplitMaxNodes = 16;
+constexpr int kSplitTab0Nodes = 8;   // next tile's layer-0 σ/σ' tables precomputed when NPC <= 8 (n_in >= 15)
+constexpr int kSplitTab0 = 516;      // floats per (node, σ|σ') row of those tables
 
 #ifdef RTN_SPLIT_DEBUG
 // bounded wait: reports which barrier a thread is stuck on, then traps
@@ -96,7 +98,8 @@ struct SplitCfg {
   static constexpr uint32_t kPreOff = kStageOff + NSTAGE * kSplitStage;   // [16][132] value-row pre
   static constexpr uint32_t kTabOff = kPreOff + kSplitMaxNodes * kSplitTab * 4;      // [16][2][132] σ, σ'
   static constexpr uint32_t kZsOff = kTabOff + kSplitMaxNodes * 2 * kSplitTab * 4;   // [16][32] z
-  static constexpr uint32_t kBarOff = kZsOff + kSplitMaxNodes * 32 * 4;
+  static constexpr uint32_t kTab0Off = kZsOff + kSplitMaxNodes * 32 * 4;                // [8][2][516] layer-0 σ, σ'
+  static constexpr uint32_t kBarOff = kTab0Off + kSplitTab0Nodes * 2 * kSplitTab0 * 4;
   // full/empty[NSTAGE], act[2][16], tmem_full[2], reg_free[2], s_free, tmem_last
   static constexpr uint32_t kNumBars = 2 * NSTAGE + 32 + 6;
   static constexpr uint32_t kMiscOff = kBarOff + kNumBars * 8;
@@ -116,6 +119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
   float* pre_t = reinterpret_cast<float*>(smem + C::kPreOff);
   float* tab = reinterpret_cast<float*>(smem + C::kTabOff);
   float* zs = reinterpret_cast<float*>(smem + C::kZsOff);
+  float* tab0 = reinterpret_cast<float*>(smem + C::kTab0Off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* full = bars;
   uint64_t* empty = bars + NSTAGE;
@@ -424,6 +428,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
           tiles_done == static_cast<uint32_t>(prm.trace_tile) + 1)
         prm.trace[180 + e] = globaltimer();
     };
+    // ---- layer 0 with precomputed tables (npc <= 8): the σ, σ' of all 512
+    // neurons for the next tile are computed in the epilogue's idle time of the
+    // current tile's first hidden layer, so the tile boundary only stores.
+    const bool pre0 = npc <= kSplitTab0Nodes;
+    const float* my_tab0 = tab0 + ((valid ? p : 0) * 2 + (j == 0 ? 0 : 1)) * kSplitTab0;
+    // quarter q of the tables (q = 0 first stages z of `tile` from znext and
+    // prefetches the tile after); one quarter per idle window
+    auto layer0_tables = [&](long long tile, int q) {
+      if (q == 0) {
+        if (zown) zs[zp * 32 + zk] = znext;
+        named_bar(3, 256);
+        znext = fetch_z(tile + npairs);
+      }
+      for (int w = etid; w < 128 * ((npc + 3) >> 2); w += 256) {
+        const int n = 128 * q + (w & 127), p0 = 4 * (w >> 7);
+        float pre[4], wk[kRowsMaxIn];
+        const float bj = __ldg(prm.b0 + n);
+#pragma unroll
+        for (int k = 0; k < kRowsMaxIn; ++k) wk[k] = k < n_in ? __ldg(prm.w0t + k * 512 + n) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pre[u] = bj;
+#pragma unroll
+        for (int k = 0; k < kRowsMaxIn; ++k) {
+          if (k < n_in) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pre[u] = fmaf(wk[k], zs[(p0 + u) * 32 + k], pre[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (p0 + u < kSplitTab0Nodes) {
+            float val, sp;
+            act_rows<ACT>(pre[u], val, sp);
+            tab0[((p0 + u) * 2) * kSplitTab0 + n] = val;
+            tab0[((p0 + u) * 2 + 1) * kSplitTab0 + n] = sp;
+          }
+        }
+      }
+    };
+    // this thread's 64 values of quarter q from tab0: W0'[n, k] loads first
+    auto layer0_quarter = [&](int q, float (&y)[64]) {
+      const int jw = j > 0 ? j - 1 : 0;
+      const float* w0r = prm.w0 + (128 * q + 16 * h) * n_in + jw;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[16 * c + i] = __ldg(w0r + (32 * c + i) * n_in);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int c0 = 128 * q + 32 * c + 16 * h;
+        float t[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(t + i) = *reinterpret_cast<const float4*>(my_tab0 + c0 + i);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[16 * c + i] = to_tf32(j == 0 ? t[i] : t[i] * y[16 * c + i]);
+      }
+    };
+    auto layer0_pre = [&]() {
+#pragma unroll 1
+      for (int qi = 0; qi < 4; ++qi) {
+        const int q = qi == 0 ? 2 : (qi == 3 ? 3 : qi - 1);  // the order the first block reads them
+        float y[64];
+        layer0_quarter(q, y);
+        if (q < 2) {
+          store_s(y, q);
+        } else {
+          const uint32_t reg = tmem_base + (q == 2 ? T0 : T1) * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tmem_st16(reg + lane_base + 32 * c + 16 * h, y + 16 * c);
+            signal_tmem(4 * q + c);
+          }
+        }
+        tb(3 + 2 * qi);
+        tb(4 + 2 * qi);
+      }
+      ++prod;
+    };
     auto layer0 = [&](long long tile) {
       mark(1);
       tb(2);
@@ -497,9 +579,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
       ++prod;
     };
 
+    if (pre0)  // the first tile's; later ones during the previous tile's first hidden layers
+      for (int q = 0; q < 4; ++q) layer0_tables(pair, q);
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
       const long long node0 = tile * (2 * npc) + static_cast<long long>(rank) * npc;
-      layer0(tile);
+      tb(2);
+      if (pre0) {
+        for (int q = n_mma < 4 ? n_mma : 4; q < 4 && tiles_done > 0; ++q) layer0_tables(tile, q);  // short nets
+        named_bar(3, 256);  // tab0 complete
+        layer0_pre();
+      } else {
+        layer0(tile);
+      }
       for (int l = 0; l < n_mma; ++l, ++layers) {
         const float* bias = prm.bh + l * 512;
         // RTN_TRACE: CTA 0 of pair 0, warp 2 lane 0, tile trace_tile: 10 events per layer at 64 + 10·l
@@ -520,6 +611,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(rf_cl);
+        // the next tile's layer-0 tables fill the wait for B1 (tab0 and zs are
+        // free: this tile's layer 0 has been stored)
+        if (pre0 && l < 4 && tile + npairs < prm.num_tiles) layer0_tables(tile + npairs, l);
         ev(1);
         // B1 (F1) → registers
         SPW(&tmem_full[1], tf_use[1]++ & 1, 11);
