@@ -803,7 +803,7 @@ def run_ours(args, rank, world, local_rank):
                          "frac_of_sustained_bf16_half": (achieved / (peaks["bf16_tflops_sustained"] / 2)
                                                          if peaks.get("bf16_tflops_sustained") else None),
                          "flop_per_node": fl, "flops_definition": "2*(1+n_in)*sum(n_l*n_{l+1}) forward-mode (BASELINE.md s2)",
-                         "kernel": "rtn_pair_kernel<512,4,4,80,TF32> (tcgen05 cta_group::2 tf32)"},
+                         "kernel": "rtn_split_kernel<4,SiLU> (tcgen05 cta_group::2 tf32, A split TMEM/smem)"},
             "clocks": clocks,
         }
         if cpu:

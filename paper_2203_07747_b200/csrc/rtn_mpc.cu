@@ -451,12 +451,14 @@ HostModel ParseRmlp(const std::vector<char>& bytes) {
   return m;
 }
 
-// Kernel choice (RTN_KERNEL=pair|latency|quad|rows forces one where it applies):
+// Kernel choice (RTN_KERNEL=pair|latency|quad|rows|split forces one where it applies):
 //   quad    : width 512, order <= 1, K <= 2·(#SMs/4) — 4-CTA clusters, each
 //             CTA pair computes one 256-neuron block (rtn_quad.cuh): one MPC step;
 //   latency : pair kernel with one node per CTA side, K <= #SMs;
 //   rows    : TF32 width-256 throughput batches, activations as the A operand
 //             in TMEM (rtn_rows.cuh);
+//   split   : TF32 width-512 throughput batches, the A operand split between
+//             TMEM and shared memory (rtn_split.cuh);
 //   pair    : pair-kernel throughput tiles (rtn_pair.cuh).
 enum class Kern { kPair, kLatency, kQuad, kRows, kSplit };
 Kern Choose(const rtn_model* m, long long K, int num_sms) {
@@ -479,7 +481,7 @@ Kern Choose(const rtn_model* m, long long K, int num_sms) {
   const char* r = std::getenv("RTN_ROWS");
   if (rows_ok && !(r && r[0] == '0')) return Kern::kRows;
   const char* sp = std::getenv("RTN_SPLIT");
-  if (split_ok && sp && sp[0] == '1') return Kern::kSplit;  // opt-in until measured faster than the pair kernel
+  if (split_ok && !(sp && sp[0] == '0')) return Kern::kSplit;
   return Kern::kPair;
 }
 

@@ -15,12 +15,13 @@ TF32_TOL = 1e-3
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["pair", "latency", "quad", "rows"])
+@pytest.fixture(params=["pair", "latency", "quad", "rows", "split"])
 def kernel(request, monkeypatch):
     """Every device kernel: CTA-pair throughput tiles, CTA-pair latency tiles (P=1), the
-    4-CTA-cluster latency kernel (width-512 models, K <= 2·(#SMs/4); others fall back) and
+    4-CTA-cluster latency kernel (width-512 models, K <= 2·(#SMs/4); others fall back),
     the width-256 rows kernel (activations as the MMA's A operand in TMEM; TF32 width-256
-    models with 7 <= n_in <= 31, others fall back)."""
+    models with 7 <= n_in <= 31, others fall back) and the width-512 split kernel (A split
+    between TMEM and shared memory; TF32 width-512 models with 7 <= n_in <= 31)."""
     monkeypatch.setenv("RTN_KERNEL", request.param)
     return request.param
 
@@ -159,4 +160,40 @@ def test_quad_kernel_bf16x3_bitwise_and_ragged(monkeypatch):
     full = eng.prepare(z, 1)
     for i in (0, 3, 6):
         one = eng.prepare(z[i:i + 1], 1)
+        assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
+
+
+def test_split_kernel_input_widths_and_ragged_tiles(monkeypatch):
+    """rtn_split.cuh: R = 1 + n_in rows per node, 128 // R nodes per CTA — 17 (7
+    nodes), 15 (8: the largest node count whose next-tile layer-0 tables are
+    precomputed), 7 (16: tables per quarter at the tile boundary), 26 and 31 (4);
+    K around the tile size and above the CTA-pair count; hidden widths that pad to
+    512; 1 to 4 hidden->hidden layers (the precomputed tables are spread over the
+    first four layers' idle windows; shorter nets finish them at the tile boundary)."""
+    monkeypatch.setenv("RTN_KERNEL", "split")
+    for k in (1, 13, 14, 15, 4099):
+        _check([17] + [512] * 4 + [6], "silu", k)
+    _check([15, 512, 512, 512, 6], "silu", 2500)
+    _check([7, 512, 512, 3], "silu", 3000)
+    _check([26, 512, 300, 3], "silu", 1000)
+    _check([31, 400, 512, 512, 6], "tanh", 501)
+    _check([17, 512, 6], "relu", 2100)             # one hidden layer: layer 0 straight into the output layer
+    _check([17, 512, 512, 6], "silu", 2100)        # one hidden->hidden layer
+    _check([17] + [512] * 4 + [6], "tanh", 2100)   # three
+    _check([17] + [512] * 5 + [6], "silu", 2100)   # four
+
+
+def test_split_kernel_default_and_bitwise_rows(monkeypatch):
+    """Without RTN_KERNEL a TF32 width-512 batch above the latency regime runs the
+    split kernel; its rows are bit-identical to single-node calls forced onto it."""
+    from paper_2203_07747_b200 import mlp_batched_eval, EvalOrder
+    om = OracleModel.random_net([17] + [512] * 6 + [6], "silu", 41)
+    z = quad_nodes(9, 5000)
+    monkeypatch.delenv("RTN_KERNEL", raising=False)
+    full = mlp_batched_eval(to_product_model(om), z, EvalOrder.JACOBIAN)
+    f, j, _ = om.batched_eval(z, 1)
+    assert max_node_rel_error(full.values, f) < TF32_TOL and max_node_rel_error(full.jacobians, j) < TF32_TOL
+    monkeypatch.setenv("RTN_KERNEL", "split")
+    for i in (0, 6, 7, 13, 14, 2072, 4999):
+        one = mlp_batched_eval(to_product_model(om), z[i:i + 1], EvalOrder.JACOBIAN)
         assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])

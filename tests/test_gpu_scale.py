@@ -38,7 +38,7 @@ def _sampled(om, prec, k, kernel, monkeypatch, every=1000, seed=2203):
 
 
 def test_cfg5_headline_kernel_tf32_many_tiles(monkeypatch):
-    """The bench's TF32 kernel (chooser default at K >> #SMs), 200,704 nodes."""
+    """The bench's TF32 kernel (chooser default at K >> #SMs: the split kernel), 200,704 nodes."""
     err = _sampled(_net([17] + [512] * 12 + [6], "silu", 2.5), "tf32", 200704, None, monkeypatch)
     assert err < 5e-3, err  # TF32's documented limit on this net (test_gpu_precision.py)
     err = _sampled(_net([17] + [512] * 12 + [6], "silu", 2.0), "tf32", 200704, None, monkeypatch)
@@ -86,4 +86,10 @@ def test_latency_tiles_forced_on_a_large_batch(monkeypatch):
 def test_cfg5_shape_bf16_single_pass_many_tiles(monkeypatch):
     """Single-pass BF16 on the throughput tiles (P = 4), 100k nodes, gain 2.0."""
     err = _sampled(_net([17] + [512] * 12 + [6], "silu", 2.0), "bf16", 100352, None, monkeypatch)
+    assert err < 1e-3, err
+
+
+def test_cfg5_pair_kernel_tf32_many_tiles(monkeypatch):
+    """The TF32 pair kernel (rtn_pair_kernel<512,4,4,80,TF32>, forced) on the same shape."""
+    err = _sampled(_net([17] + [512] * 12 + [6], "silu", 2.0), "tf32", 200704, "pair", monkeypatch)
     assert err < 1e-3, err
