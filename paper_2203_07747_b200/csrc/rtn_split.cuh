@@ -83,13 +83,13 @@ __device__ __forceinline__ void split_wait(uint64_t* bar, uint32_t parity, int t
 #endif
 
 // K-chunk order of a block: the first block of a layer (and the output layer)
-// takes quarter 2 (chunks 8..11, rewritten in place while the previous layer's
-// B3 still ran), then S (chunks 0..7, stored while B3 read T: those stores
-// need the shared-memory port that S-operand MMAs saturate), then quarter 3
-// (rewritten last); the other blocks S then T, so B3 frees S at its midpoint.
-__host__ __device__ constexpr int split_chunk(int i, bool first) {
-  return first ? (i < 4 ? 8 + i : (i < 12 ? i - 4 : i)) : i;
-}
+// takes the quarters in the order the epilogue finishes them — 2 (chunks 8..11,
+// rewritten in place while the previous layer's B3 still ran), 0 (stored into
+// S while B3 read T: those stores need the shared-memory port that S-operand
+// MMAs saturate), 3 (rewritten once B3 is done), 1 (stored last); the other
+// blocks S then T, so B3 frees S at its midpoint.
+__host__ __device__ constexpr int split_quarter(int qi, bool first) { return first ? (0x1302 >> (4 * qi)) & 15 : qi; }
+__host__ __device__ constexpr int split_chunk(int i, bool first) { return 4 * split_quarter(i >> 2, first) + (i & 3); }
 
 template <int NSTAGE>
 struct SplitCfg {
@@ -209,6 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
       const bool stream_only = prm.dbg & 128;  // dbg 128: weight stream + MMAs only (timing)
       const bool tr_pair = prm.trace && pair == 0 && !(prm.dbg & 256);
       long long tix = 0;
+      unsigned long long* tchunk = nullptr;  // RTN_TRACE: per-chunk issue times of one B0 (layer 5)
       auto block = [&](uint32_t d, uint32_t idesc, bool wait_input, uint32_t sbar, bool first) {
         wait_input = wait_input && !stream_only;
         uint64_t* a_set = act + 16 * (prod & 1);
@@ -221,15 +222,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
           // their barrier is the one of the quarter's first chunk
           if (wait_input && (c >= 8 || (c & 3) == 0)) SPWC(&a_set[c], par, 100 + c);
           if (lane == 0) SPT(3, (static_cast<unsigned long long>(prod) << 32) | c);
+          if (tchunk) tchunk[2 * i] = globaltimer();
           SPW(&full[st], ph, 3);
           tc_fence_after();
+          if (tchunk) tchunk[2 * i + 1] = globaltimer();
           const uint64_t wd = w0d + st * kStageD;
-          if (c < 8) {
-            mma4_tf32_pair_commit(d, s0d + c * kChunkD, wd, idesc, i != 0, smem_u32(&empty[st]),
+          // dbg 512 / 1024 (with 128; timing only): every chunk's A from S / from T
+          const bool from_s = (prm.dbg & 512) ? true : ((prm.dbg & 1024) ? false : c < 8);
+          if (from_s) {
+            mma4_tf32_pair_commit(d, s0d + (c & 7) * kChunkD, wd, idesc, i != 0, smem_u32(&empty[st]),
                                   c == 7 ? sbar : 0u);
           } else {
-            const uint32_t treg = tmem_base + (c < 12 ? T0 : T1) * 128 + (c & 3) * 32;
+            const uint32_t treg = tmem_base + ((c & 7) < 4 ? T0 : T1) * 128 + (c & 3) * 32;
             mma4_tf32_pair_ts_commit(d, treg, wd, idesc, i != 0, smem_u32(&empty[st]));
+            if (c == 7 && sbar) mma_commit_pair(s_free);  // dbg 1024 only: S is never read
           }
           if (++st == NSTAGE) {
             st = 0;
@@ -241,7 +247,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
         const bool tr = tr_pair && tix == prm.trace_tile && lane == 0;
         for (int l = 0; l < n_mma; ++l, ++layers) {
           if (tr && l < 11) prm.trace[l * 5] = globaltimer();
+          tchunk = (tr && l == 4) ? prm.trace + 200 : nullptr;
           block(tmem_base + F0 * 128, idesc_h, true, 0u, true);
+          tchunk = nullptr;
           mma_commit_pair(&tmem_full[0]);
           if (tr && l < 11) prm.trace[l * 5 + 1] = globaltimer();
           block(tmem_base + F1 * 128, idesc_h, false, 0u, false);
@@ -488,7 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
     auto layer0_pre = [&]() {
 #pragma unroll 1
       for (int qi = 0; qi < 4; ++qi) {
-        const int q = qi == 0 ? 2 : (qi == 3 ? 3 : qi - 1);  // the order the first block reads them
+        const int q = split_quarter(qi, true);  // the order the first block reads them
         float y[64];
         layer0_quarter(q, y);
         if (q < 2) {
@@ -516,7 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
       const int jw = j > 0 ? j - 1 : 0;
 #pragma unroll 1
       for (int qi = 0; qi < 4; ++qi) {
-        const int q = qi == 0 ? 2 : (qi == 3 ? 3 : qi - 1);  // the order the first block reads them
+        const int q = split_quarter(qi, true);  // the order the first block reads them
         mark(10 + q);
         // tables: thread = (neuron n of the quarter, 4-node group); the W0' column
         // loads are all issued before the FMAs (one L2 round trip, not n_in)
@@ -636,7 +644,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
         SPW(s_free, layers & 1, 13);
         ev(6);
         store_s(y0, 0);
-        store_s(y1, 1);
         ev(7);
         // B3 (F1) rewritten in place: quarter 3
         SPW(&tmem_full[1], tf_use[1]++ & 1, 14);
@@ -644,6 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 1)
         ev(8);
         tables(tmem_base + F1 * 128, bias + 384);
         rewrite_block(tmem_base + F1 * 128, 3);
+        store_s(y1, 1);
         ev(9);
         ++prod;
         const int t0 = T0, t1 = T1;

@@ -38,3 +38,7 @@ if os.environ.get("RTN_DEBUG", "0") == "0":
     print("tile boundary (us from L11 B3 issue end): out seen", f"{(tbv[0] - base) / 1e3:.2f}", "out written",
           f"{(tbv[1] - base) / 1e3:.2f}", "layer0 start", f"{(tbv[2] - base) / 1e3:.2f}",
           "quarters (tables, stored):", " ".join(f"{(x - base) / 1e3:.2f}" for x in tbv[3:11]))
+    ch = np.array(buf[200:232], dtype=np.float64).reshape(16, 2)
+    b0 = t[4, 0]
+    print("L5 B0 per chunk (us from its issue start): act-ready / weights-ready")
+    print(" ".join(f"{(a - b0) / 1e3:.2f}/{(b - b0) / 1e3:.2f}" for a, b in ch))
