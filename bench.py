@@ -749,8 +749,9 @@ def run_ours(args, rank, world, local_rank):
         traffic = None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
-            traffic = prof.get("dram_bytes_per_launch_per_node", None)
-            traffic = traffic * k if traffic is not None else None
+            per_node = prof.get("dram_bytes_per_launch_per_node", None)
+            # per launch, like `achieved`: the step's node rows are split over n_launch / steps launches
+            traffic = per_node * k / max(1.0, n_launch / args.steps) if per_node is not None else None
         except Exception:
             pass
         cpu = None
