@@ -303,7 +303,17 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
                      "hardware_frac_basis": "MMA passes x algorithmic FLOPs vs the TF32 peak (bf16 MMAs run at 2x tf32)",
                      "kernel": {"3xtf32": "rtn_pair_kernel<512,8,1,24,3xTF32> (four main accumulators)",
                                 "bf16x3": "rtn_pair_kernel<512,4,4,80,bf16x3>",
-                                "bf16": "rtn_pair_kernel<512,8,4,80,bf16> (one kind::f16 pass)"}[name]}
+                                "bf16": "rtn_rowsb_kernel<8,SiLU> (one kind::f16 pass, whole layer input as the A "
+                                        "operand in TMEM)"}[name]}
+        if name == "bf16":
+            try:
+                pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+                out[name]["roofline"] = {"bound": "tensor", "achieved": ach, "unit": "TFLOP/s",
+                                         "peak": pk["bf16_tflops_sustained"], "frac": ach / pk["bf16_tflops_sustained"],
+                                         "frac_of_burst": ach / pk["bf16_tflops"],
+                                         "peak_source": "MEASURED_PEAKS.json bf16 (sustained; burst in frac_of_burst)"}
+            except Exception:
+                pass
         eng.close()
         runs[name] = (lambda f_, j_: (lambda idx: (f_[idx].cpu().numpy(), j_[idx].cpu().numpy())))(f, j)
     return out, runs

@@ -69,7 +69,7 @@ struct rtn_model {
   void* d_wt_hidden = nullptr;  // split x (n_hidden-1)·wp rows x wp cols (fp32 or bf16)
   void* d_wt_last = nullptr;    // split x 16 rows x wp cols
   CUtensorMap tmap_h{}, tmap_l{};
-  CUtensorMap tmap_h64{};  // TF32 width 512: the same hidden pack in 64-row boxes (split kernel)
+  CUtensorMap tmap_h64{};  // width 512, TF32 / BF16: the same hidden pack in 64-row boxes (split / rowsb kernels)
   int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3 / kBF16
   // rtn_model_load_rmlp's digest-keyed cache: shared handles are reference counted
   int refs = 1;

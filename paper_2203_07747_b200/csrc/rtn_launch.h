@@ -61,12 +61,16 @@ cudaError_t LaunchQuadBF16(const KParams& prm, const CUtensorMap& th, const CUte
 // (rtn_rows.cuh): TF32, order <= 1, 7 <= n_in <= 31, prm.P = 128 / (1 + n_in)
 // nodes per CTA, grid = 2 x pairs.
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
-constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 11;
+constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 11, kRbMinInHost = 15;
 // TF32 width-512 throughput, activations split between TMEM and shared memory
 // (rtn_split.cuh); th = the hidden pack in 64-row boxes. Same row geometry as the
 // rows kernel (7 <= n_in <= 31).
 cudaError_t LaunchSplitTF32(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,
                             cudaStream_t st);
+// BF16 width-512 throughput, the whole layer input as the A operand in TMEM
+// (rtn_rowsb.cuh); 15 <= n_in <= 31.
+cudaError_t LaunchRowsBF16(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,
+                           cudaStream_t st);
 
 
 // Order 2 (value + Jacobian + Hessian), n_in <= kMaxIn2. Order2Ntc picks the

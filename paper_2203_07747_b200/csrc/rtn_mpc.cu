@@ -296,7 +296,7 @@ rtn_model* UploadModel(const Packed& pk, int device) {
   const size_t hid_rows = static_cast<size_t>(std::max(pk.n_layers - 2, 1)) * pk.pwp;
   m->tmap_h = MakeTmap(m->d_wt_hidden, pk.split * hid_rows, pk.pwp, 128, pk.bf16);
   m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(pk.split) * 16, pk.pwp, 8, pk.bf16);
-  if (pk.pwp == 512 && pk.split == 1 && !pk.bf16) m->tmap_h64 = MakeTmap(m->d_wt_hidden, hid_rows, pk.pwp, 64, false);
+  if (pk.pwp == 512 && pk.split == 1) m->tmap_h64 = MakeTmap(m->d_wt_hidden, hid_rows, pk.pwp, 64, pk.bf16);
   m->lo_rows = static_cast<int>(hid_rows);
   return m.release();
 }
@@ -451,7 +451,7 @@ HostModel ParseRmlp(const std::vector<char>& bytes) {
   return m;
 }
 
-// Kernel choice (RTN_KERNEL=pair|latency|quad|rows|split forces one where it applies):
+// Kernel choice (RTN_KERNEL=pair|latency|quad|rows|split|rowsb forces one where it applies):
 //   quad    : width 512, order <= 1, K <= 2·(#SMs/4) — 4-CTA clusters, each
 //             CTA pair computes one 256-neuron block (rtn_quad.cuh): one MPC step;
 //   latency : pair kernel with one node per CTA side, K <= #SMs;
@@ -459,18 +459,23 @@ HostModel ParseRmlp(const std::vector<char>& bytes) {
 //             in TMEM (rtn_rows.cuh);
 //   split   : TF32 width-512 throughput batches, the A operand split between
 //             TMEM and shared memory (rtn_split.cuh);
+//   rowsb   : BF16 width-512 throughput batches (n_in >= 15), the whole layer
+//             input as the A operand in TMEM (rtn_rowsb.cuh);
 //   pair    : pair-kernel throughput tiles (rtn_pair.cuh).
-enum class Kern { kPair, kLatency, kQuad, kRows, kSplit };
+enum class Kern { kPair, kLatency, kQuad, kRows, kSplit, kRowsB };
 Kern Choose(const rtn_model* m, long long K, int num_sms) {
   const bool lat_ok = m->n_in + 1 <= 24;
   const bool quad_ok = lat_ok && m->pair_wp == 512 && m->n_in <= rtn::kMaxIn0 && K <= 2 * (num_sms / 4);
   const bool rows_geom = m->pair_mode == rtn::kTF32 && m->n_in >= rtn::kRowsMinIn && m->n_in <= rtn::kRowsMaxInHost;
   const bool rows_ok = rows_geom && m->pair_wp == 256 && m->n_hidden - 1 <= rtn::kRowsMaxMmaHost;
   const bool split_ok = rows_geom && m->pair_wp == 512;
+  const bool rowsb_ok = m->pair_mode == rtn::kBF16 && m->pair_wp == 512 && m->n_in >= rtn::kRbMinInHost &&
+                        m->n_in <= rtn::kRowsMaxInHost;
   if (const char* e = std::getenv("RTN_KERNEL")) {
     if (std::strcmp(e, "quad") == 0 && quad_ok) return Kern::kQuad;
     if (std::strcmp(e, "rows") == 0 && rows_ok) return Kern::kRows;
     if (std::strcmp(e, "split") == 0 && split_ok) return Kern::kSplit;
+    if (std::strcmp(e, "rowsb") == 0 && rowsb_ok) return Kern::kRowsB;
     if (std::strcmp(e, "latency") == 0 && lat_ok) return Kern::kLatency;
     if (std::strcmp(e, "pair") == 0) return Kern::kPair;
     // a kernel that does not apply to this model: the default choice below
@@ -482,6 +487,8 @@ Kern Choose(const rtn_model* m, long long K, int num_sms) {
   if (rows_ok && !(r && r[0] == '0')) return Kern::kRows;
   const char* sp = std::getenv("RTN_SPLIT");
   if (split_ok && !(sp && sp[0] == '0')) return Kern::kSplit;
+  const char* rb = std::getenv("RTN_ROWSB");
+  if (rowsb_ok && !(rb && rb[0] == '0')) return Kern::kRowsB;
   return Kern::kPair;
 }
 
@@ -556,6 +563,17 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
         : m->pair_mode == rtn::k3xTF32 ? rtn::LaunchQuad3xTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream)
                                        : rtn::LaunchQuadTF32(prm, m->tmap_h, m->tmap_l, g4, c->stream);
     if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("quad kernel launch: ") + cudaGetErrorString(e));
+    c->launches += 1;
+    return;
+  }
+  if (kern == Kern::kRowsB) {
+    // BF16 width 512: the whole layer input as the A operand in TMEM (rtn_rowsb.cuh)
+    prm.P = 128 / (1 + m->n_in);
+    prm.nt = 128;
+    prm.num_tiles = (K + 2 * prm.P - 1) / (2 * prm.P);
+    const int g6 = 2 * static_cast<int>(std::min<long long>(prm.num_tiles, c->num_sms / 2));
+    e = rtn::LaunchRowsBF16(prm, m->tmap_h64, m->tmap_l, g6, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("rowsb kernel launch: ") + cudaGetErrorString(e));
     c->launches += 1;
     return;
   }

@@ -4,6 +4,7 @@
 
 #include "rtn_launch.h"
 // #define RTN_SPLIT_DEBUG 1  // bounded waits + progress stamps (RTN_TRACE_HOST) for hang hunting
+#include "rtn_rowsb.cuh"
 #include "rtn_split.cuh"
 
 #ifndef SPLIT_NS
@@ -19,6 +20,16 @@ cudaError_t LaunchSplitTF32(const KParams& prm, const CUtensorMap& th64, const C
   const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
   kern<<<grid, kSplitThreads, Cfg::kSmemBytes, st>>>(prm, th64, tl);
+  return cudaGetLastError();
+}
+
+cudaError_t LaunchRowsBF16(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,
+                           cudaStream_t st) {
+  using Cfg = RowsBCfg<8>;
+  auto kern = prm.act == 0 ? rtn_rowsb_kernel<8, 0> : (prm.act == 1 ? rtn_rowsb_kernel<8, 1> : rtn_rowsb_kernel<8, 2>);
+  const cudaError_t e = EnsureSmem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kRbThreads, Cfg::kSmemBytes, st>>>(prm, th64, tl);
   return cudaGetLastError();
 }
 

@@ -197,3 +197,37 @@ def test_split_kernel_default_and_bitwise_rows(monkeypatch):
     for i in (0, 6, 7, 13, 14, 2072, 4999):
         one = mlp_batched_eval(to_product_model(om), z[i:i + 1], EvalOrder.JACOBIAN)
         assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])
+
+
+def test_rowsb_kernel_bf16_widths_ragged_and_bitwise(monkeypatch):
+    """rtn_rowsb.cuh (BF16, width 512, the whole layer input as the A operand in
+    TMEM): equal to the pair kernel's BF16 results within the bf16 class on the
+    input widths it takes (15, 17, 26, 31), ragged K, 1 to 5 hidden->hidden
+    layers, and rows of a batch bit-identical to single-node calls."""
+    from paper_2203_07747_b200 import _lib
+    bf16 = _lib.PRECISIONS["bf16"]
+
+    def run(sizes, act, k, kernel, seed=2203):
+        om = OracleModel.random_net(sizes, act, 11, True)
+        monkeypatch.setenv("RTN_KERNEL", kernel)
+        z = quad_nodes(seed, k) if sizes[0] == 17 else np.random.default_rng(seed).uniform(-2, 2, (k, sizes[0]))
+        got = to_product_model(om).engine(precision=bf16).prepare(z, 1)
+        f, j, _ = om.batched_eval(z, 1)
+        return got, max(max_node_rel_error(got.values, f), max_node_rel_error(got.jacobians, j))
+
+    for sizes, act, k in (([17] + [512] * 4 + [6], "silu", 1), ([17] + [512] * 4 + [6], "silu", 15),
+                          ([17] + [512] * 4 + [6], "silu", 4099), ([15, 512, 512, 512, 6], "silu", 2500),
+                          ([26, 512, 300, 3], "silu", 1000), ([31, 400, 512, 512, 6], "tanh", 501),
+                          ([17, 512, 6], "relu", 2100), ([17] + [512] * 6 + [6], "silu", 2100)):
+        got, err = run(sizes, act, k, "rowsb")
+        ref, err_pair = run(sizes, act, k, "pair")
+        assert np.isfinite(got.values).all() and np.isfinite(got.jacobians).all()
+        assert err < max(2 * err_pair, 2e-3), (sizes, k, err, err_pair)
+    om = OracleModel.random_net([17] + [512] * 6 + [6], "silu", 41)
+    z = quad_nodes(9, 3000)
+    monkeypatch.setenv("RTN_KERNEL", "rowsb")
+    eng = to_product_model(om).engine(precision=bf16)
+    full = eng.prepare(z, 1)
+    for i in (0, 6, 7, 13, 14, 2999):
+        one = eng.prepare(z[i:i + 1], 1)
+        assert np.array_equal(one.values[0], full.values[i]) and np.array_equal(one.jacobians[0], full.jacobians[i])

@@ -141,13 +141,13 @@ def test_inputs_far_from_zero(prec, monkeypatch):
     assert errs[1] < 2 * errs[0] + 1e-7, errs
 
 
-@pytest.mark.parametrize("kernel", ["pair", "latency", "quad"])
+@pytest.mark.parametrize("kernel", ["pair", "latency", "quad", "rowsb"])
 def test_bf16_single_pass_documented_bounds(kernel, monkeypatch):
     """Single-pass BF16 (RTN_BF16: bf16 operands, one kind::f16 pass, 2x the tf32
     MMA rate): 8-bit mantissa operand rounding, ~8x the TF32 error. It meets the
     1e-3 bound where |J| is well below 1 (12x512 g2.0: 3.2e-4; 5x256 g1.5: 8.9e-4)
     and reaches ~3e-2 on the |J| ~ 2 net — measured limits asserted here."""
-    k = 2048 if kernel == "pair" else 20
+    k = 2048 if kernel in ("pair", "rowsb") else 20
     assert _err(_net([17] + [512] * 12 + [6], "silu", 2.0), "bf16", k, kernel, monkeypatch) < 1e-3
     assert _err(_net([17] + [512] * 12 + [6], "silu", 1.0), "bf16", k, kernel, monkeypatch) < 1e-6
     assert _err(_net([17] + [512] * 12 + [6], "silu", 2.5), "bf16", k, kernel, monkeypatch) < 5e-2

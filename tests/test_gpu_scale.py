@@ -84,7 +84,7 @@ def test_latency_tiles_forced_on_a_large_batch(monkeypatch):
 
 
 def test_cfg5_shape_bf16_single_pass_many_tiles(monkeypatch):
-    """Single-pass BF16 on the throughput tiles (P = 4), 100k nodes, gain 2.0."""
+    """Single-pass BF16 at cfg5 scale (the rowsb kernel: A in TMEM), 100k nodes, gain 2.0."""
     err = _sampled(_net([17] + [512] * 12 + [6], "silu", 2.0), "bf16", 100352, None, monkeypatch)
     assert err < 1e-3, err
 
