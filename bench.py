@@ -278,9 +278,10 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
     L = _lib.lib()
     out, runs = {}, {}
     fl = flops_per_node(sizes, 1)
-    for name in ("bf16x3", "3xtf32", "bf16"):
+    for name in ("bf16x3", "3xtf32", "bf16", "tf32_reverse"):
         m = make_mlp(sizes, "silu", "full", SEED)
-        eng = m.engine(precision=_lib.PRECISIONS[name])
+        reverse = name == "tf32_reverse"
+        eng = m.engine(precision=_lib.PRECISIONS["tf32" if reverse else name], jacobian_mode=1 if reverse else 0)
         eng._ensure(k, 1)
         st = torch.cuda.Stream()
         raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
@@ -304,7 +305,18 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
                      "kernel": {"3xtf32": "rtn_pair_kernel<512,8,1,24,3xTF32> (four main accumulators)",
                                 "bf16x3": "rtn_pair_kernel<512,4,4,80,bf16x3>",
                                 "bf16": "rtn_rowsb_kernel<8,SiLU> (one kind::f16 pass, whole layer input as the A "
-                                        "operand in TMEM)"}[name]}
+                                        "operand in TMEM)"}.get(name, "")}
+        if reverse:  # its own FLOP basis: one value row + one adjoint row per output
+            fl_rev = fl * (1 + sizes[-1]) / (1 + sizes[0])
+            ach_rev = k * fl_rev / (ms * 1e-3) / 1e12
+            out[name].update({
+                "achieved_tflops": ach_rev, "frac_of_tf32_peak": ach_rev / tf32_peak if tf32_peak else None,
+                "hardware_frac": ach_rev / tf32_peak if tf32_peak else None,
+                "hardware_frac_basis": "reverse-mode FLOPs vs the TF32 peak",
+                "flop_per_node": fl_rev, "flops_definition": "2*(1+n_out)*sum(n_l*n_{l+1}): the value row + one "
+                                                             "adjoint row per output (the reference's reverse sweep)",
+                "kernel": "rtn_rev_kernel pass 0 (values, sigma' to an HBM scratch) + pass 1 (adjoints, J), "
+                          "split-kernel schedule; rtn_ctx_set_jacobian_mode(ctx, 1)"})
         if name == "bf16":
             try:
                 pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -577,7 +589,9 @@ def parity_leg(torch, eng_dev, z_dev, k, modes_engines, threads):
     for name, run in modes_engines.items():
         f, j = run(idx)
         e_bench = errs(f, j, f_ref, j_ref)
-        got = cm.engine(precision=_lib.PRECISIONS[name]).prepare(z_c, 1)
+        reverse = name == "tf32_reverse"
+        got = cm.engine(precision=_lib.PRECISIONS["tf32" if reverse else name],
+                        jacobian_mode=1 if reverse else 0).prepare(z_c, 1)
         e_cond = errs(got.values, got.jacobians, fc, jc)
         bound = 1e-5 if name == "3xtf32" else 1e-3
         out[name] = {"bench_inputs": e_bench, "bench_inputs_max": max(e_bench.values()),
@@ -778,7 +792,7 @@ def run_ours(args, rank, world, local_rank):
                    "value_1thread": v_one, "sample_1thread": sample1, "cpu_model": cpu_model(),
                    "algorithm": "oracle/ restatement of proj/src/neural.cpp BatchedCore (reverse mode, fp64)"}
             if modes is not None:
-                order_ = {k_: mode_runs[k_] for k_ in ("tf32", "3xtf32", "bf16x3", "bf16")}
+                order_ = {k_: mode_runs[k_] for k_ in ("tf32", "3xtf32", "bf16x3", "bf16", "tf32_reverse")}
                 parity = parity_leg(torch, eng, z, k, order_, threads)
         cfg4 = cfg4_bench(torch, tf32_peak, not args.no_cpu) if world == 1 and not args.no_modes else None
         blocks = None

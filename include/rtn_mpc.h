@@ -117,6 +117,13 @@ rtn_status rtn_ctx_synchronize(rtn_ctx* c);
  * reference's controller policy on a bad cycle (reuse the last command,
  * sqp_rti.cpp:233-267) stays with the caller. Synchronises the context stream. */
 rtn_status rtn_ctx_nonfinite(rtn_ctx* c, int* flag, int reset);
+/* Jacobian algorithm for order-1 calls: 0 = forward mode (default; one pass,
+ * 1 + n_in rows per node), 1 = reverse mode (the reference's own adjoint sweep,
+ * neural.cpp:132-163: a value pass that keeps every layer's slope in an HBM
+ * scratch, then 1 adjoint row per output: 1 + n_out rows per node). Reverse
+ * mode needs a TF32 model of padded width 512 with n_in <= 24
+ * (RTN_EUNSUPPORTED otherwise); order 0 and 2 calls are unaffected. */
+rtn_status rtn_ctx_set_jacobian_mode(rtn_ctx* c, int mode);
 
 /* Counters (EvalCounters::batched_calls / batched_points, neural.hpp:38-44)
  * and the number of device kernel launches this context has issued. */

@@ -22,7 +22,8 @@ VARIANTS = {"full": (0, 17, 6), "a": (1, 3, 3), "a_u": (2, 7, 3), "ground": (3, 
 EXPORTS = (
     "rtn_model_load_rmlp", "rtn_model_from_arrays", "rtn_model_free", "rtn_model_info", "rtn_model_digest",
     "rtn_ctx_create", "rtn_ctx_free", "rtn_prepare", "rtn_prepare_device",
-    "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_ctx_nonfinite", "rtn_last_error",
+    "rtn_ctx_set_stream", "rtn_ctx_synchronize", "rtn_ctx_counters", "rtn_ctx_nonfinite",
+    "rtn_ctx_set_jacobian_mode", "rtn_last_error",
     "rtn_build_qp", "rtn_build_qp_device", "rtn_cycle_qp", "rtn_solve_feedback",
     "rtn_comm_unique_id", "rtn_comm_create", "rtn_comm_free", "rtn_prepare_partitioned",
     "rtn_prepare_partitioned_device", "rtn_comm_bind_root_outputs", "rtn_prepare_partitioned_p2p",
@@ -110,6 +111,7 @@ def lib() -> C.CDLL:
     L.rtn_comm_free.argtypes = [_vp]
     L.rtn_comm_free.restype = None
     L.rtn_prepare_partitioned.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp]
+    L.rtn_ctx_set_jacobian_mode.argtypes = [_vp, C.c_int]
     L.rtn_comm_bind_root_outputs.argtypes = [_vp, C.c_int, _vp, _vp, C.c_longlong]
     L.rtn_prepare_partitioned_p2p.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int]
     L.rtn_ipc_export.argtypes = [_vp, C.c_char_p]

@@ -70,6 +70,12 @@ struct rtn_model {
   void* d_wt_last = nullptr;    // split x 16 rows x wp cols
   CUtensorMap tmap_h{}, tmap_l{};
   CUtensorMap tmap_h64{};  // width 512, TF32 / BF16: the same hidden pack in 64-row boxes (split / rowsb kernels)
+  // reverse mode (TF32, width 512; rtn_reverse.cuh): the hidden layers transposed
+  // (W_l^T, [k][n]) and W0' input-major zero-padded to 32 rows, both tf32-rounded
+  void* d_wt_hidden_t = nullptr;
+  float* d_w0t_pad = nullptr;
+  CUtensorMap tmap_ht64{}, tmap_w0p{};
+  bool reverse_ok = false;
   int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3 / kBF16
   // rtn_model_load_rmlp's digest-keyed cache: shared handles are reference counted
   int refs = 1;
@@ -89,6 +95,8 @@ struct rtn_model {
       cudaFree(d_wt_hidden);
       cudaFree(d_wt_last);
       cudaFree(d_bh_pair);
+      cudaFree(d_wt_hidden_t);
+      cudaFree(d_w0t_pad);
       cudaSetDevice(prev);
     }
   }
@@ -112,6 +120,9 @@ struct rtn_ctx {
   int num_sms = 148;
   unsigned long long calls = 0, points = 0, launches = 0;
   unsigned int* h_nonfinite = nullptr;  // host-mapped NaN/Inf flag the output epilogues raise
+  int jac_mode = 0;                     // 0 forward mode, 1 reverse mode (rtn_ctx_set_jacobian_mode)
+  float* d_rev_s = nullptr;             // reverse mode: σ' scratch [n_hidden][chunk][512]
+  size_t rev_s_cap = 0;                 // floats
   // end-to-end pipeline: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_k;
@@ -182,6 +193,7 @@ struct rtn_ctx {
       cudaFree(d_fb_small);
       cudaFreeHost(h_status);
       cudaFreeHost(h_nonfinite);
+      cudaFree(d_rev_s);
       cudaSetDevice(prev);
     }
   }

@@ -77,6 +77,10 @@ struct KParams {
   const double* zx;
   const double* zu;
   int zN;
+  // reverse mode (rtn_reverse.cuh): σ'_l of every node, [n_hidden][K][512] fp32,
+  // written by the value pass and read by the adjoint pass; W_L' rows (fp32)
+  float* rev_s;
+  const float* wl;
 };
 
 // Layer-0 weight row of neuron j in registers (n_in <= kMaxIn0 for every tile

@@ -62,11 +62,17 @@ cudaError_t LaunchQuadBF16(const KParams& prm, const CUtensorMap& th, const CUte
 // nodes per CTA, grid = 2 x pairs.
 cudaError_t LaunchRowsTF32(const KParams& prm, const CUtensorMap& th, const CUtensorMap& tl, int grid, cudaStream_t st);
 constexpr int kRowsMinIn = 7, kRowsMaxInHost = 31, kRowsMaxMmaHost = 11, kRbMinInHost = 15;
+constexpr int kRevMaxInHost = 24;  // reverse mode: W0' (512 x n_in) staged in shared memory
 // TF32 width-512 throughput, activations split between TMEM and shared memory
 // (rtn_split.cuh); th = the hidden pack in 64-row boxes. Same row geometry as the
 // rows kernel (7 <= n_in <= 31).
 cudaError_t LaunchSplitTF32(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,
                             cudaStream_t st);
+// Reverse mode (TF32, width 512; rtn_reverse.cuh): pass 0 = values + σ' scratch
+// (ta = hidden pack 64-row boxes, tb = output pack), pass 1 = adjoints + J
+// (ta = transposed hidden pack, tb = W0' input-major padded to 32 rows).
+cudaError_t LaunchReverse(int pass, const KParams& prm, const CUtensorMap& ta, const CUtensorMap& tb, int grid,
+                          cudaStream_t st);
 // BF16 width-512 throughput, the whole layer input as the A operand in TMEM
 // (rtn_rowsb.cuh); 15 <= n_in <= 31.
 cudaError_t LaunchRowsBF16(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,

@@ -297,6 +297,24 @@ rtn_model* UploadModel(const Packed& pk, int device) {
   m->tmap_h = MakeTmap(m->d_wt_hidden, pk.split * hid_rows, pk.pwp, 128, pk.bf16);
   m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(pk.split) * 16, pk.pwp, 8, pk.bf16);
   if (pk.pwp == 512 && pk.split == 1) m->tmap_h64 = MakeTmap(m->d_wt_hidden, hid_rows, pk.pwp, 64, pk.bf16);
+  // reverse mode (TF32, width 512): transposed hidden pack and padded input-major W0'
+  if (pk.mode == rtn::kTF32 && pk.pwp == 512 && pk.n_in <= rtn::kRevMaxInHost && pk.n_out <= rtn::kMaxOut) {
+    const int nh = std::max(pk.n_layers - 2, 1), wpp = pk.pwp;
+    std::vector<float> th(pk.th.size() / 4), tt(pk.th.size() / 4);
+    std::memcpy(th.data(), pk.th.data(), pk.th.size());
+    for (int l = 0; l < nh; ++l)
+      for (int k = 0; k < wpp; ++k)
+        for (int n = 0; n < wpp; ++n)
+          tt[(static_cast<size_t>(l) * wpp + k) * wpp + n] = th[(static_cast<size_t>(l) * wpp + n) * wpp + k];
+    std::vector<float> w0p(static_cast<size_t>(32) * wpp, 0.0f);
+    for (int i = 0; i < pk.n_in; ++i)
+      for (int n = 0; n < wpp; ++n) w0p[static_cast<size_t>(i) * wpp + n] = RoundTf32(pk.w0t[static_cast<size_t>(i) * wpp + n]);
+    up(&m->d_wt_hidden_t, tt.data(), tt.size() * 4);
+    up(reinterpret_cast<void**>(&m->d_w0t_pad), w0p.data(), w0p.size() * 4);
+    m->tmap_ht64 = MakeTmap(m->d_wt_hidden_t, hid_rows, wpp, 64, false);
+    m->tmap_w0p = MakeTmap(m->d_w0t_pad, 32, wpp, 16, false);
+    m->reverse_ok = true;
+  }
   m->lo_rows = static_cast<int>(hid_rows);
   return m.release();
 }
@@ -492,6 +510,46 @@ Kern Choose(const rtn_model* m, long long K, int num_sms) {
   return Kern::kPair;
 }
 
+// Reverse mode (rtn_reverse.cuh): per chunk of at most kRevChunk nodes, the
+// value pass (f and the σ' scratch) then the adjoint pass (J).
+constexpr long long kRevChunk = 65536;
+void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
+  const rtn_model* m = c->model;
+  const long long R = std::min(K, kRevChunk);
+  const size_t need = static_cast<size_t>(m->n_hidden) * static_cast<size_t>(R) * 512;
+  if (need > c->rev_s_cap) {
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->d_rev_s);
+    c->d_rev_s = nullptr;
+    c->rev_s_cap = 0;
+    CUDA_CHECK(cudaMalloc(&c->d_rev_s, need * sizeof(float)));
+    c->rev_s_cap = need;
+  }
+  const int n_in = m->n_in, n_out = m->n_out;
+  for (long long lo = 0; lo < K; lo += R) {
+    const long long n = std::min(R, K - lo);
+    rtn::KParams p = base;
+    p.z = base.z + lo * n_in;
+    p.f = base.f + lo * n_out;
+    p.jac = base.jac + lo * n_out * n_in;
+    p.K = n;
+    p.rev_s = c->d_rev_s;
+    p.wl = static_cast<const float*>(m->d_wt_last);
+    p.nt = 128;
+    p.P = 128;  // pass 0: one row per node
+    p.num_tiles = (n + 255) / 256;
+    int grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
+    cudaError_t e = rtn::LaunchReverse(0, p, m->tmap_h64, m->tmap_l, grid, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse value pass: ") + cudaGetErrorString(e));
+    p.P = 128 / n_out;  // pass 1: n_out adjoint rows per node
+    p.num_tiles = (n + 2 * p.P - 1) / (2 * p.P);
+    grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
+    e = rtn::LaunchReverse(1, p, m->tmap_ht64, m->tmap_w0p, grid, c->stream);
+    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse adjoint pass: ") + cudaGetErrorString(e));
+    c->launches += 2;
+  }
+}
+
 // d_zx/d_zu (optional): gather the quadrotor rows [x_k; u_k] from an iterate
 // (n_inst x (N+1) x 13 states, K x 4 inputs) instead of reading d_z.
 void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f, double* d_jac, double* d_hess,
@@ -535,6 +593,10 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     prm.trace = trace_buf;
   }
   cudaError_t e;
+  if (order == 1 && c->jac_mode == 1 && m->reverse_ok && prm.jac != nullptr && d_zx == nullptr) {
+    EnqueueReverse(c, prm, K);
+    return;
+  }
   if (order == 2) {
     // pair tiles of the node's carrier (value + tangents) plus Hessian slots
     prm.P = 1;
@@ -800,6 +862,20 @@ rtn_status rtn_ctx_synchronize(rtn_ctx* c) {
   return Guard([&] {
     if (!c) throw Error(RTN_ECONFIG, "null context");
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+rtn_status rtn_ctx_set_jacobian_mode(rtn_ctx* c, int mode) {
+  return Guard([&] {
+    if (!c) throw Error(RTN_ECONFIG, "null context");
+    if (mode != 0 && mode != 1) throw Error(RTN_ECONFIG, "jacobian mode must be 0 (forward) or 1 (reverse)");
+    if (mode == 1 && !c->model->reverse_ok)
+      throw Error(RTN_EUNSUPPORTED, "reverse mode needs a TF32 model of padded width 512 with n_in <= 24");
+    if (mode != c->jac_mode) {  // captured latency graphs hold the other mode's kernels
+      for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+      c->graphs.clear();
+    }
+    c->jac_mode = mode;
   });
 }
 

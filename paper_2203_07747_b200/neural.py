@@ -108,11 +108,12 @@ class MlpModel:
             eng.close()
         self._engines.clear()
 
-    def engine(self, device: int = 0, precision: int = _lib.RTN_TF32, latency_mode: int = 0) -> "Engine":
-        key = (device, precision, latency_mode)
+    def engine(self, device: int = 0, precision: int = _lib.RTN_TF32, latency_mode: int = 0,
+               jacobian_mode: int = 0) -> "Engine":
+        key = (device, precision, latency_mode, jacobian_mode)
         eng = self._engines.get(key)
         if eng is None:
-            eng = Engine(self, device, precision, latency_mode=latency_mode)
+            eng = Engine(self, device, precision, latency_mode=latency_mode, jacobian_mode=jacobian_mode)
             self._engines[key] = eng
         return eng
 
@@ -125,7 +126,7 @@ class Engine:
     """One packed device model plus one context (stream + workspace)."""
 
     def __init__(self, model: MlpModel, device: int = 0, precision: int = _lib.RTN_TF32,
-                 max_rows: int = 1024, latency_mode: int = 0):
+                 max_rows: int = 1024, latency_mode: int = 0, jacobian_mode: int = 0):
         model.validate()
         L = _lib.lib()
         self.model_ptr = C.c_void_p()
@@ -146,6 +147,7 @@ class Engine:
         self.max_rows = 0
         self.max_order = 1 if model.activation == "relu" else 1
         self.latency_mode = latency_mode
+        self.jacobian_mode = jacobian_mode
         self._ensure(max_rows, 1)
 
     def _ensure(self, rows: int, order: int) -> None:
@@ -159,6 +161,14 @@ class Engine:
         self.max_order = max(order, self.max_order)
         raise_for_status(L.rtn_ctx_create(self.model_ptr, self.max_rows, self.max_order, self.latency_mode,
                                           C.byref(self.ctx_ptr)))
+        if self.jacobian_mode:
+            raise_for_status(L.rtn_ctx_set_jacobian_mode(self.ctx_ptr, self.jacobian_mode))
+
+    def set_jacobian_mode(self, mode: int) -> None:
+        """0 = forward mode (default), 1 = reverse mode (rtn_ctx_set_jacobian_mode:
+        TF32 models of padded width 512 with n_in <= 24)."""
+        raise_for_status(_lib.lib().rtn_ctx_set_jacobian_mode(self.ctx_ptr, mode))
+        self.jacobian_mode = mode
 
     def prepare(self, z: np.ndarray, order: int) -> BatchEval:
         z = np.ascontiguousarray(z, dtype=np.float64)

@@ -1,7 +1,7 @@
 """cfg5-shape device time of the throughput kernel under the RTN_DEBUG isolation
 switches (rtn_pair.cuh): 0 full, 4 epilogue math/stores skipped (publish only),
 8 peer-side stores made local (DSMEM cost), 128 weight stream + MMAs only.
-Usage: RTN_DEBUG=<n> python scripts/pair_isolate.py [K]"""
+Usage: RTN_DEBUG=<n> [JMODE=1: reverse mode] python scripts/pair_isolate.py [K]"""
 import ctypes as C
 import os
 import sys
@@ -17,7 +17,7 @@ sizes = [17] + [512] * int(os.environ.get("DEPTH", "12")) + [int(os.environ.get(
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 409600
 prec = int(os.environ.get("PREC", "0"))
 m = make_mlp(sizes, "silu", "full", 12512)
-eng = m.engine(precision=prec)
+eng = m.engine(precision=prec, jacobian_mode=int(os.environ.get("JMODE", "0")))
 eng._ensure(k, 1)
 L = _lib.lib()
 z = torch.from_numpy(synth_quad_nodes(2203, k)).cuda()
