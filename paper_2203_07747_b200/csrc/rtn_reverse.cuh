@@ -31,6 +31,7 @@ namespace rtn {
 
 constexpr int kRevThreads = 320;
 constexpr int kRevMaxIn = 24;       // PASS 0 stages W0' (512 x n_in fp32) in shared memory
+constexpr int kRevStageNodes = 32;  // PASS 1 stages σ' blocks (nodes x 128 fp32, double-buffered) when NPC <= 32
 
 template <int NSTAGE>
 struct RevCfg {
@@ -229,6 +230,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
       const long long nd = node < prm.K ? node : 0;
       return prm.rev_s + (static_cast<long long>(li) * prm.K + nd) * 512;
     };
+    // PASS 1: σ'_li of the CTA's nodes for one 128-column block, staged in shared
+    // memory (the W0' area) one block ahead by cp.async — per-piece global loads
+    // left the adjoint epilogue waiting on HBM (ncu: 70% long-scoreboard stalls)
+    const int etid = threadIdx.x - 64;
+    const bool stage_sp = PASS == 1 && npc <= kRevStageNodes;
+    float* sbuf = w0s;
+    uint32_t pf = 0, pc = 0;  // σ' blocks prefetched / consumed
+    long long node0 = 0;      // the CTA's first node of the tile
+    auto sp_prefetch = [&](int li, int b) {
+      float* dst = sbuf + (pf & 1) * kRevStageNodes * 128;
+      for (int ch = etid; ch < npc * 32; ch += 256) {
+        const int pn = ch >> 5, cq = ch & 31;
+        const long long nd = node0 + pn < prm.K ? node0 + pn : 0;
+        const float* src = prm.rev_s + (static_cast<long long>(li) * prm.K + nd) * 512 + 128 * b + 4 * cq;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + pn * 128 + 4 * cq)), "l"(src)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      ++pf;
+    };
+    // the next block's σ' in flight, this block's complete and visible to every epilogue thread
+    auto sp_ready = [&](bool more, int li_next, int b_next) {
+      named_bar(3, 256);  // every thread is done with the buffer the next prefetch overwrites
+      if (more) {
+        sp_prefetch(li_next, b_next);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      named_bar(3, 256);
+    };
     // 8 accumulator columns c0.. of region reg → σ (PASS 0, σ' to the scratch) or
     // d·σ' (PASS 1), tf32; n0 = the neuron index of column c0 in the layer
     auto finish8 = [&](uint32_t reg, int c0, int n0, int li, const float* bias, float* y) {
@@ -240,7 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
         const bool st = valid && node < prm.K;
 #pragma unroll
         for (int hq = 0; hq < 2; ++hq) {  // 4 columns at a time: few live registers next to the held blocks
-          const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0 + 4 * hq));
+          const float4 b4 = *reinterpret_cast<const float4*>(bias + n0 + 4 * hq);
           const float b[4] = {b4.x, b4.y, b4.z, b4.w};
           float sp[4];
 #pragma unroll
@@ -252,10 +284,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
           if (st) *reinterpret_cast<float4*>(dst + 4 * hq) = make_float4(sp[0], sp[1], sp[2], sp[3]);
         }
       } else {
-        const float* src = srow(li) + n0;
         float sp[8];
-        *reinterpret_cast<float4*>(sp) = __ldg(reinterpret_cast<const float4*>(src));
-        *reinterpret_cast<float4*>(sp + 4) = __ldg(reinterpret_cast<const float4*>(src + 4));
+        if (stage_sp) {
+          const float* src = sbuf + (pc & 1) * kRevStageNodes * 128 + (valid ? p : 0) * 128 + c0;
+          *reinterpret_cast<float4*>(sp) = *reinterpret_cast<const float4*>(src);
+          *reinterpret_cast<float4*>(sp + 4) = *reinterpret_cast<const float4*>(src + 4);
+        } else {
+          const float* src = srow(li) + n0;
+          *reinterpret_cast<float4*>(sp) = __ldg(reinterpret_cast<const float4*>(src));
+          *reinterpret_cast<float4*>(sp + 4) = __ldg(reinterpret_cast<const float4*>(src + 4));
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = to_tf32(m[i] * sp[i]);
@@ -377,33 +415,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
     };
 
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
-      node = tile * (2 * npc) + static_cast<long long>(rank) * npc + p;
+      node0 = tile * (2 * npc) + static_cast<long long>(rank) * npc;
+      node = node0 + p;
+      if (stage_sp && n_mma > 0) sp_prefetch(n_mma - 1, 0);  // the first backward step's first block
       first_layer(tile);
       for (int l = 0; l < n_mma; ++l, ++layers) {
         // PASS 0: hidden layer l produces σ'_{l+1}; PASS 1: backward step l multiplies by σ'_{n_mma-1-l}
         const int li = PASS == 0 ? l + 1 : n_mma - 1 - l;
         const float* bias = prm.bh + l * 512;
+        if constexpr (PASS == 0) {  // the layer's biases in shared memory (zs area), by layer parity
+          float* bs = zs + (l & 1) * 512;
+          bs[etid] = __ldg(bias + etid);
+          bs[etid + 256] = __ldg(bias + etid + 256);
+          named_bar(3, 256);
+          bias = bs;
+        }
+        // PASS 1: make block b's σ' ready, prefetch the next one (the next step's block 0 after block 3)
+        auto sp_next = [&](int b) {  // block #pc uses prefetch #pc (buffer pc & 1)
+          if (!stage_sp) return;
+          const bool more = b < 3 || l + 1 < n_mma;
+          sp_ready(more, b < 3 ? li : li - 1, b < 3 ? b + 1 : 0);
+        };
         float y0[64], y1[64];
         mbar_wait_sleep(&tmem_full[0], tf_use[0]++ & 1);
         tc_fence_after();
+        sp_next(0);
         read_block(tmem_base + F0 * 128, 0, li, bias, y0);
+        ++pc;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(rf_cl);
         mbar_wait_sleep(&tmem_full[1], tf_use[1]++ & 1);
         tc_fence_after();
+        sp_next(1);
         read_block(tmem_base + F1 * 128, 1, li, bias, y1);
+        ++pc;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(rf_cl + 8);
         mbar_wait_sleep(&tmem_full[0], tf_use[0]++ & 1);
         tc_fence_after();
+        sp_next(2);
         rewrite_block(tmem_base + F0 * 128, 2, li, bias, 2);
+        ++pc;
         mbar_wait_sleep(s_free, layers & 1);
         store_s(y0, 0);
         mbar_wait_sleep(&tmem_full[1], tf_use[1]++ & 1);
         tc_fence_after();
+        sp_next(3);
         rewrite_block(tmem_base + F1 * 128, 3, li, bias, 3);
+        ++pc;
         store_s(y1, 1);
         ++prod;
         const int t0 = T0, t1 = T1;
