@@ -522,7 +522,7 @@ void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
     cudaFree(c->d_rev_s);
     c->d_rev_s = nullptr;
     c->rev_s_cap = 0;
-    CUDA_CHECK(cudaMalloc(&c->d_rev_s, need * sizeof(float)));
+    CUDA_CHECK(cudaMalloc(&c->d_rev_s, need * sizeof(uint16_t)));  // fp16 slopes
     c->rev_s_cap = need;
   }
   const int n_in = m->n_in, n_out = m->n_out;

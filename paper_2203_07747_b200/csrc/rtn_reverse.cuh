@@ -12,16 +12,21 @@
 //   PASS 0 (values): rows = nodes (128 per CTA). Layer 0 on CUDA cores (fp32,
 //     W0' staged in shared memory), hidden layers y = σ(d + b); every layer's
 //     σ'(pre) goes to an HBM scratch [n_hidden][K][512] (the reverse sweep's
-//     stored activations: 2 KB per node and layer); the output layer gives f.
+//     stored activations: 1 KB per node and layer, fp16); the output layer gives f.
 //   PASS 1 (adjoints): rows = (node, output o), n_out per node. The rows start
 //     as W_L'[o, :] ⊙ σ'_{H−1} (CUDA cores), each backward step is
 //     y[row, k] = (Σ_n G[row, n] W_l[n, k]) · σ'_{l−1}[node, k] — an MMA with
 //     the TRANSPOSED hidden pack as B — and the last one multiplies by W0'
 //     (input-major copy, zero-padded to 32 rows: N = 32) to give J[o, :].
 // Roofline: 2·(1 + n_out)·P_W FLOP per node (bench.py `reverse_mode`).
+// The slopes are stored as fp16: σ' of tanh / SiLU / ReLU lies in [-0.1, 1.1],
+// where fp16's 11 significant bits round exactly like the tf32 operands the
+// adjoint MMAs consume anyway, at half the scratch traffic (the value pass
+// spent 20% of its time on fp32 slope stores).
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "rtn_kernel.cuh"
 #include "rtn_rows.cuh"
@@ -225,26 +230,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(act_cl + 8 * (16 * (prod & 1) + c));
     };
-    // σ' row of this thread's node for layer li (PASS 1 reads, PASS 0 writes)
-    auto srow = [&](int li) -> float* {
+    // σ' row (fp16) of this thread's node for layer li (PASS 1 reads, PASS 0 writes)
+    uint16_t* const rs = reinterpret_cast<uint16_t*>(prm.rev_s);
+    auto srow = [&](int li) -> uint16_t* {
       const long long nd = node < prm.K ? node : 0;
-      return prm.rev_s + (static_cast<long long>(li) * prm.K + nd) * 512;
+      return rs + (static_cast<long long>(li) * prm.K + nd) * 512;
+    };
+    auto pack8 = [](const float* v) {  // 8 floats → 8 fp16 (16 bytes)
+      uint4 u;
+      __half2 h;
+      h = __floats2half2_rn(v[0], v[1]);
+      u.x = *reinterpret_cast<uint32_t*>(&h);
+      h = __floats2half2_rn(v[2], v[3]);
+      u.y = *reinterpret_cast<uint32_t*>(&h);
+      h = __floats2half2_rn(v[4], v[5]);
+      u.z = *reinterpret_cast<uint32_t*>(&h);
+      h = __floats2half2_rn(v[6], v[7]);
+      u.w = *reinterpret_cast<uint32_t*>(&h);
+      return u;
+    };
+    auto unpack8 = [](uint4 u, float* v) {
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(*reinterpret_cast<__half2*>(&w[i]));
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+      }
     };
     // PASS 1: σ'_li of the CTA's nodes for one 128-column block, staged in shared
     // memory (the W0' area) one block ahead by cp.async — per-piece global loads
     // left the adjoint epilogue waiting on HBM (ncu: 70% long-scoreboard stalls)
     const int etid = threadIdx.x - 64;
     const bool stage_sp = PASS == 1 && npc <= kRevStageNodes;
-    float* sbuf = w0s;
+    uint16_t* sbuf = reinterpret_cast<uint16_t*>(w0s);
     uint32_t pf = 0, pc = 0;  // σ' blocks prefetched / consumed
     long long node0 = 0;      // the CTA's first node of the tile
     auto sp_prefetch = [&](int li, int b) {
-      float* dst = sbuf + (pf & 1) * kRevStageNodes * 128;
-      for (int ch = etid; ch < npc * 32; ch += 256) {
-        const int pn = ch >> 5, cq = ch & 31;
+      uint16_t* dst = sbuf + (pf & 1) * kRevStageNodes * 128;
+      for (int ch = etid; ch < npc * 16; ch += 256) {  // 16-byte pieces: 8 slopes
+        const int pn = ch >> 4, cq = ch & 15;
         const long long nd = node0 + pn < prm.K ? node0 + pn : 0;
-        const float* src = prm.rev_s + (static_cast<long long>(li) * prm.K + nd) * 512 + 128 * b + 4 * cq;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + pn * 128 + 4 * cq)), "l"(src)
+        const uint16_t* src = rs + (static_cast<long long>(li) * prm.K + nd) * 512 + 128 * b + 8 * cq;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + pn * 128 + 8 * cq)), "l"(src)
                      : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -268,32 +296,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
       tmem_ld8(reg + lane_base + c0, m);
       if constexpr (PASS == 0) {
         tmem_ld_wait();
-        float* dst = srow(li) + n0;
-        const bool st = valid && node < prm.K;
+        const bool st = valid && node < prm.K && !(prm.dbg & 2);  // dbg 2: no slope stores (timing only)
+        float spv[8];
 #pragma unroll
         for (int hq = 0; hq < 2; ++hq) {  // 4 columns at a time: few live registers next to the held blocks
           const float4 b4 = *reinterpret_cast<const float4*>(bias + n0 + 4 * hq);
           const float b[4] = {b4.x, b4.y, b4.z, b4.w};
-          float sp[4];
+          float* sp = spv + 4 * hq;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             float val;
-            act_rows<ACT>(m[4 * hq + i] + b[i], val, sp[i]);
+            if (prm.dbg & 4) {  // dbg 4: no activation math (timing only)
+              val = m[4 * hq + i] + b[i];
+              sp[i] = val;
+            } else {
+              act_rows<ACT>(m[4 * hq + i] + b[i], val, sp[i]);
+            }
             y[4 * hq + i] = to_tf32(val);
           }
-          if (st) *reinterpret_cast<float4*>(dst + 4 * hq) = make_float4(sp[0], sp[1], sp[2], sp[3]);
         }
+        if (st) *reinterpret_cast<uint4*>(srow(li) + n0) = pack8(spv);
       } else {
         float sp[8];
-        if (stage_sp) {
-          const float* src = sbuf + (pc & 1) * kRevStageNodes * 128 + (valid ? p : 0) * 128 + c0;
-          *reinterpret_cast<float4*>(sp) = *reinterpret_cast<const float4*>(src);
-          *reinterpret_cast<float4*>(sp + 4) = *reinterpret_cast<const float4*>(src + 4);
-        } else {
-          const float* src = srow(li) + n0;
-          *reinterpret_cast<float4*>(sp) = __ldg(reinterpret_cast<const float4*>(src));
-          *reinterpret_cast<float4*>(sp + 4) = __ldg(reinterpret_cast<const float4*>(src + 4));
-        }
+        if (stage_sp)
+          unpack8(*reinterpret_cast<const uint4*>(sbuf + (pc & 1) * kRevStageNodes * 128 + (valid ? p : 0) * 128 + c0), sp);
+        else
+          unpack8(__ldg(reinterpret_cast<const uint4*>(srow(li) + n0)), sp);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = to_tf32(m[i] * sp[i]);
@@ -380,16 +408,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
               y[i] = to_tf32(val);
             }
             if (valid && node < prm.K) {
-              float* dst = srow(0) + n0;
-#pragma unroll
-              for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = *reinterpret_cast<const float4*>(sp + i);
+              uint16_t* dst = srow(0) + n0;
+              *reinterpret_cast<uint4*>(dst) = pack8(sp);
+              *reinterpret_cast<uint4*>(dst + 8) = pack8(sp + 8);
             }
             put16(y, q, c);
           }
         }
       } else {
         // adjoint rows W_L'[o, :] ⊙ σ'_{H-1} (the last hidden layer's slopes)
-        const float* src = srow(n_mma);
+        const uint16_t* src = srow(n_mma);
         const float* wlr = prm.wl + (o < n_out ? o : 0) * 512;
 #pragma unroll 1
         for (int qi = 0; qi < 4; ++qi) {
@@ -397,15 +425,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRevThreads, 1)
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             const int n0 = 128 * q + 32 * c + 16 * h;
-            float y[16];
+            float y[16], sv[16];
+            unpack8(__ldg(reinterpret_cast<const uint4*>(src + n0)), sv);
+            unpack8(__ldg(reinterpret_cast<const uint4*>(src + n0 + 8)), sv + 8);
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
-              const float4 s4 = __ldg(reinterpret_cast<const float4*>(src + n0 + i));
               const float4 w4 = __ldg(reinterpret_cast<const float4*>(wlr + n0 + i));
-              y[i] = to_tf32(s4.x * w4.x);
-              y[i + 1] = to_tf32(s4.y * w4.y);
-              y[i + 2] = to_tf32(s4.z * w4.z);
-              y[i + 3] = to_tf32(s4.w * w4.w);
+              y[i] = to_tf32(sv[i] * w4.x);
+              y[i + 1] = to_tf32(sv[i + 1] * w4.y);
+              y[i + 2] = to_tf32(sv[i + 2] * w4.z);
+              y[i + 3] = to_tf32(sv[i + 3] * w4.w);
             }
             put16(y, q, c);
           }
