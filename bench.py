@@ -860,13 +860,14 @@ def latency_suite(torch, tf32_peak, with_cpu):
     each beside the reference's CPU path on this host (oracle BatchedCore: 1
     thread and all threads, CPU model stated)."""
     threads = os.cpu_count() or 1
-    cases = [("cfg3_12x512_N20", SIZES, SEED, 20, 1, 0, "silu", 1000),
-             ("cfg3_12x512_N20_order2", SIZES, SEED, 20, 2, 0, "silu", 300),
-             ("cfg3_12x512_N20_bf16x3", SIZES, SEED, 20, 1, 2, "silu", 300),
-             ("cfg3_12x512_N20_3xtf32", SIZES, SEED, 20, 1, 1, "silu", 300),
-             ("cfg3_12x512_N20_bf16", SIZES, SEED, 20, 1, 3, "silu", 300),
-             ("cfg2_5x256_N20", [17] + [256] * 5 + [6], 5256, 20, 1, 0, "silu", 1000),
-             ("cfg1_2x64_N10", [17, 64, 64, 6], 2064, 10, 1, 0, "tanh", 1000)]
+    from paper_2203_07747_b200._lib import PRECISIONS as P
+    cases = [("cfg3_12x512_N20", SIZES, SEED, 20, 1, P["tf32"], "silu", 1000),
+             ("cfg3_12x512_N20_order2", SIZES, SEED, 20, 2, P["tf32"], "silu", 300),
+             ("cfg3_12x512_N20_bf16x3", SIZES, SEED, 20, 1, P["bf16x3"], "silu", 300),
+             ("cfg3_12x512_N20_3xtf32", SIZES, SEED, 20, 1, P["3xtf32"], "silu", 300),
+             ("cfg3_12x512_N20_bf16", SIZES, SEED, 20, 1, P["bf16"], "silu", 300),
+             ("cfg2_5x256_N20", [17] + [256] * 5 + [6], 5256, 20, 1, P["tf32"], "silu", 1000),
+             ("cfg1_2x64_N10", [17, 64, 64, 6], 2064, 10, 1, P["tf32"], "tanh", 1000)]
     out = {}
     for name, sizes, seed, k, order, prec, act, steps in cases:
         out[name] = latency(torch, sizes, seed, k, steps=steps, order=order, precision=prec, act=act,

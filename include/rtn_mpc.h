@@ -54,8 +54,9 @@ typedef enum {
 typedef enum {
   RTN_TF32 = 0,   /* one tcgen05 kind::tf32 pass, fp32 accumulate               */
   RTN_3XTF32 = 1, /* tf32 hi/lo split operands, 3 kind::tf32 passes (1e-5 class) */
-  RTN_BF16X3 = 2, /* bf16 hi/lo split operands, 3 kind::f16 passes (1e-4 class) */
-  RTN_BF16 = 3    /* one kind::f16 pass on bf16 operands: 2x the tf32 MMA rate, ~8x its error */
+  RTN_BF16 = 2,   /* one kind::f16 pass on bf16 operands: 2x the tf32 MMA rate, ~8x its error
+                     (SURVEY.md §8b's RTN_BF16) */
+  RTN_BF16X3 = 3  /* bf16 hi/lo split operands, 3 kind::f16 passes (1e-4 class) */
 } rtn_precision;
 
 typedef enum { RTN_ACT_TANH = 0, RTN_ACT_RELU = 1, RTN_ACT_SILU = 2 } rtn_activation;

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RTN_LIB", os.path.join(_HERE, "librtn_mpc.so"))
 
 RTN_OK, RTN_ECONFIG, RTN_EDOMAIN, RTN_EUNSUPPORTED, RTN_ECUDA, RTN_ENCCL, RTN_ERUNTIME = range(7)
-RTN_TF32, RTN_3XTF32, RTN_BF16X3, RTN_BF16 = range(4)
+RTN_TF32, RTN_3XTF32, RTN_BF16, RTN_BF16X3 = range(4)  # include/rtn_mpc.h rtn_precision
 PRECISIONS = {"tf32": RTN_TF32, "3xtf32": RTN_3XTF32, "bf16x3": RTN_BF16X3, "bf16": RTN_BF16}
 # rtn_variant codes and (n_f, n_r) per residual variant (dynamics.hpp:95-131)
 VARIANTS = {"full": (0, 17, 6), "a": (1, 3, 3), "a_u": (2, 7, 3), "ground": (3, 26, 3)}

@@ -14,7 +14,7 @@ from paper_2203_07747_b200.errors import raise_for_status  # noqa: E402
 
 width, depth, act, k = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], int(sys.argv[4])
 launches = int(sys.argv[5]) if len(sys.argv) > 5 else 2
-prec = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+prec = (_lib.PRECISIONS.get(sys.argv[6]) if sys.argv[6] in _lib.PRECISIONS else int(sys.argv[6])) if len(sys.argv) > 6 else 0
 sizes = [17] + [width] * depth + [6]
 m = make_mlp(sizes, act, "full", 1000 * depth + width)
 eng = m.engine(precision=prec)

@@ -15,7 +15,8 @@ from paper_2203_07747_b200.errors import raise_for_status  # noqa: E402
 
 sizes = [17] + [512] * int(os.environ.get("DEPTH", "12")) + [int(os.environ.get("NOUT", "6"))]
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 409600
-prec = int(os.environ.get("PREC", "0"))
+prec = _lib.PRECISIONS.get(os.environ.get("PREC", "tf32"), None)
+prec = int(os.environ.get("PREC")) if prec is None else prec  # a name (tf32, bf16, ...) or the enum value
 m = make_mlp(sizes, "silu", "full", 12512)
 eng = m.engine(precision=prec, jacobian_mode=int(os.environ.get("JMODE", "0")))
 eng._ensure(k, 1)

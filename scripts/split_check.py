@@ -30,7 +30,7 @@ for l, (w, b) in enumerate(om.layers()):
     if l < len(om.layers()) - 1:
         om.set_layer(l, w * float(os.environ.get("GAIN", "2.0")), b)
 z = oracle.quad_nodes(3, k)
-got = oracle.to_product_model(om).engine(precision=int(os.environ.get("PREC", "0"))).prepare(z, 1)
+got = oracle.to_product_model(om).engine(precision=_lib.PRECISIONS.get(os.environ.get("PREC", "tf32"), None) or int(os.environ.get("PREC", "0"))).prepare(z, 1)
 idx = np.arange(0, k, 7)
 f, j, _ = om.batched_eval(z[idx], 1)
 print(os.environ["RTN_KERNEL"], "max err f", oracle.max_node_rel_error(got.values[idx], f), "J",
