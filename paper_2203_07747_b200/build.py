@@ -23,7 +23,7 @@ NVCC_FLAGS = [
 ]
 
 SOURCES = ["rtn_mpc.cu", "rtn_comm.cu", "rtn_pair_tf32.cu", "rtn_pair_3xtf32.cu", "rtn_pair_bf16x3.cu", "rtn_pair_bf16.cu", "rtn_pair_order2.cu",
-           "rtn_split.cu", "rtn_blocks.cu", "rtn_qpsolve.cu", "rtn_synth.cpp"]
+           "rtn_split.cu", "rtn_pair_rev.cu", "rtn_blocks.cu", "rtn_qpsolve.cu", "rtn_synth.cpp"]
 HEADERS = ["rtn_kernel.cuh", "rtn_pair.cuh", "rtn_pair_launch.cuh", "rtn_launch.h", "rtn_blocks.h", "rtn_quad.cuh",
            "rtn_qpsolve.h", "rtn_rows.cuh", "rtn_split.cuh", "rtn_rowsb.cuh", "rtn_reverse.cuh", "rtn_internal.h"]
 DEPS = SOURCES + HEADERS

@@ -73,9 +73,11 @@ struct rtn_model {
   // reverse mode (TF32, width 512; rtn_reverse.cuh): the hidden layers transposed
   // (W_l^T, [k][n]) and W0' input-major zero-padded to 32 rows, both tf32-rounded
   void* d_wt_hidden_t = nullptr;
-  float* d_w0t_pad = nullptr;
-  CUtensorMap tmap_ht64{}, tmap_w0p{};
-  bool reverse_ok = false;
+  void* d_w0t_pad = nullptr;
+  float* d_wl32 = nullptr;  // W_L' (fp32: the output pack's hi + lo)
+  CUtensorMap tmap_ht64{}, tmap_ht{}, tmap_w0p{};
+  bool reverse_ok = false;       // TF32 width 512: split-schedule reverse kernels
+  bool reverse_pair_ok = false;  // other modes / width 256: pair-kernel reverse variants
   int pair_mode = 0;   // rtn::kTF32 / k3xTF32 / kBF16x3 / kBF16
   // rtn_model_load_rmlp's digest-keyed cache: shared handles are reference counted
   int refs = 1;
@@ -97,6 +99,7 @@ struct rtn_model {
       cudaFree(d_bh_pair);
       cudaFree(d_wt_hidden_t);
       cudaFree(d_w0t_pad);
+      cudaFree(d_wl32);
       cudaSetDevice(prev);
     }
   }

@@ -73,6 +73,12 @@ cudaError_t LaunchSplitTF32(const KParams& prm, const CUtensorMap& th64, const C
 // (ta = transposed hidden pack, tb = W0' input-major padded to 32 rows).
 cudaError_t LaunchReverse(int pass, const KParams& prm, const CUtensorMap& ta, const CUtensorMap& tb, int grid,
                           cudaStream_t st);
+// Reverse mode on the pair kernel (3xTF32 / bf16x3, width 256 or 512; rtn_pair.cuh
+// variants 3 = values, 4 = adjoints): th = hidden pack (pass 0) or its transpose
+// (pass 1), tl = output pack (pass 0) or W0' padded to 32 rows (pass 1).
+cudaError_t LaunchPairReverse(int mode, int wp, int pass, const KParams& prm, const CUtensorMap& th,
+                              const CUtensorMap& tl, int grid, cudaStream_t st);
+inline int PairReverseNtc(int mode, int wp) { return (mode == k3xTF32 && wp == 512) ? 24 : 80; }
 // BF16 width-512 throughput, the whole layer input as the A operand in TMEM
 // (rtn_rowsb.cuh); 15 <= n_in <= 31.
 cudaError_t LaunchRowsBF16(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,

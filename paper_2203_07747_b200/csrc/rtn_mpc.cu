@@ -297,23 +297,67 @@ rtn_model* UploadModel(const Packed& pk, int device) {
   m->tmap_h = MakeTmap(m->d_wt_hidden, pk.split * hid_rows, pk.pwp, 128, pk.bf16);
   m->tmap_l = MakeTmap(m->d_wt_last, static_cast<uint64_t>(pk.split) * 16, pk.pwp, 8, pk.bf16);
   if (pk.pwp == 512 && pk.split == 1) m->tmap_h64 = MakeTmap(m->d_wt_hidden, hid_rows, pk.pwp, 64, pk.bf16);
-  // reverse mode (TF32, width 512): transposed hidden pack and padded input-major W0'
-  if (pk.mode == rtn::kTF32 && pk.pwp == 512 && pk.n_in <= rtn::kRevMaxInHost && pk.n_out <= rtn::kMaxOut) {
-    const int nh = std::max(pk.n_layers - 2, 1), wpp = pk.pwp;
-    std::vector<float> th(pk.th.size() / 4), tt(pk.th.size() / 4);
-    std::memcpy(th.data(), pk.th.data(), pk.th.size());
-    for (int l = 0; l < nh; ++l)
-      for (int k = 0; k < wpp; ++k)
-        for (int n = 0; n < wpp; ++n)
-          tt[(static_cast<size_t>(l) * wpp + k) * wpp + n] = th[(static_cast<size_t>(l) * wpp + n) * wpp + k];
-    std::vector<float> w0p(static_cast<size_t>(32) * wpp, 0.0f);
+  // reverse mode (rtn_ctx_set_jacobian_mode): the hidden packs transposed (W_l^T,
+  // [k][n], per split half, in the mode's element type), W0' input-major padded
+  // to 32 rows as the J output pack ([hi; lo] in the split modes), and W_L' in
+  // fp32 (the pack's hi + lo) for the adjoint rows' start. TF32 width 512 runs
+  // on the split-schedule kernels (64-row boxes); every other mode of width 256
+  // or 512 on the pair kernel's reverse variants (quadrotor outputs: n_out = 6).
+  if ((pk.pwp == 512 || pk.pwp == 256) && pk.n_in <= rtn::kRevMaxInHost && pk.n_in <= rtn::kMaxIn2 &&
+      pk.n_layers >= 2) {
+    const int nh = std::max(pk.n_layers - 2, 1), wpp = pk.pwp, eb = pk.bf16 ? 2 : 4, sp = pk.split;
+    std::vector<uint8_t> tt(pk.th.size());
+    for (int h = 0; h < sp; ++h)
+      for (int l = 0; l < nh; ++l) {
+        const size_t blk = (static_cast<size_t>(h) * nh + l) * wpp;  // first row of layer l in split half h
+        for (int k = 0; k < wpp; ++k)
+          for (int n = 0; n < wpp; ++n)
+            std::memcpy(&tt[((blk + k) * wpp + n) * eb], &pk.th[((blk + n) * wpp + k) * eb], eb);
+      }
+    std::vector<uint8_t> w0p(static_cast<size_t>(sp) * 32 * wpp * eb, 0);
     for (int i = 0; i < pk.n_in; ++i)
-      for (int n = 0; n < wpp; ++n) w0p[static_cast<size_t>(i) * wpp + n] = RoundTf32(pk.w0t[static_cast<size_t>(i) * wpp + n]);
-    up(&m->d_wt_hidden_t, tt.data(), tt.size() * 4);
-    up(reinterpret_cast<void**>(&m->d_w0t_pad), w0p.data(), w0p.size() * 4);
-    m->tmap_ht64 = MakeTmap(m->d_wt_hidden_t, hid_rows, wpp, 64, false);
-    m->tmap_w0p = MakeTmap(m->d_w0t_pad, 32, wpp, 16, false);
-    m->reverse_ok = true;
+      for (int n = 0; n < wpp; ++n) {
+        const float w = pk.w0t[static_cast<size_t>(i) * wpp + n];
+        const float hi = pk.bf16 ? RoundBf16(w) : RoundTf32(w);
+        const float lo = pk.bf16 ? RoundBf16(w - hi) : RoundTf32(w - hi);
+        for (int h = 0; h < sp; ++h) {
+          const float v = h == 0 ? hi : lo;
+          uint8_t* dst = &w0p[((static_cast<size_t>(h) * 32 + i) * wpp + n) * eb];
+          if (pk.bf16) {
+            const uint16_t b = Bf16Bits(v);
+            std::memcpy(dst, &b, 2);
+          } else {
+            std::memcpy(dst, &v, 4);
+          }
+        }
+      }
+    std::vector<float> wl(static_cast<size_t>(rtn::kMaxOut) * wpp, 0.0f);
+    for (int o = 0; o < rtn::kMaxOut; ++o)
+      for (int n = 0; n < wpp; ++n)
+        for (int h = 0; h < sp; ++h) {
+          const size_t idx = (static_cast<size_t>(h) * 16 + o) * wpp + n;
+          float v;
+          if (pk.bf16) {
+            uint16_t b;
+            std::memcpy(&b, &pk.tl[idx * 2], 2);
+            const uint32_t u = static_cast<uint32_t>(b) << 16;
+            std::memcpy(&v, &u, 4);
+          } else {
+            std::memcpy(&v, &pk.tl[idx * 4], 4);
+          }
+          wl[static_cast<size_t>(o) * wpp + n] += v;
+        }
+    up(&m->d_wt_hidden_t, tt.data(), tt.size());
+    up(reinterpret_cast<void**>(&m->d_w0t_pad), w0p.data(), w0p.size());
+    up(reinterpret_cast<void**>(&m->d_wl32), wl.data(), wl.size() * 4);
+    m->tmap_ht = MakeTmap(m->d_wt_hidden_t, sp * hid_rows, wpp, 128, pk.bf16);
+    m->tmap_w0p = MakeTmap(m->d_w0t_pad, static_cast<uint64_t>(sp) * 32, wpp, 16, pk.bf16);
+    if (pk.mode == rtn::kTF32 && wpp == 512) {
+      m->tmap_ht64 = MakeTmap(m->d_wt_hidden_t, hid_rows, wpp, 64, false);
+      m->reverse_ok = true;  // split-schedule kernels (rtn_reverse.cuh)
+    } else if (pk.n_out == 6 && rtn::IsSplitMode(pk.mode)) {
+      m->reverse_pair_ok = true;  // pair-kernel variants (rtn_pair.cuh ORD2 = 3, 4)
+    }
   }
   m->lo_rows = static_cast<int>(hid_rows);
   return m.release();
@@ -515,17 +559,20 @@ Kern Choose(const rtn_model* m, long long K, int num_sms) {
 constexpr long long kRevChunk = 65536;
 void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
   const rtn_model* m = c->model;
+  const bool split_sched = m->reverse_ok;  // TF32 width 512; else the pair-kernel variants
   const long long R = std::min(K, kRevChunk);
-  const size_t need = static_cast<size_t>(m->n_hidden) * static_cast<size_t>(R) * 512;
+  // scratch: fp16 slopes (split schedule) / fp32 slopes (pair variants: the split-precision modes)
+  const size_t need = static_cast<size_t>(m->n_hidden) * static_cast<size_t>(R) * m->pair_wp * (split_sched ? 2 : 4);
   if (need > c->rev_s_cap) {
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
     cudaFree(c->d_rev_s);
     c->d_rev_s = nullptr;
     c->rev_s_cap = 0;
-    CUDA_CHECK(cudaMalloc(&c->d_rev_s, need * sizeof(uint16_t)));  // fp16 slopes
+    CUDA_CHECK(cudaMalloc(&c->d_rev_s, need));
     c->rev_s_cap = need;
   }
   const int n_in = m->n_in, n_out = m->n_out;
+  const int ntc = rtn::PairReverseNtc(m->pair_mode, m->pair_wp);
   for (long long lo = 0; lo < K; lo += R) {
     const long long n = std::min(R, K - lo);
     rtn::KParams p = base;
@@ -534,18 +581,35 @@ void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
     p.jac = base.jac + lo * n_out * n_in;
     p.K = n;
     p.rev_s = c->d_rev_s;
-    p.wl = static_cast<const float*>(m->d_wt_last);
-    p.nt = 128;
-    p.P = 128;  // pass 0: one row per node
-    p.num_tiles = (n + 255) / 256;
-    int grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
-    cudaError_t e = rtn::LaunchReverse(0, p, m->tmap_h64, m->tmap_l, grid, c->stream);
-    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse value pass: ") + cudaGetErrorString(e));
-    p.P = 128 / n_out;  // pass 1: n_out adjoint rows per node
-    p.num_tiles = (n + 2 * p.P - 1) / (2 * p.P);
-    grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
-    e = rtn::LaunchReverse(1, p, m->tmap_ht64, m->tmap_w0p, grid, c->stream);
-    if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse adjoint pass: ") + cudaGetErrorString(e));
+    p.wl = m->d_wl32;
+    cudaError_t e;
+    if (split_sched) {
+      p.nt = 128;
+      p.P = 128;  // pass 0: one row per node
+      p.num_tiles = (n + 255) / 256;
+      int grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
+      e = rtn::LaunchReverse(0, p, m->tmap_h64, m->tmap_l, grid, c->stream);
+      if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse value pass: ") + cudaGetErrorString(e));
+      p.P = 128 / n_out;  // pass 1: n_out adjoint rows per node
+      p.num_tiles = (n + 2 * p.P - 1) / (2 * p.P);
+      grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
+      e = rtn::LaunchReverse(1, p, m->tmap_ht64, m->tmap_w0p, grid, c->stream);
+      if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse adjoint pass: ") + cudaGetErrorString(e));
+    } else {
+      p.lo_rows = m->lo_rows;
+      p.P = ntc;  // pass 0: one row per node, ntc nodes per CTA side
+      p.nt = ntc;
+      p.num_tiles = (n + 2 * ntc - 1) / (2 * ntc);
+      int grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
+      e = rtn::LaunchPairReverse(m->pair_mode, m->pair_wp, 0, p, m->tmap_h, m->tmap_l, grid, c->stream);
+      if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse value pass: ") + cudaGetErrorString(e));
+      p.P = ntc / 6;  // pass 1: 6 adjoint rows per node
+      p.nt = ((p.P * 6 + 7) / 8) * 8;
+      p.num_tiles = (n + 2 * p.P - 1) / (2 * p.P);
+      grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
+      e = rtn::LaunchPairReverse(m->pair_mode, m->pair_wp, 1, p, m->tmap_ht, m->tmap_w0p, grid, c->stream);
+      if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse adjoint pass: ") + cudaGetErrorString(e));
+    }
     c->launches += 2;
   }
 }
@@ -593,7 +657,8 @@ void Enqueue(rtn_ctx* c, const double* d_z, long long K, int order, double* d_f,
     prm.trace = trace_buf;
   }
   cudaError_t e;
-  if (order == 1 && c->jac_mode == 1 && m->reverse_ok && prm.jac != nullptr && d_zx == nullptr) {
+  if (order == 1 && c->jac_mode == 1 && (m->reverse_ok || m->reverse_pair_ok) && prm.jac != nullptr &&
+      d_zx == nullptr) {
     EnqueueReverse(c, prm, K);
     return;
   }
@@ -869,8 +934,10 @@ rtn_status rtn_ctx_set_jacobian_mode(rtn_ctx* c, int mode) {
   return Guard([&] {
     if (!c) throw Error(RTN_ECONFIG, "null context");
     if (mode != 0 && mode != 1) throw Error(RTN_ECONFIG, "jacobian mode must be 0 (forward) or 1 (reverse)");
-    if (mode == 1 && !c->model->reverse_ok)
-      throw Error(RTN_EUNSUPPORTED, "reverse mode needs a TF32 model of padded width 512 with n_in <= 24");
+    if (mode == 1 && !c->model->reverse_ok && !c->model->reverse_pair_ok)
+      throw Error(RTN_EUNSUPPORTED,
+                  "reverse mode needs n_in <= 24 and a TF32 model of padded width 512, or a 3xTF32 / bf16x3 model "
+                  "of padded width 256 or 512 with 6 outputs");
     if (mode != c->jac_mode) {  // captured latency graphs hold the other mode's kernels
       for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
       c->graphs.clear();

@@ -27,6 +27,10 @@
 // per chain), the small hi·lo + lo·hi corrections go to their own accumulator,
 // and the epilogue adds them once in fp32: D0 + ((D1 + D2 + D3) + Dcorr).
 //
+// Variant (ORD2): 0 = order 1; 1, 2 = order 2 (below); 3, 4 = the value and
+// adjoint passes of reverse mode (the reference's own algorithm: rtn_reverse.cuh
+// describes it; here for the split-precision and BF16 modes, whose operands do
+// not fit the split kernel's TMEM/shared-memory layout).
 // Order 2 (ORD2): 1 = quadrotor tiles (n_in = 17, compile-time Hessian slot
 // tables, NTC = 48); 2 = generic tiles for any n_in <= 31 (runtime slot table
 // in shared memory). Both carry the node's value + tangent rows (the
@@ -102,7 +106,8 @@ struct PairCfg {
   static_assert(kNMB >= 1 && kNMB <= 2, "pair kernel handles 256 or 512 padded width");
   static_assert(kN % 16 == 0 && kN <= 256, "pair MMA N");
   static_assert((kChains + (kCorr ? 1 : 0)) * kN <= kBlkCols, "TMEM capacity");
-  static_assert(5 * 16 <= kBlkCols, "output-layer accumulators");
+  static constexpr int kOutN = ORD2 == 4 ? 32 : kMaxOut;  // output MMA N (reverse adjoint pass: J over 32 inputs)
+  static_assert((kChains + (kCorr ? 1 : 0)) * kOutN <= kBlkCols, "output-layer accumulators");
   static_assert(kSmemBytes <= 232448, "shared memory budget");
   static_assert(kStagesPerMB % NSTAGE == 0, "every 256-block starts at stage 0 (static stage indices)");
   // the output layer's M = 128-row A reads run past the last chunk into the stage ring
@@ -253,7 +258,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (long long tile = pair; tile < prm.num_tiles; tile += npairs) {
       for (int l = 0; l < n_mma_layers; ++l)
         for (int mb = 0; mb < NMB; ++mb) {
-          const int y = l * WP + mb * 256 + yr;
+          const int wl = ORD2 == 4 ? n_mma_layers - 1 - l : l;  // the adjoint pass walks the layers backwards
+          const int y = wl * WP + mb * 256 + yr;
 #pragma unroll
           for (int i = 0; i < NKC * SPLIT; ++i) {
             const int c = i / SPLIT, sp = i % SPLIT, st = i % NSTAGE;
@@ -267,9 +273,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < NKC * SPLIT; ++i) {
         const int c = i / SPLIT, sp = i % SPLIT, st = i % NSTAGE;
         mbar_wait(&empty[st], ph ^ 1);
-        if (leader) mbar_expect_tx_elect(&full[st], 2 * kLastHalfBytes);
-        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * C::kCK, sp * 16 + static_cast<int>(rank) * 8, &full[st],
-                     pol);
+        if (leader) mbar_expect_tx_elect(&full[st], 2 * (C::kOutN / 2) * 128);
+        tma_load_2sm(stage_s + st * kStageBytes, &tmap_l, c * C::kCK, sp * C::kOutN + static_cast<int>(rank) * (C::kOutN / 2),
+                     &full[st], pol);
         if (st == NSTAGE - 1) ph ^= 1;
       }
     }
@@ -277,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================== pair MMA issuer (leader CTA) ======================
     if (leader) {
       const uint32_t idesc_h = IsBf16Mode(MODE) ? idesc_bf16(256, 2 * ntc) : idesc_tf32(256, 2 * ntc);
-      const uint32_t idesc_o = IsBf16Mode(MODE) ? idesc_bf16(256, kMaxOut) : idesc_tf32(256, kMaxOut);
+      const uint32_t idesc_o = IsBf16Mode(MODE) ? idesc_bf16(256, C::kOutN) : idesc_tf32(256, C::kOutN);
       // descriptors advance by (bytes >> 4) in the start-address field
       const uint64_t a0 = sw128_desc(smem_u32(stage_s));
       const uint64_t b0 = sw128_desc(smem_u32(act_s));
@@ -366,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full[st0], ph);
           if constexpr (SPLIT == 2) mbar_wait(&full[st1], ph);
           tc_fence_after();
-          chunk_mma(tmem_base + (c % C::kChains) * 16, C::kCorr ? tmem_base + 16 * C::kChains : tmem_base,
+          chunk_mma(tmem_base + (c % C::kChains) * C::kOutN, C::kCorr ? tmem_base + C::kOutN * C::kChains : tmem_base,
                     a0 + st0 * kStageD, a0 + st1 * kStageD, st0, st1, b0 + c * kChunkD, b0 + kSplitD + c * kChunkD,
                     idesc_o, chain_acc(c), 0u, false);
           if (st1 == NSTAGE - 1) ph ^= 1;
@@ -722,6 +728,164 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+    }
+   } else if constexpr (ORD2 >= 3) {
+    // ===================== reverse mode: value (3) / adjoint (4) pass ========
+    // Rows: value pass = nodes (pn = prm.P per side); adjoint pass = node-major
+    // (node, output o) rows, kRevOut = 6 outputs (the quadrotor residual; the
+    // host refuses other n_out), pn nodes x 6 rows per side. Slopes σ'_l of
+    // every node go to / come from prm.rev_s, [n_hidden][K][WP] fp32 (thread =
+    // neuron: a warp's 32 neurons of one node are one 128-byte line).
+    constexpr bool kAdj = ORD2 == 4;
+    constexpr int kRevOut = 6;
+    constexpr int kAdjNodes = (NTC + kRevOut - 1) / kRevOut;  // adjoint pass: the side's nodes
+    const int n_out = prm.n_out, pn = prm.P;
+    const int rows_used = kAdj ? pn * kRevOut : pn;
+    const long long K = prm.K;
+    const int n_mma = n_mma_layers;
+    float* const rs = prm.rev_s;
+    auto slope = [&](int li, long long node, int j) -> float* { return rs + (static_cast<long long>(li) * K + node) * WP + j; };
+    constexpr int kG0 = NG / 2;
+    // first production of a tile: value pass = layer 0 (CUDA cores, fp32; z from
+    // global, read by every thread: L1 broadcasts), adjoint pass = W_L'[o, j]·σ'_H;
+    // each CTA writes every K-group for its OWN side's rows (local stores only)
+    // one element (row i of neuron column j) into this CTA's operand buffer
+    auto store_row = [&](int i, int j, float x) {
+      const uint32_t a = act_local + (j / C::kCK) * C::kChunkStride + ((((j % C::kCK) * C::kEB) >> 4) << 4) +
+                         ((j * C::kEB) & 15) + (i >> 3) * 1024 + ((((((j * C::kEB) >> 4) & 7) ^ (i & 7)) -
+                                                                    (((j * C::kEB) >> 4) & 7)) * 16 + (i & 7) * 128);
+      if constexpr (MODE == k3xTF32) {
+        const float h = to_tf32(x);
+        st_shared_f32(a, h);
+        st_shared_f32(a + C::kSplitStride, to_tf32(x - h));
+      } else {  // bf16x3 (the pair reverse variants are the split-precision modes)
+        const uint16_t h = bf16_rn_bits(x);
+        st_shared_u16(a, h);
+        st_shared_u16(a + C::kSplitStride, bf16_rn_bits(x - bf16_to_f32(h)));
+      }
+    };
+    // first production of a tile: value pass = layer 0 (CUDA cores, fp32), adjoint
+    // pass = W_L'[o, j]·σ'_H; each CTA writes every K-group for its OWN side's rows
+    // (local stores only). Rolled loops over the rows (one element each) keep the
+    // code (and the compile) small; this runs once per tile.
+    auto first_store = [&](long long tile) {
+      const long long nb = tile * (2 * pn) + static_cast<long long>(rank) * pn;
+#pragma unroll 1
+      for (int gi = 0; gi < kG0; ++gi) {
+        const int g = half + 2 * gi;
+        const int j = g * 128 + tid_h;
+        if constexpr (!kAdj) {
+          float w[kMaxIn2];
+#pragma unroll
+          for (int k = 0; k < kMaxIn2; ++k) w[k] = k < n_in ? __ldg(prm.w0t + k * WP + j) : 0.0f;
+          const float bj = __ldg(prm.b0 + j);
+#pragma unroll 1
+          for (int i = 0; i < ntc; ++i) {
+            const long long node = nb + i;
+            float val = 0.0f;
+            if (i < rows_used && node < K) {
+              float pre = bj;
+#pragma unroll
+              for (int k = 0; k < kMaxIn2; ++k)
+                if (k < n_in) pre = fmaf(w[k], static_cast<float>(load_z(prm, node, k)), pre);
+              float sp;
+              act_fwd(act, pre, val, sp);
+              *slope(0, node, j) = sp;
+            }
+            store_row(i, j, val);
+          }
+        } else {
+#pragma unroll 1
+          for (int i = 0; i < ntc; ++i) {
+            const int p = i / kRevOut, o = i - p * kRevOut;
+            const long long node = nb + p;
+            store_row(i, j, (i < rows_used && node < K) ? __ldg(prm.wl + o * WP + j) * __ldg(slope(n_mma, node, j)) : 0.0f);
+          }
+        }
+        publish_chunk(g, true);
+      }
+    };
+    // hidden block mb of MMA layer l: value pass y = σ(d + b) and σ' to the
+    // scratch; adjoint pass y = d·σ' (slopes of the side's nodes loaded before
+    // the accumulator wait)
+    auto do_block = [&](int mb, int l, long long tile) {
+      const int grp = 2 * mb + static_cast<int>(rank);
+      const int j = mb * 256 + static_cast<int>(rank) * 128 + tid_h;
+      const int li = kAdj ? n_mma - 1 - l : l + 1;
+      const long long nb = tile * (2 * pn) + static_cast<long long>(half) * pn;  // side `half`'s nodes
+      const uint32_t tsd = tmem_base + lane_base + mb * C::kBlkCols + half * ntc;
+      float sn[kAdj ? kAdjNodes : 1];
+      if constexpr (kAdj) {
+#pragma unroll
+        for (int p = 0; p < kAdjNodes; ++p) sn[p] = (p < pn && nb + p < K) ? __ldg(slope(li, nb + p, j)) : 0.0f;
+      }
+      const float bj = kAdj ? 0.0f : __ldg(prm.bh + l * WP + j);
+      mbar_wait_sleep(&tmem_full[mb], hl & 1);
+      tc_fence_after();
+      float v[NTC];
+      tmem_read_acc<C, NTC>(tsd, v, ntc, C::kN, C::kCorrOff);
+      tmem_release(mb);
+      if constexpr (!kAdj) {
+#pragma unroll 1
+        for (int i = 0; i < ntc; ++i) {  // rolled: the activation is not replicated NTC times
+          const long long node = nb + i;
+          float val = 0.0f, sp;
+          if (i < rows_used) {
+            act_fwd(act, v[i] + bj, val, sp);
+            if (node < K) *slope(li, node, j) = sp;
+          }
+          v[i] = val;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NTC; ++i) v[i] = i < rows_used ? v[i] * sn[i / kRevOut] : 0.0f;
+      }
+      mbar_wait_sleep(&in_free[grp], hl & 1);
+      store_publish([&](int i) { return v[i]; }, j, grp);
+    };
+    // outputs of a finished tile: this CTA's rows in its TMEM lanes
+    auto write_out = [&](long long tile) {
+      float o[C::kOutN];
+      tmem_read_acc<C, C::kOutN>(tmem_base + lane_base, o, C::kOutN, static_cast<uint32_t>(C::kOutN),
+                                 static_cast<uint32_t>(C::kOutN * C::kChains));
+      const int r = tid_h;
+      const long long nb = tile * (2 * pn) + static_cast<long long>(rank) * pn;
+      if (r < rows_used) {
+        if constexpr (!kAdj) {
+          const long long node = nb + r;
+          if (node < K) {
+            note_nonfinite(prm, o, n_out);
+            for (int oo = 0; oo < n_out; ++oo) prm.f[node * n_out + oo] = static_cast<double>(o[oo] + __ldg(prm.bl + oo));
+          }
+        } else {
+          const int p = r / kRevOut, oo = r - p * kRevOut;
+          const long long node = nb + p;
+          if (node < K) {
+            note_nonfinite(prm, o, n_in);
+            double* jr = prm.jac + (node * kRevOut + oo) * n_in;
+            for (int i = 0; i < n_in; ++i) jr[i] = static_cast<double>(o[i]);
+          }
+        }
+      }
+    };
+    long long prev_tile = -1;
+    for (long long tile = pair; tile < prm.num_tiles; tile += npairs, ++tiles_done) {
+      if (tiles_done > 0) {  // the previous tile's output MMAs have read the activation buffer
+        mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
+        tc_fence_after();
+        if (half == 0) write_out(prev_tile);
+        tmem_release(0);
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      first_store(tile);
+      for (int l = 0; l < n_mma_layers; ++l, ++hl)
+        for (int mb = 0; mb < NMB; ++mb) do_block(mb, l, tile);
+      prev_tile = tile;
+    }
+    if (tiles_done > 0) {
+      mbar_wait_sleep(tmem_last, (tiles_done - 1) & 1);
+      tc_fence_after();
+      if (half == 0) write_out(prev_tile);
     }
    } else {
     // ===================== order-1 epilogue ===================================

@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2203_07747_b200 import _lib, flops_per_node, make_mlp, synth_quad_nodes  # noqa: E402
 from paper_2203_07747_b200.errors import raise_for_status  # noqa: E402
 
-sizes = [17] + [512] * int(os.environ.get("DEPTH", "12")) + [int(os.environ.get("NOUT", "6"))]
+sizes = [17] + [int(os.environ.get("WIDTH", "512"))] * int(os.environ.get("DEPTH", "12")) + [int(os.environ.get("NOUT", "6"))]
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 409600
 prec = _lib.PRECISIONS.get(os.environ.get("PREC", "tf32"), None)
 prec = int(os.environ.get("PREC")) if prec is None else prec  # a name (tf32, bf16, ...) or the enum value

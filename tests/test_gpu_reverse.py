@@ -110,8 +110,8 @@ def test_jacobian_mode_api_errors_and_switching():
     raise_for_status(L.rtn_ctx_set_jacobian_mode(eng.ctx_ptr, 1))
     h = eng.prepare(z[:5], 2)
     assert np.isfinite(h.hessians).all()
-    for sizes, prec in (([17] + [256] * 3 + [6], "tf32"), ([17] + [512] * 3 + [6], "3xtf32"),
-                        ([30, 512, 512, 6], "tf32")):
+    for sizes, prec in (([17] + [256] * 3 + [6], "tf32"), ([17] + [512] * 3 + [3], "3xtf32"),
+                        ([30, 512, 512, 6], "tf32"), ([17] + [512] * 3 + [6], "bf16")):
         e2 = to_product_model(_net(sizes, "silu", 1.0)).engine(precision=_lib.PRECISIONS[prec])
         assert L.rtn_ctx_set_jacobian_mode(e2.ctx_ptr, 1) == _lib.RTN_EUNSUPPORTED, (sizes, prec)
 
@@ -130,3 +130,17 @@ def test_reverse_mode_latency_graphs_follow_the_mode():
     assert np.array_equal(b.jacobians, ref.jacobians)
     f, j, _ = om.batched_eval(z, 1)
     assert max_node_rel_error(a.jacobians, j) < 1e-3 and max_node_rel_error(b.jacobians, j) < 1e-3
+
+
+@pytest.mark.parametrize("prec,bound", [("3xtf32", 1e-5), ("bf16x3", 1e-4)])
+@pytest.mark.parametrize("width,depth,k", [(512, 12, 600), (256, 5, 2000), (512, 3, 97)])
+def test_reverse_mode_split_precision_on_pair_tiles(prec, bound, width, depth, k):
+    """3xTF32 / bf16x3 reverse mode (the pair kernel's value and adjoint variants,
+    fp32 slope scratch) on the conditioned nets of the forward-mode precision tests,
+    at the modes' bounds; ragged K and more nodes than one tile per CTA pair."""
+    om = _net([17] + [width] * depth + [6], "silu", 2.5 if depth == 12 else 2.0)
+    z = quad_nodes(13, k)
+    got = to_product_model(om).engine(precision=_lib.PRECISIONS[prec], jacobian_mode=1).prepare(z, 1)
+    f, j, _ = om.batched_eval(z, 1)
+    ef, ej = max_node_rel_error(got.values, f), max_node_rel_error(got.jacobians, j)
+    assert ef < bound and ej < bound, (prec, width, depth, ef, ej)
