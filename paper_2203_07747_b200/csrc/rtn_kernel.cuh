@@ -104,15 +104,15 @@ __device__ __forceinline__ float layer0_pre(float b, const float (&w)[kMaxIn0], 
 // (proj/src/neural.cpp:107-109); folding the mean into the fp32 layer-0 bias
 // instead (b0 − W0'·μ) cancels catastrophically for inputs far from zero
 // relative to in_scale, so only the 1/in_scale scaling is folded into W0'.
+// address of the raw (uncentred) element k of node z
+__device__ __forceinline__ const double* z_ptr(const KParams& prm, long long node, int k) {
+  if (prm.zx == nullptr) return prm.z + node * prm.n_in + k;
+  const long long xrow = node + node / prm.zN;  // inst·(N+1) + n
+  return k < 13 ? prm.zx + xrow * 13 + k : prm.zu + node * 4 + (k - 13);
+}
+__device__ __forceinline__ double load_z_raw(const KParams& prm, long long node, int k) { return *z_ptr(prm, node, k); }
 __device__ __forceinline__ double load_z(const KParams& prm, long long node, int k) {
-  double v;
-  if (prm.zx == nullptr) {
-    v = prm.z[node * prm.n_in + k];
-  } else {
-    const long long xrow = node + node / prm.zN;  // inst·(N+1) + n
-    v = k < 13 ? prm.zx[xrow * 13 + k] : prm.zu[node * 4 + (k - 13)];
-  }
-  return v - __ldg(prm.mu + k);
+  return load_z_raw(prm, node, k) - __ldg(prm.mu + k);
 }
 
 // Per-call NaN/Inf flag: a thread about to write the outputs o[0..n)

@@ -597,12 +597,17 @@ void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
       if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse adjoint pass: ") + cudaGetErrorString(e));
     } else {
       p.lo_rows = m->lo_rows;
+      const char* tp = std::getenv("RTN_TRACE_PASS");  // profiling aid: trace only this pass
+      const int trace_pass = tp ? std::atoi(tp) : 1;
+      unsigned long long* const trace = p.trace;
+      p.trace = trace_pass == 0 ? trace : nullptr;
       p.P = ntc;  // pass 0: one row per node, ntc nodes per CTA side
       p.nt = ntc;
       p.num_tiles = (n + 2 * ntc - 1) / (2 * ntc);
       int grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
       e = rtn::LaunchPairReverse(m->pair_mode, m->pair_wp, 0, p, m->tmap_h, m->tmap_l, grid, c->stream);
       if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse value pass: ") + cudaGetErrorString(e));
+      p.trace = trace_pass == 1 ? trace : nullptr;
       p.P = ntc / 6;  // pass 1: 6 adjoint rows per node
       p.nt = ((p.P * 6 + 7) / 8) * 8;
       p.num_tiles = (n + 2 * p.P - 1) / (2 * p.P);

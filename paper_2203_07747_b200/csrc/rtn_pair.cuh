@@ -58,6 +58,7 @@
 //                early and the MMA of the next layer resumes on them while the
 //                rest is in flight.
 #pragma once
+#include <type_traits>
 
 #include <cuda.h>
 
@@ -768,41 +769,90 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // pass = W_L'[o, j]·σ'_H; each CTA writes every K-group for its OWN side's rows
     // (local stores only). Rolled loops over the rows (one element each) keep the
     // code (and the compile) small; this runs once per tile.
+    // value pass: z rows of this CTA's nodes of `tile` into L1 (thread = row
+    // end: the first and last element's lines)
+    auto prefetch_z = [&](long long tile) {
+      if constexpr (!kAdj) {
+        const int t = half * 128 + tid_h, i = t >> 1;
+        const long long node = tile * (2 * pn) + static_cast<long long>(rank) * pn + i;
+        if (tile < prm.num_tiles && i < rows_used && node < K)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(z_ptr(prm, node, (t & 1) ? n_in - 1 : 0)));
+      }
+    };
     auto first_store = [&](long long tile) {
       const long long nb = tile * (2 * pn) + static_cast<long long>(rank) * pn;
-#pragma unroll 1
-      for (int gi = 0; gi < kG0; ++gi) {
-        const int g = half + 2 * gi;
-        const int j = g * 128 + tid_h;
-        if constexpr (!kAdj) {
-          float w[kMaxIn2];
+      if constexpr (!kAdj) {
+        // this thread's neurons j = g·128 + tid_h of the groups g = half + 2·gi;
+        // rows two at a time: 2·kG0 independent fma chains per shuffle of z
+        float w[kG0][kMaxIn2], bj[kG0];
 #pragma unroll
-          for (int k = 0; k < kMaxIn2; ++k) w[k] = k < n_in ? __ldg(prm.w0t + k * WP + j) : 0.0f;
-          const float bj = __ldg(prm.b0 + j);
-#pragma unroll 1
-          for (int i = 0; i < ntc; ++i) {
-            const long long node = nb + i;
-            float val = 0.0f;
-            if (i < rows_used && node < K) {
-              float pre = bj;
+        for (int gi = 0; gi < kG0; ++gi) {
+          const int j = (half + 2 * gi) * 128 + tid_h;
 #pragma unroll
-              for (int k = 0; k < kMaxIn2; ++k)
-                if (k < n_in) pre = fmaf(w[k], static_cast<float>(load_z(prm, node, k)), pre);
-              float sp;
-              act_fwd(act, pre, val, sp);
-              *slope(0, node, j) = sp;
+          for (int k = 0; k < kMaxIn2; ++k) w[gi][k] = k < n_in ? __ldg(prm.w0t + k * WP + j) : 0.0f;
+          bj[gi] = __ldg(prm.b0 + j);
+        }
+        // lane k holds z[node][k] (one coalesced load per row, raw and centred at
+        // use, the next row pair's loads in flight); the warp broadcasts it by
+        // shuffle. The rows were prefetched into L1 (prefetch_z): a cold z row
+        // costs ~1.5 us under the weight stream, once per row pair otherwise.
+        const double mu_l = lane < n_in ? __ldg(prm.mu + lane) : 0.0;
+        auto zlane = [&](int i) -> double {  // unconditional load (pads read μ)
+          const long long node = nb + i;
+          return *((lane < n_in && i < rows_used && node < K) ? z_ptr(prm, node, lane)
+                                                              : prm.mu + (lane < n_in ? lane : 0));
+        };
+        double zr0 = zlane(0), zr1 = zlane(1);
+        static_assert(NTC % 2 == 0, "rows in pairs");
+#pragma unroll 1
+        for (int i = 0; i < ntc; i += 2) {
+          const double zn0 = zlane(i + 2), zn1 = zlane(i + 3);
+          const float zk0 = static_cast<float>(zr0 - mu_l), zk1 = static_cast<float>(zr1 - mu_l);
+          float pre[2][kG0];
+#pragma unroll
+          for (int gi = 0; gi < kG0; ++gi) pre[0][gi] = pre[1][gi] = bj[gi];
+#pragma unroll
+          for (int k = 0; k < kMaxIn2; ++k) {
+            const float a0 = __shfl_sync(0xffffffffu, zk0, k), a1 = __shfl_sync(0xffffffffu, zk1, k);
+#pragma unroll
+            for (int gi = 0; gi < kG0; ++gi) {
+              pre[0][gi] = fmaf(w[gi][k], a0, pre[0][gi]);
+              pre[1][gi] = fmaf(w[gi][k], a1, pre[1][gi]);
             }
-            store_row(i, j, val);
           }
-        } else {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const long long node = nb + i + r;
+            const bool live = i + r < rows_used && node < K;
+#pragma unroll
+            for (int gi = 0; gi < kG0; ++gi) {
+              const int j = (half + 2 * gi) * 128 + tid_h;
+              float val = 0.0f, sp;
+              if (live) {
+                act_fwd(act, pre[r][gi], val, sp);
+                *slope(0, node, j) = sp;
+              }
+              store_row(i + r, j, val);
+            }
+          }
+          zr0 = zn0;
+          zr1 = zn1;
+        }
+#pragma unroll
+        for (int gi = 0; gi < kG0; ++gi) publish_chunk(half + 2 * gi, true);
+      } else {
+#pragma unroll 1
+        for (int gi = 0; gi < kG0; ++gi) {
+          const int g = half + 2 * gi;
+          const int j = g * 128 + tid_h;
 #pragma unroll 1
           for (int i = 0; i < ntc; ++i) {
             const int p = i / kRevOut, o = i - p * kRevOut;
             const long long node = nb + p;
             store_row(i, j, (i < rows_used && node < K) ? __ldg(prm.wl + o * WP + j) * __ldg(slope(n_mma, node, j)) : 0.0f);
           }
+          publish_chunk(g, true);
         }
-        publish_chunk(g, true);
       }
     };
     // hidden block mb of MMA layer l: value pass y = σ(d + b) and σ' to the
@@ -822,26 +872,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float bj = kAdj ? 0.0f : __ldg(prm.bh + l * WP + j);
       mbar_wait_sleep(&tmem_full[mb], hl & 1);
       tc_fence_after();
+      const bool tr = trace_on();
+      unsigned long long* tp = tr ? prm.trace + 48 + rank * 66 + (l * 2 + mb) * 3 : nullptr;
+      if (tr) tp[0] = globaltimer();
       float v[NTC];
       tmem_read_acc<C, NTC>(tsd, v, ntc, C::kN, C::kCorrOff);
       tmem_release(mb);
       if constexpr (!kAdj) {
-#pragma unroll 1
-        for (int i = 0; i < ntc; ++i) {  // rolled: the activation is not replicated NTC times
-          const long long node = nb + i;
-          float val = 0.0f, sp;
-          if (i < rows_used) {
-            act_fwd(act, v[i] + bj, val, sp);
-            if (node < K) *slope(li, node, j) = sp;
+        // unrolled over the rows (v stays in registers: a rolled loop would index
+        // it dynamically, i.e. put it in local memory, which spills to L2 with
+        // the shared-memory carve-out) with the activation switch hoisted
+        auto act_rows = [&](auto kact) {
+          constexpr int kAct = decltype(kact)::value;
+          float* sl = slope(li, nb, j);
+#pragma unroll
+          for (int i = 0; i < NTC; ++i) {
+            float val = 0.0f, sp;
+            if (i < rows_used) {
+              act_fwd(kAct, v[i] + bj, val, sp);
+              if (nb + i < K) sl[i * WP] = sp;
+            }
+            v[i] = val;
           }
-          v[i] = val;
-        }
+        };
+        if (act == 0) act_rows(std::integral_constant<int, 0>{});
+        else if (act == 1) act_rows(std::integral_constant<int, 1>{});
+        else act_rows(std::integral_constant<int, 2>{});
       } else {
 #pragma unroll
         for (int i = 0; i < NTC; ++i) v[i] = i < rows_used ? v[i] * sn[i / kRevOut] : 0.0f;
       }
+      if (tr) tp[1] = globaltimer();
       mbar_wait_sleep(&in_free[grp], hl & 1);
       store_publish([&](int i) { return v[i]; }, j, grp);
+      if (tr) tp[2] = globaltimer();
     };
     // outputs of a finished tile: this CTA's rows in its TMEM lanes
     auto write_out = [&](long long tile) {
@@ -877,9 +941,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_release(0);
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (trace_on()) prm.trace[192 + rank] = globaltimer();
+      if (tiles_done == 0) prefetch_z(tile);
       first_store(tile);
-      for (int l = 0; l < n_mma_layers; ++l, ++hl)
+      if (trace_on()) prm.trace[194 + rank] = globaltimer();
+      for (int l = 0; l < n_mma_layers; ++l, ++hl) {
+        if (l == n_mma_layers - 1) prefetch_z(tile + npairs);  // the next tile's z, a layer ahead
         for (int mb = 0; mb < NMB; ++mb) do_block(mb, l, tile);
+      }
       prev_tile = tile;
     }
     if (tiles_done > 0) {
