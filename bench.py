@@ -268,6 +268,28 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0, ac
                          "time": "device p50 (CUDA events)"}}
 
 
+def _mode(name):
+    """'<precision>[_reverse]' -> (precision name, reverse mode?)"""
+    return (name[:-len("_reverse")], True) if name.endswith("_reverse") else (name, False)
+
+
+def _reverse_fields(base, k, fl, sizes, ms, tf32_peak):
+    """Reverse mode's own FLOP basis: one value row + one adjoint row per output."""
+    fl_rev = fl * (1 + sizes[-1]) / (1 + sizes[0])
+    ach = k * fl_rev / (ms * 1e-3) / 1e12
+    passes = {"tf32": 1, "3xtf32": 3, "bf16x3": 1.5}[base]  # MMA passes at the TF32 rate
+    kern = ("rtn_rev_kernel pass 0 (values, sigma' to an HBM scratch) + pass 1 (adjoints, J), split-kernel schedule"
+            if base == "tf32" else
+            f"rtn_pair_kernel<{sizes[1] if sizes[1] > 256 else 256},..,{base},ORD2=3> (values, sigma' to an HBM "
+            f"scratch) + <..,ORD2=4> (adjoints, J)")
+    return {"achieved_tflops": ach, "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
+            "hardware_frac": passes * ach / tf32_peak if tf32_peak else None,
+            "hardware_frac_basis": "MMA passes x reverse-mode FLOPs vs the TF32 peak (bf16 MMAs run at 2x tf32)",
+            "flop_per_node": fl_rev, "flops_definition": "2*(1+n_out)*sum(n_l*n_{l+1}): the value row + one "
+                                                         "adjoint row per output (the reference's reverse sweep)",
+            "kernel": kern + "; rtn_ctx_set_jacobian_mode(ctx, 1)"}
+
+
 def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
     """Same workload in the split-precision modes (device-resident, 1 warm-up
     + `steps` timed launches each). Returns the timings and, per mode, a reader
@@ -278,10 +300,10 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
     L = _lib.lib()
     out, runs = {}, {}
     fl = flops_per_node(sizes, 1)
-    for name in ("bf16x3", "3xtf32", "bf16", "tf32_reverse"):
+    for name in ("bf16x3", "3xtf32", "bf16", "tf32_reverse", "3xtf32_reverse", "bf16x3_reverse"):
         m = make_mlp(sizes, "silu", "full", SEED)
-        reverse = name == "tf32_reverse"
-        eng = m.engine(precision=_lib.PRECISIONS["tf32" if reverse else name], jacobian_mode=1 if reverse else 0)
+        base, reverse = _mode(name)
+        eng = m.engine(precision=_lib.PRECISIONS[base], jacobian_mode=1 if reverse else 0)
         eng._ensure(k, 1)
         st = torch.cuda.Stream()
         raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
@@ -306,17 +328,8 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
                                 "bf16x3": "rtn_pair_kernel<512,4,4,80,bf16x3>",
                                 "bf16": "rtn_rowsb_kernel<8,SiLU> (one kind::f16 pass, whole layer input as the A "
                                         "operand in TMEM)"}.get(name, "")}
-        if reverse:  # its own FLOP basis: one value row + one adjoint row per output
-            fl_rev = fl * (1 + sizes[-1]) / (1 + sizes[0])
-            ach_rev = k * fl_rev / (ms * 1e-3) / 1e12
-            out[name].update({
-                "achieved_tflops": ach_rev, "frac_of_tf32_peak": ach_rev / tf32_peak if tf32_peak else None,
-                "hardware_frac": ach_rev / tf32_peak if tf32_peak else None,
-                "hardware_frac_basis": "reverse-mode FLOPs vs the TF32 peak",
-                "flop_per_node": fl_rev, "flops_definition": "2*(1+n_out)*sum(n_l*n_{l+1}): the value row + one "
-                                                             "adjoint row per output (the reference's reverse sweep)",
-                "kernel": "rtn_rev_kernel pass 0 (values, sigma' to an HBM scratch) + pass 1 (adjoints, J), "
-                          "split-kernel schedule; rtn_ctx_set_jacobian_mode(ctx, 1)"})
+        if reverse:
+            out[name].update(_reverse_fields(base, k, fl, sizes, ms, tf32_peak))
         if name == "bf16":
             try:
                 pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -344,9 +357,10 @@ def cfg4_bench(torch, tf32_peak, with_cpu=True, steps=5):
     f = torch.empty((k, 6), dtype=torch.float64, device="cuda")
     j = torch.empty((k, 6, 17), dtype=torch.float64, device="cuda")
     out = {"workload": "cfg4: 4096 instances x N=20 nodes, MLP 5x256 SiLU (17->6), order 1", "nodes": k}
-    for name in ("tf32", "3xtf32"):
+    for name in ("tf32", "3xtf32", "3xtf32_reverse"):
         m = make_mlp(sizes, "silu", "full", 5256)
-        eng = m.engine(precision=_lib.PRECISIONS[name])
+        base, reverse = _mode(name)
+        eng = m.engine(precision=_lib.PRECISIONS[base], jacobian_mode=1 if reverse else 0)
         eng._ensure(k, 1)
         st = torch.cuda.Stream()
         raise_for_status(L.rtn_ctx_set_stream(eng.ctx_ptr, C.c_void_p(st.cuda_stream)))
@@ -368,6 +382,8 @@ def cfg4_bench(torch, tf32_peak, with_cpu=True, steps=5):
                                 if name == "tf32" else "rtn_pair_kernel<256,4,4,80,3xTF32> (two main accumulators + corrections)"),
                      "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
                      "hardware_frac": (3 if name == "3xtf32" else 1) * ach / tf32_peak if tf32_peak else None}
+        if reverse:
+            out[name].update(_reverse_fields(base, k, fl, sizes, ms, tf32_peak))
         eng.close()
     if with_cpu:
         threads = os.cpu_count() or 1
@@ -589,11 +605,10 @@ def parity_leg(torch, eng_dev, z_dev, k, modes_engines, threads):
     for name, run in modes_engines.items():
         f, j = run(idx)
         e_bench = errs(f, j, f_ref, j_ref)
-        reverse = name == "tf32_reverse"
-        got = cm.engine(precision=_lib.PRECISIONS["tf32" if reverse else name],
-                        jacobian_mode=1 if reverse else 0).prepare(z_c, 1)
+        base, reverse = _mode(name)
+        got = cm.engine(precision=_lib.PRECISIONS[base], jacobian_mode=1 if reverse else 0).prepare(z_c, 1)
         e_cond = errs(got.values, got.jacobians, fc, jc)
-        bound = 1e-5 if name == "3xtf32" else 1e-3
+        bound = 1e-5 if base == "3xtf32" else 1e-3
         out[name] = {"bench_inputs": e_bench, "bench_inputs_max": max(e_bench.values()),
                      "conditioned_net": e_cond, "conditioned_net_max": max(e_cond.values()),
                      "north_star_bound": bound,
@@ -792,7 +807,8 @@ def run_ours(args, rank, world, local_rank):
                    "value_1thread": v_one, "sample_1thread": sample1, "cpu_model": cpu_model(),
                    "algorithm": "oracle/ restatement of proj/src/neural.cpp BatchedCore (reverse mode, fp64)"}
             if modes is not None:
-                order_ = {k_: mode_runs[k_] for k_ in ("tf32", "3xtf32", "bf16x3", "bf16", "tf32_reverse")}
+                order_ = {k_: mode_runs[k_] for k_ in ("tf32", "3xtf32", "bf16x3", "bf16", "tf32_reverse", "3xtf32_reverse",
+                                                  "bf16x3_reverse")}
                 parity = parity_leg(torch, eng, z, k, order_, threads)
         cfg4 = cfg4_bench(torch, tf32_peak, not args.no_cpu) if world == 1 and not args.no_modes else None
         blocks = None

@@ -554,15 +554,21 @@ Kern Choose(const rtn_model* m, long long K, int num_sms) {
   return Kern::kPair;
 }
 
-// Reverse mode (rtn_reverse.cuh): per chunk of at most kRevChunk nodes, the
-// value pass (f and the σ' scratch) then the adjoint pass (J).
-constexpr long long kRevChunk = 65536;
+// Reverse mode (rtn_reverse.cuh, rtn_pair.cuh ORD2 3/4): per chunk of nodes,
+// the value pass (f and the σ' scratch) then the adjoint pass (J). Chunks are
+// as large as a kRevScratchBytes scratch allows and of equal size (no short
+// last chunk leaving most CTA pairs idle).
+constexpr size_t kRevScratchBytes = size_t{2} << 30;
 void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
   const rtn_model* m = c->model;
   const bool split_sched = m->reverse_ok;  // TF32 width 512; else the pair-kernel variants
-  const long long R = std::min(K, kRevChunk);
   // scratch: fp16 slopes (split schedule) / fp32 slopes (pair variants: the split-precision modes)
-  const size_t need = static_cast<size_t>(m->n_hidden) * static_cast<size_t>(R) * m->pair_wp * (split_sched ? 2 : 4);
+  const size_t per_node = static_cast<size_t>(m->n_hidden) * m->pair_wp * (split_sched ? 2 : 4);
+  long long r_max = std::max<long long>(1024, static_cast<long long>(kRevScratchBytes / per_node));
+  if (const char* ch = std::getenv("RTN_REV_CHUNK")) r_max = std::max(1LL, std::atoll(ch));  // tests: force chunking
+  const long long n_chunks = (K + r_max - 1) / r_max;
+  const long long R = (K + n_chunks - 1) / n_chunks;
+  const size_t need = per_node * static_cast<size_t>(R);
   if (need > c->rev_s_cap) {
     CUDA_CHECK(cudaStreamSynchronize(c->stream));
     cudaFree(c->d_rev_s);

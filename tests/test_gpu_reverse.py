@@ -5,6 +5,7 @@ layer's slope in an HBM scratch, then one adjoint row per output. Checked
 against the fp64 oracle in the reference metric (proj/tests/oracles.hpp:30-32)
 with the TF32 tolerances of the forward-mode tests, and against forward mode."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -66,12 +67,18 @@ def test_reverse_mode_shapes(sizes, act):
 
 
 def test_reverse_mode_chunked_and_documented_limit():
-    """More nodes than one scratch chunk (65,536): every chunk's J; and the
-    |J| ~ 2 edge-of-stability net, where TF32 (either algorithm) reaches ~3e-3."""
+    """More nodes than one scratch chunk (forced to 65,536 by RTN_REV_CHUNK; the
+    default is a 2 GiB scratch in equal chunks): every chunk's J; and the |J| ~ 2
+    edge-of-stability net, where TF32 (either algorithm) reaches ~3e-3."""
     om = _net([17] + [512] * 4 + [6], "silu", 1.5)
     z = quad_nodes(5, 70000)
-    got = to_product_model(om).engine(jacobian_mode=1).prepare(z, 1)
-    idx = np.unique(np.concatenate([np.arange(0, 70000, 997), np.arange(65530, 65542), [69999]]))
+    os.environ["RTN_REV_CHUNK"] = "65536"
+    try:
+        got = to_product_model(om).engine(jacobian_mode=1).prepare(z, 1)
+    finally:
+        del os.environ["RTN_REV_CHUNK"]
+    # 70,000 nodes in two equal chunks of 35,000
+    idx = np.unique(np.concatenate([np.arange(0, 70000, 997), np.arange(34995, 35005), [69999]]))
     f, j, _ = om.batched_eval(z[idx], 1)
     assert max_node_rel_error(got.jacobians[idx], j) < 1e-3
     assert max_node_rel_error(got.values[idx], f) < 1e-3
@@ -144,3 +151,19 @@ def test_reverse_mode_split_precision_on_pair_tiles(prec, bound, width, depth, k
     f, j, _ = om.batched_eval(z, 1)
     ef, ej = max_node_rel_error(got.values, f), max_node_rel_error(got.jacobians, j)
     assert ef < bound and ej < bound, (prec, width, depth, ef, ej)
+
+
+@pytest.mark.parametrize("prec", ["3xtf32", "bf16x3"])
+def test_reverse_pair_chunking_is_bitwise_neutral(prec):
+    """Scratch chunking of the pair-kernel reverse passes (forced small by
+    RTN_REV_CHUNK: 7 equal chunks of 286 nodes) gives the same bits as one chunk."""
+    om = _net([17] + [256] * 5 + [6], "silu", 2.0)
+    z = quad_nodes(17, 2000)
+    pm = to_product_model(om)
+    one = pm.engine(precision=_lib.PRECISIONS[prec], jacobian_mode=1).prepare(z, 1)
+    os.environ["RTN_REV_CHUNK"] = "300"
+    try:
+        many = pm.engine(precision=_lib.PRECISIONS[prec], jacobian_mode=1).prepare(z, 1)
+    finally:
+        del os.environ["RTN_REV_CHUNK"]
+    assert np.array_equal(one.values, many.values) and np.array_equal(one.jacobians, many.jacobians)
