@@ -122,7 +122,8 @@ rtn_status rtn_ctx_nonfinite(rtn_ctx* c, int* flag, int reset);
  * 1 + n_in rows per node), 1 = reverse mode (the reference's own adjoint sweep,
  * neural.cpp:132-163: a value pass that keeps every layer's slope in an HBM
  * scratch, then 1 adjoint row per output: 1 + n_out rows per node). Reverse
- * mode needs a TF32 model of padded width 512 with n_in <= 24
+ * mode needs n_in <= 24 and either a TF32 model of padded width 512, or a
+ * 3xTF32 / bf16x3 model of padded width 256 or 512 with n_out = 6
  * (RTN_EUNSUPPORTED otherwise); order 0 and 2 calls are unaffected. */
 rtn_status rtn_ctx_set_jacobian_mode(rtn_ctx* c, int mode);
 
