@@ -28,7 +28,7 @@ for l in range(11):
     nxt = ((t[l + 1, 0] - t[l, 4]) / 1e3) if l < 10 else float("nan")
     print(f"L{l + 1:2d}: " + " ".join(f"{x:8.2f}" for x in r) + " | " + " ".join(f"{x:5.2f}" for x in d) +
           f" | gap to next layer {nxt:5.2f}")
-if os.environ.get("RTN_DEBUG", "0") == "0":
+if not int(os.environ.get("RTN_DEBUG", "0")) & 128:
     e = np.array(buf[64:174], dtype=np.float64).reshape(11, 10)
     print("epilogue CTA0 (us from layer-1 B0 issue): B0 seen/done, B1 seen/done, B2 seen/done, s_free seen, S stored, B3 seen/done")
     for l in range(11):
