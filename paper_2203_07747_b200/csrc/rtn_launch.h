@@ -2,6 +2,7 @@
 // per precision mode (rtn_pair_{tf32,3xtf32,bf16x3,order2}.cu) so they compile
 // in parallel; rtn_mpc.cu dispatches.
 #pragma once
+#include <cstdlib>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -78,7 +79,14 @@ cudaError_t LaunchReverse(int pass, const KParams& prm, const CUtensorMap& ta, c
 // (pass 1), tl = output pack (pass 0) or W0' padded to 32 rows (pass 1).
 cudaError_t LaunchPairReverse(int mode, int wp, int pass, const KParams& prm, const CUtensorMap& th,
                               const CUtensorMap& tl, int grid, cudaStream_t st);
-inline int PairReverseNtc(int mode, int wp) { return (mode == k3xTF32 && wp == 512) ? 24 : 80; }
+// rows per CTA side of the pair reverse passes
+inline int PairReverseNtc(int mode, int wp, int pass) {
+  if (mode == k3xTF32 && wp == 512) {
+    static const bool adj24 = std::getenv("RTN_REV_ADJ24") != nullptr;  // A/B switch
+    return pass == 1 && !adj24 ? 40 : 24;
+  }
+  return 80;
+}
 // BF16 width-512 throughput, the whole layer input as the A operand in TMEM
 // (rtn_rowsb.cuh); 15 <= n_in <= 31.
 cudaError_t LaunchRowsBF16(const KParams& prm, const CUtensorMap& th64, const CUtensorMap& tl, int grid,

@@ -578,7 +578,7 @@ void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
     c->rev_s_cap = need;
   }
   const int n_in = m->n_in, n_out = m->n_out;
-  const int ntc = rtn::PairReverseNtc(m->pair_mode, m->pair_wp);
+  const int ntc = rtn::PairReverseNtc(m->pair_mode, m->pair_wp, 0), ntc1 = rtn::PairReverseNtc(m->pair_mode, m->pair_wp, 1);
   for (long long lo = 0; lo < K; lo += R) {
     const long long n = std::min(R, K - lo);
     rtn::KParams p = base;
@@ -614,8 +614,8 @@ void EnqueueReverse(rtn_ctx* c, const rtn::KParams& base, long long K) {
       e = rtn::LaunchPairReverse(m->pair_mode, m->pair_wp, 0, p, m->tmap_h, m->tmap_l, grid, c->stream);
       if (e != cudaSuccess) throw Error(RTN_ECUDA, std::string("reverse value pass: ") + cudaGetErrorString(e));
       p.trace = trace_pass == 1 ? trace : nullptr;
-      p.P = ntc / 6;  // pass 1: 6 adjoint rows per node
-      p.nt = ((p.P * 6 + 7) / 8) * 8;
+      p.P = ntc1 / 6;  // pass 1: 6 adjoint rows per node
+      p.nt = ntc1;
       p.num_tiles = (n + 2 * p.P - 1) / (2 * p.P);
       grid = 2 * static_cast<int>(std::min<long long>(p.num_tiles, c->num_sms / 2));
       e = rtn::LaunchPairReverse(m->pair_mode, m->pair_wp, 1, p, m->tmap_ht, m->tmap_w0p, grid, c->stream);

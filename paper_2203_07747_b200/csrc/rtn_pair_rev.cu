@@ -10,7 +10,8 @@ cudaError_t LaunchPairReverse(int mode, int wp, int pass, const KParams& prm, co
   if (mode == k3xTF32) {
     if (wp == 512)
       return pass == 0 ? LaunchPairT<512, 8, 1, 24, k3xTF32, 3>(prm, th, tl, grid, st)
-                       : LaunchPairT<512, 8, 1, 24, k3xTF32, 4>(prm, th, tl, grid, st);
+                       : (prm.nt == 40 ? LaunchPairT<512, 4, 1, 40, k3xTF32, 4>(prm, th, tl, grid, st)
+                                       : LaunchPairT<512, 8, 1, 24, k3xTF32, 4>(prm, th, tl, grid, st));
     return pass == 0 ? LaunchPairT<256, 4, 1, 80, k3xTF32, 3>(prm, th, tl, grid, st)
                      : LaunchPairT<256, 4, 1, 80, k3xTF32, 4>(prm, th, tl, grid, st);
   }

@@ -1,6 +1,6 @@
 """Summarise an ncu report: key raw metrics + top stall / instruction hot spots.
 
-usage: python scripts/ncu_analyze.py <report.ncu-rep> [top]
+usage: python scripts/ncu_analyze.py <report.ncu-rep> [top] [mangled-name regex: one kernel of a multi-kernel report]
 """
 import csv
 import io
@@ -9,10 +9,11 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+filt = ["--kernel-name-base", "mangled", "-k", f"regex:{sys.argv[3]}"] if len(sys.argv) > 3 else []
 
 
 def ncu(*args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *filt, *args], capture_output=True, text=True).stdout
 
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
@@ -31,8 +32,11 @@ for w in want:
         print(f"  {w:70s} {vals[i]:>20s} {units[i]}")
 
 rows = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source=sass"))))
-h = rows[1]
-data = rows[2:]
+# a multi-kernel report prints one block per kernel ("Kernel Name" line, header, rows): keep the first
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+h = rows[starts[0] + 1]
+data = rows[starts[0] + 2:starts[1]]
+print("source page of:", rows[starts[0]][1][:100])
 i_s = h.index("Warp Stall Sampling (All Samples)")
 i_e = h.index("Instructions Executed")
 tot_s = sum(float(r[i_s] or 0) for r in data) or 1
