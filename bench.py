@@ -262,7 +262,7 @@ def latency(torch, sizes, seed, k, steps=1000, warm=50, order=1, precision=0, ac
     ach = fl / (d50 * 1e-6) / 1e12
     return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99)], "device_p50_us": d50,
             "device_p99_us": dev[int(len(dev) * 0.99)], "steps": steps, "nodes": k, "order": order,
-            "precision": ["tf32", "3xtf32", "bf16x3", "bf16"][precision],
+            "precision": {v: nm for nm, v in _lib.PRECISIONS.items()}[precision],
             "roofline": {"bound": "tensor (serial layer chain)", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                          "frac": ach / tf32_peak if tf32_peak else None, "flop_per_step": fl,
                          "time": "device p50 (CUDA events)"}}
