@@ -322,7 +322,7 @@ def precision_modes(torch, z, k, sizes, tf32_peak=None, steps=2):
         ach = k * fl / (ms * 1e-3) / 1e12
         out[name] = {"value": k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "achieved_tflops": ach,
                      "frac_of_tf32_peak": ach / tf32_peak if tf32_peak else None,
-                     "hardware_frac": ((3 if name != "bf16" else 0.5) * ach / tf32_peak) if tf32_peak else None,
+                     "hardware_frac": ({"3xtf32": 3, "bf16x3": 1.5, "bf16": 0.5}.get(base, 1) * ach / tf32_peak) if tf32_peak else None,
                      "hardware_frac_basis": "MMA passes x algorithmic FLOPs vs the TF32 peak (bf16 MMAs run at 2x tf32)",
                      "kernel": {"3xtf32": "rtn_pair_kernel<512,8,1,24,3xTF32> (four main accumulators)",
                                 "bf16x3": "rtn_pair_kernel<512,4,4,80,bf16x3>",
