@@ -841,15 +841,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int gi = 0; gi < kG0; ++gi) publish_chunk(half + 2 * gi, true);
       } else {
+        // row (node p, output o) = W_L'[o, j]·σ'_H[node p, j]: the 6 weights and the
+        // side's slopes are loaded up front (one round trip, not one per row)
 #pragma unroll 1
         for (int gi = 0; gi < kG0; ++gi) {
           const int g = half + 2 * gi;
           const int j = g * 128 + tid_h;
-#pragma unroll 1
-          for (int i = 0; i < ntc; ++i) {
-            const int p = i / kRevOut, o = i - p * kRevOut;
-            const long long node = nb + p;
-            store_row(i, j, (i < rows_used && node < K) ? __ldg(prm.wl + o * WP + j) * __ldg(slope(n_mma, node, j)) : 0.0f);
+          float wlo[kRevOut], sl[kAdjNodes];
+#pragma unroll
+          for (int o = 0; o < kRevOut; ++o) wlo[o] = __ldg(prm.wl + o * WP + j);
+#pragma unroll
+          for (int p = 0; p < kAdjNodes; ++p) sl[p] = (p < pn && nb + p < K) ? __ldg(slope(n_mma, nb + p, j)) : 0.0f;
+#pragma unroll
+          for (int i = 0; i < NTC; ++i) {
+            if ((i & ~7) >= ntc) continue;
+            store_row(i, j, i < rows_used ? wlo[i % kRevOut] * sl[i / kRevOut] : 0.0f);
           }
           publish_chunk(g, true);
         }
