@@ -829,7 +829,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const int j = (half + 2 * gi) * 128 + tid_h;
               float val = 0.0f, sp;
               if (live) {
-                act_fwd(act, pre[r][gi], val, sp);
+                act_fwd_rows(act, pre[r][gi], val, sp);
                 *slope(0, node, j) = sp;
               }
               store_row(i + r, j, val);
@@ -895,7 +895,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < NTC; ++i) {
             float val = 0.0f, sp;
             if (i < rows_used) {
-              act_fwd(kAct, v[i] + bj, val, sp);
+              act_fwd_rows(kAct, v[i] + bj, val, sp);
               if (nb + i < K) sl[i * WP] = sp;
             }
             v[i] = val;
