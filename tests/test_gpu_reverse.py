@@ -167,3 +167,16 @@ def test_reverse_pair_chunking_is_bitwise_neutral(prec):
     finally:
         del os.environ["RTN_REV_CHUNK"]
     assert np.array_equal(one.values, many.values) and np.array_equal(one.jacobians, many.jacobians)
+
+
+@pytest.mark.parametrize("prec,bound", [("3xtf32", 1e-5), ("bf16x3", 1e-4)])
+@pytest.mark.parametrize("n_in,width", [(3, 256), (24, 256), (9, 512), (24, 512)])
+def test_reverse_pair_input_widths(prec, bound, n_in, width):
+    """Pair-kernel reverse passes at the input widths the adjoint's 32-column W0'
+    output covers (n_in <= 24), both padded widths, 6 outputs; ragged K."""
+    om = _net([n_in] + [width] * 4 + [6], "silu", 2.0)
+    z = _z(n_in, 333, n_in)
+    got = to_product_model(om).engine(precision=_lib.PRECISIONS[prec], jacobian_mode=1).prepare(z, 1)
+    f, j, _ = om.batched_eval(z, 1)
+    ef, ej = max_node_rel_error(got.values, f), max_node_rel_error(got.jacobians, j)
+    assert ef < bound and ej < bound, (prec, n_in, width, ef, ej)
