@@ -180,3 +180,18 @@ def test_reverse_pair_input_widths(prec, bound, n_in, width):
     f, j, _ = om.batched_eval(z, 1)
     ef, ej = max_node_rel_error(got.values, f), max_node_rel_error(got.jacobians, j)
     assert ef < bound and ej < bound, (prec, n_in, width, ef, ej)
+
+
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32", "bf16x3"])
+def test_reverse_empty_and_single_node(prec):
+    """K = 0 launches nothing and returns empty blocks; K = 1 matches the oracle
+    (the reference's single-input contract, proj/src/neural.cpp:300-318)."""
+    om = _net([17] + [512] * 3 + [6], "silu", 2.0)
+    eng = to_product_model(om).engine(precision=_lib.PRECISIONS[prec], jacobian_mode=1)
+    z = quad_nodes(3, 1)
+    empty = eng.prepare(z[:0], 1)
+    assert empty.values.shape == (0, 6) and empty.jacobians.shape == (0, 6, 17)
+    one = eng.prepare(z, 1)
+    f, j, _ = om.batched_eval(z, 1)
+    bound = 1e-5 if prec == "3xtf32" else 1e-3
+    assert max_node_rel_error(one.values, f) < bound and max_node_rel_error(one.jacobians, j) < bound
